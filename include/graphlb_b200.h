@@ -1,0 +1,190 @@
+/*
+ * graphlb_b200.h -- C-ABI of libgraphlb_b200.so, the sm_100a implementation of
+ * the BFS/SSSP task-distribution hot path of `graphlb` (arXiv 1711.00231).
+ *
+ * Every entry point is `extern "C"`, takes plain pointers and sizes, and returns
+ * an int status (GLB_OK == 0).  On failure a thread-local message is available
+ * from glb_last_error().  Host arrays are always the reference's int64 layout
+ * (graphlb/csr.py:16-21 INDEX_DTYPE = np.int64); the library narrows them on the
+ * device and owns all device memory.
+ *
+ * Reference interfaces each entry point replaces (paths under
+ * /root/reference/pkg/src/graphlb/):
+ *   glb_graph_create     CsrGraph.__post_init__/_validate       csr.py:55-85
+ *                        (+ the per-run `.tolist()` of csr_locals, strategies/common.py:73-82)
+ *   glb_run              run_strategy                           strategies/__init__.py:17-41
+ *                        run_bs / run_ep / run_wd / run_ns / run_hp
+ *                        node_based.py:19, edge_based.py:31, workload.py:162,
+ *                        splitting.py:102, hierarchical.py:27
+ *   glb_histogram        build_histogram + compute_mdt          degrees.py:45-76
+ *   glb_degree_stats     degree_stats                           degrees.py:27-32
+ *   glb_split_graph      split_graph                            strategies/splitting.py:58-99
+ *   glb_csr_to_coo       csr_to_coo                             csr.py:155-170
+ *   glb_inclusive_scan   inclusive_scan                         scan.py:19-65
+ *   glb_find_offsets     find_offsets                           strategies/workload.py:45-72
+ *
+ * Status -> Python exception mapping used by the drop-in package:
+ *   GLB_EINVAL -> ValueError, GLB_ERANGE -> IndexError, GLB_EOVERFLOW -> OverflowError,
+ *   GLB_ECOO_CAPACITY -> StrategyRun(status="infeasible: memory") (never raised),
+ *   GLB_ECUDA / GLB_ENODEV / GLB_ENOMEM -> RuntimeError.
+ */
+#ifndef GRAPHLB_B200_H
+#define GRAPHLB_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GLB_OK 0
+#define GLB_EINVAL 1
+#define GLB_ERANGE 2
+#define GLB_ECOO_CAPACITY 3
+#define GLB_ECUDA 4
+#define GLB_ENOMEM 5
+#define GLB_EOVERFLOW 6
+#define GLB_ENODEV 7
+
+/* strategy ids (STRATEGY_TAGS order, strategies/__init__.py:14) */
+#define GLB_BS 0
+#define GLB_EP 1
+#define GLB_WD 2
+#define GLB_NS 3
+#define GLB_HP 4
+/* record tag for hierarchical.py:24 FALLBACK_TAG = "WD-fallback" */
+#define GLB_TAG_WD_FALLBACK 5
+
+/* RelaxOp kinds (strategies/common.py:23-42) */
+#define GLB_BFS 0
+#define GLB_SSSP 1
+
+/* host loop driving the device iterations */
+#define GLB_LOOP_HOST 0  /* one host round trip per launch (exact per-launch records) */
+#define GLB_LOOP_GRAPH 1 /* device-driven: CUDA graph with a conditional WHILE node */
+
+typedef struct glb_graph glb_graph;
+
+typedef struct glb_run_params {
+  int32_t strategy;        /* GLB_BS..GLB_HP */
+  int32_t algo;            /* GLB_BFS / GLB_SSSP */
+  int64_t source;          /* 0 <= source < n else GLB_EINVAL (common.py:68-70) */
+  int32_t bins;            /* histogram bins for NS/HP MDT (default 10) */
+  int32_t chunked;         /* EP work chunking (edge_based.py:81-85) */
+  int64_t mdt;             /* <= 0: compute_mdt(build_histogram(g, bins)) */
+  int64_t max_cells;       /* EP COO cell budget (csr.py:16-18) */
+  int32_t block_size;      /* KernelConfig.block_size: HP fallback threshold (hierarchical.py:49) */
+  int32_t hp_fallback;     /* run_hp(fallback=...) */
+  int64_t virtual_threads; /* KernelConfig.virtual_threads (0 = auto); reported only */
+  int32_t dist_bits;       /* 0 = auto (u32, re-run in u64 on overflow), 32, 64 */
+  int32_t loop_mode;       /* GLB_LOOP_HOST / GLB_LOOP_GRAPH */
+  int32_t record_timing;   /* per-launch CUDA event timing into records */
+  int32_t reserved;
+} glb_run_params;
+
+typedef struct glb_run_stats {
+  int32_t status;          /* GLB_OK or GLB_ECOO_CAPACITY (EP infeasible) */
+  int32_t dist_bits;       /* distance width actually used */
+  int64_t iterations;      /* super-iterations */
+  int64_t launches;        /* relax-kernel invocations (one MetricsRecord each) */
+  int64_t sub_iterations;  /* HP sub-iteration launches */
+  int64_t relax_ops;       /* atomic_relax_min calls (engine.py:120-139) */
+  int64_t push_ops;        /* successful worklist reservations (worklist.py:84-130) */
+  int64_t edges_examined;  /* sum of per-thread work */
+  int64_t active_items;    /* sum over launches of worklist sizes */
+  int64_t mdt;             /* threshold used by NS/HP, else 0 */
+  int64_t num_split_nodes; /* NS */
+  int64_t num_children;    /* NS */
+  double split_fraction;   /* NS split fraction (splitting.py:44-50), else -1 */
+  double device_ms;        /* CUDA-event time of the whole run on the library stream */
+  double kernel_ms;        /* sum of relax-kernel event times (record_timing=1) */
+  double overhead_ms;      /* device time outside relax kernels (scan/split/coo/init) */
+  double setup_ms;         /* per-run preprocessing (histogram, split, coo, init) */
+  int64_t n_records;       /* records produced (may exceed the caller's capacity) */
+} glb_run_stats;
+
+/* One kernel invocation, mirroring MetricsRecord (engine.py:142-174).
+ * per_thread_work is summarised on device (sum / sum of squares / max). */
+typedef struct glb_record {
+  int32_t iteration;
+  int32_t sub_iteration;   /* -1 = None */
+  int32_t tag;             /* GLB_BS..GLB_HP or GLB_TAG_WD_FALLBACK */
+  int32_t reserved;
+  int64_t active_items;
+  int64_t threads;
+  int64_t work_total;
+  int64_t work_max;
+  double work_sumsq;
+  int64_t relax_ops;
+  int64_t push_ops;
+  double kernel_ms;
+  double overhead_ms;
+} glb_record;
+
+/* ---- library / device ---- */
+const char* glb_last_error(void);
+const char* glb_version(void);
+int glb_device_count(int* count);
+
+/* ---- graph (csr.py:42-118) ---- */
+/* Copies the host CSR (int64 row_offsets[n+1], col[m], weights[m] or NULL) into
+ * HBM on `device`, narrowing col/weights to 32 bits on the device.  Validates
+ * the CsrGraph invariants (csr.py:66-85); weights must be < 2^32. */
+int glb_graph_create(const int64_t* row_offsets, const int64_t* col,
+                     const int64_t* weights_or_null, int64_t n, int64_t m,
+                     int device, glb_graph** out);
+int glb_graph_destroy(glb_graph* g);
+int glb_graph_info(const glb_graph* g, int64_t* n, int64_t* m, int* weighted,
+                   int* device);
+/* cudaStream_t of the graph's library stream (for event timing by callers) */
+int glb_graph_stream(const glb_graph* g, void** stream);
+
+/* ---- strategies (strategies/__init__.py:17-41) ---- */
+/* dist_out: caller-allocated int64[n]; INF is INT64_MAX (engine.py:27).
+ * records may be NULL; *n_records is the capacity on input (ignored when
+ * records is NULL) and stats->n_records the produced count on output.
+ * EP over the COO budget returns GLB_OK with stats->status = GLB_ECOO_CAPACITY
+ * and leaves dist_out untouched (edge_based.py:41-46). */
+int glb_run(glb_graph* g, const glb_run_params* params, int64_t* dist_out,
+            glb_run_stats* stats, glb_record* records, int64_t records_capacity);
+
+/* Records of the graph's most recent glb_run, from `offset` on (for callers
+ * whose capacity was too small); *written receives the count copied. */
+int glb_run_records(glb_graph* g, int64_t offset, glb_record* records,
+                    int64_t capacity, int64_t* written);
+
+/* ---- degree analysis (degrees.py) ---- */
+int glb_degree_stats(glb_graph* g, int64_t* max_degree, int64_t* sum_degree,
+                     double* sum_sq_degree);
+/* counts: caller-allocated int64[bins] (1-based bin b at counts[b-1]) */
+int glb_histogram(glb_graph* g, int bins, int64_t* counts, int64_t* max_degree,
+                  int32_t* arg_max_bin, int64_t* mdt);
+
+/* ---- node splitting (splitting.py:58-99) ----
+ * Two-call protocol: call with new_row_offsets == NULL to get *new_n and
+ * *num_children; then call again with buffers of int64 [new_n+1], [m], [m]
+ * (weights, ignored when unweighted), [num_children], [n+1]. */
+int glb_split_graph(glb_graph* g, int64_t mdt, int64_t* new_n,
+                    int64_t* num_children, int64_t* new_row_offsets,
+                    int64_t* new_col, int64_t* new_weights, int64_t* parent_of,
+                    int64_t* children_start);
+
+/* ---- COO expansion (csr.py:155-170) ----
+ * Returns GLB_ECOO_CAPACITY when (3 if weighted else 2) * m > max_cells.
+ * src_out: int64[m] (dst/weights are the CSR arrays, copied by the caller). */
+int glb_csr_to_coo(glb_graph* g, int64_t max_cells, int64_t* src_out);
+
+/* ---- device primitives on host arrays (scan.py, workload.py) ---- */
+/* out[i] = values[0] + ... + values[i]; GLB_EOVERFLOW past int64. */
+int glb_inclusive_scan(const int64_t* values, int64_t n, int64_t* out, int device);
+/* Per-thread (worklist index, edge offset) by binary search of the inclusive
+ * prefix (workload.py:45-72); idle threads get node_off = -1, edge_off = 0. */
+int glb_find_offsets(const int64_t* prefix, int64_t size, int64_t edges_per_thread,
+                     int64_t threads, int64_t* node_off, int64_t* edge_off,
+                     int device);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* GRAPHLB_B200_H */

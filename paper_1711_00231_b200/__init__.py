@@ -1,0 +1,61 @@
+"""paper_1711_00231_b200: B200-native BFS/SSSP task-distribution strategies.
+
+Drop-in for the hot path of the reference package ``graphlb`` (arXiv
+1711.00231, graphlb/__init__.py:11-57): the same public names for graph
+construction, degree analysis, node splitting, workload decomposition and the
+five strategies (BS, EP, WD, NS, HP), executed by hand-written sm_100a CUDA
+kernels in libgraphlb_b200.so through a C-ABI (include/graphlb_b200.h).
+
+Not provided here (outside the hot path): the CPU launch emulation
+(launch_kernel, ThreadCtx, Worklist, atomic_relax_min), the sequential oracles
+(they live in oracle/ as test infrastructure), file loaders, reports and CLI.
+"""
+
+from .analysis import (
+    DegreeHistogram,
+    DegreeStats,
+    VerificationReport,
+    build_histogram,
+    compute_mdt,
+    degree_stats,
+    inclusive_scan,
+    verify,
+)
+from .graph import (
+    COO_ID_BYTES,
+    DEFAULT_COO_BUDGET_BYTES,
+    DEFAULT_COO_BUDGET_CELLS,
+    DEFAULT_MAX_WEIGHT,
+    DEFAULT_RMAT_PARAMS,
+    CooCapacityError,
+    CooGraph,
+    CsrGraph,
+    csr_to_coo,
+    generate_er,
+    generate_rmat,
+    graph_from_degrees,
+    grid_graph,
+    path_graph,
+    ring_graph,
+    star_graph,
+)
+from .runtime import INF, DistArray, KernelConfig, KernelLaunchError, MetricsRecord, resolve_threads
+from .strategies import (
+    FALLBACK_TAG,
+    INFEASIBLE_MEMORY,
+    STRATEGY_TAGS,
+    OffsetTable,
+    RelaxOp,
+    SplitGraph,
+    StrategyRun,
+    find_offsets,
+    run_bs,
+    run_ep,
+    run_hp,
+    run_ns,
+    run_strategy,
+    run_wd,
+    split_graph,
+)
+
+__version__ = "0.1.0"

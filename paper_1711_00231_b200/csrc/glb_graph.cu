@@ -1,0 +1,928 @@
+// glb_graph.cu -- graph upload (CsrGraph, csr.py:42-118), degree analysis
+// (degrees.py:27-76), COO expansion (csr.py:155-170), node splitting
+// (splitting.py:58-99) and the device primitives behind inclusive_scan
+// (scan.py:19-65) and find_offsets (workload.py:45-72).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <mutex>
+#include <thread>
+#include <vector>
+
+#include "glb_internal.cuh"
+#include "glb_scan.cuh"
+
+namespace glb {
+
+// ======================================================== error plumbing ===
+static thread_local std::string g_last_error;
+void set_error(const std::string& msg) { g_last_error = msg; }
+const char* last_error() { return g_last_error.c_str(); }
+
+void* ensure(DevBuf& b, size_t bytes) {
+  if (bytes == 0) bytes = 16;
+  if (b.bytes >= bytes) return b.p;
+  if (b.p) GLB_CUDA_TRY(cudaFree(b.p));
+  b.p = nullptr;
+  b.bytes = 0;
+  GLB_CUDA_TRY(cudaMalloc(&b.p, bytes));
+  b.bytes = bytes;
+  return b.p;
+}
+
+void free_buf(DevBuf& b) {
+  if (b.p) cudaFree(b.p);
+  b.p = nullptr;
+  b.bytes = 0;
+}
+
+int max_resident_blocks(const void* kernel, int block, size_t smem, int num_sms) {
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, block, smem) != cudaSuccess ||
+      per_sm < 1)
+    per_sm = 1;
+  return per_sm * num_sms;
+}
+
+// ========================================================== graph upload ===
+// Narrow int64 -> uint32 with 128-bit loads (two int64 per ld.v2.s64) and a
+// range check [0, limit); any violation sets *bad.
+__global__ void k_narrow_u32(const long long* __restrict__ src, uint32_t* __restrict__ dst,
+                             long long count, unsigned long long limit, unsigned int* bad,
+                             unsigned int bad_code) {
+  long long pairs = count >> 1;
+  const longlong2* s2 = reinterpret_cast<const longlong2*>(src);
+  uint2* d2 = reinterpret_cast<uint2*>(dst);
+  bool err = false;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < pairs;
+       i += (long long)gridDim.x * blockDim.x) {
+    longlong2 v = __ldcs(s2 + i);
+    err |= (unsigned long long)v.x >= limit || (unsigned long long)v.y >= limit;
+    d2[i] = make_uint2((uint32_t)v.x, (uint32_t)v.y);
+  }
+  if ((count & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+    long long v = src[count - 1];
+    err |= (unsigned long long)v >= limit;
+    dst[count - 1] = (uint32_t)v;
+  }
+  if (err) atomicOr(bad, bad_code);
+}
+
+// Row-offset invariants (csr.py:74-79) + max outdegree.
+__global__ void k_check_rows(const long long* __restrict__ row, long long n, long long m,
+                             unsigned int* bad, unsigned long long* max_deg) {
+  unsigned long long mx = 0;
+  bool err = false;
+  for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; v < n;
+       v += (long long)gridDim.x * blockDim.x) {
+    long long d = row[v + 1] - row[v];
+    err |= d < 0;
+    if (d > 0 && (unsigned long long)d > mx) mx = (unsigned long long)d;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) err |= (row[0] != 0) || (row[n] != m);
+  for (int off = 16; off > 0; off >>= 1) {
+    unsigned long long o = __shfl_xor_sync(0xffffffffu, mx, off);
+    mx = o > mx ? o : mx;
+  }
+  if ((threadIdx.x & 31) == 0 && mx) atomicMax(max_deg, mx);
+  if (err) atomicOr(bad, 1u);
+}
+
+namespace {
+// Process-wide pinned staging ring for pageable -> HBM uploads.
+struct Staging {
+  std::mutex mu;
+  static constexpr size_t kChunk = size_t(8) << 20;  // int64 elements per chunk (64 MB)
+  void* pinned[2] = {nullptr, nullptr};
+  bool ok = false;
+  bool init() {
+    if (ok) return true;
+    for (int i = 0; i < 2; ++i)
+      if (cudaHostAlloc(&pinned[i], kChunk * 8, cudaHostAllocDefault) != cudaSuccess) return false;
+    ok = true;
+    return true;
+  }
+};
+Staging& staging() {
+  static Staging s;
+  return s;
+}
+
+void parallel_copy(void* dst, const void* src, size_t bytes) {
+  unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+  unsigned nt = (unsigned)std::min<size_t>(std::min(16u, hw), bytes / (size_t(4) << 20) + 1);
+  if (nt <= 1) {
+    std::memcpy(dst, src, bytes);
+    return;
+  }
+  std::vector<std::thread> th;
+  size_t per = (bytes + nt - 1) / nt;
+  per = (per + 63) & ~size_t(63);
+  for (unsigned t = 0; t < nt; ++t) {
+    size_t off = t * per;
+    if (off >= bytes) break;
+    size_t len = std::min(per, bytes - off);
+    th.emplace_back([=] { std::memcpy((char*)dst + off, (const char*)src + off, len); });
+  }
+  for (auto& t : th) t.join();
+}
+}  // namespace
+
+// Upload `count` int64 host values: either verbatim into an int64 device
+// array (narrow == false) or narrowed into uint32 with a range check.
+static void upload_int64(glb_graph* g, const int64_t* host, long long count, void* dst,
+                         bool narrow, unsigned long long limit, unsigned bad_code,
+                         unsigned int* d_bad) {
+  if (count <= 0) return;
+  Staging& st = staging();
+  std::lock_guard<std::mutex> lk(st.mu);
+  if (!st.init()) throw Error{GLB_ENOMEM, "cudaHostAlloc of the upload staging ring failed"};
+  DevBuf& stage = g->ws.misc;
+  long long* dstage[2];
+  if (narrow) {
+    ensure(stage, Staging::kChunk * 8 * 2);
+    dstage[0] = (long long*)stage.p;
+    dstage[1] = dstage[0] + Staging::kChunk;
+  }
+  cudaEvent_t done[2];
+  GLB_CUDA_TRY(cudaEventCreateWithFlags(&done[0], cudaEventDisableTiming));
+  GLB_CUDA_TRY(cudaEventCreateWithFlags(&done[1], cudaEventDisableTiming));
+  bool used[2] = {false, false};
+  long long chunks = (count + (long long)Staging::kChunk - 1) / (long long)Staging::kChunk;
+  for (long long c = 0; c < chunks; ++c) {
+    int b = (int)(c & 1);
+    long long off = c * (long long)Staging::kChunk;
+    long long len = std::min<long long>((long long)Staging::kChunk, count - off);
+    if (used[b]) GLB_CUDA_TRY(cudaEventSynchronize(done[b]));
+    parallel_copy(st.pinned[b], host + off, (size_t)len * 8);
+    if (narrow) {
+      GLB_CUDA_TRY(cudaMemcpyAsync(dstage[b], st.pinned[b], (size_t)len * 8,
+                                   cudaMemcpyHostToDevice, g->stream));
+      unsigned grid = grid_for((len + 1) / 2, kBlock, g->num_sms * 8);
+      k_narrow_u32<<<grid, kBlock, 0, g->stream>>>(dstage[b], (uint32_t*)dst + off, len, limit,
+                                                   d_bad, bad_code);
+      GLB_CHECK_LAUNCH();
+    } else {
+      GLB_CUDA_TRY(cudaMemcpyAsync((long long*)dst + off, st.pinned[b], (size_t)len * 8,
+                                   cudaMemcpyHostToDevice, g->stream));
+    }
+    GLB_CUDA_TRY(cudaEventRecord(done[b], g->stream));
+    used[b] = true;
+  }
+  GLB_CUDA_TRY(cudaStreamSynchronize(g->stream));
+  cudaEventDestroy(done[0]);
+  cudaEventDestroy(done[1]);
+}
+
+void graph_upload(glb_graph* g, const int64_t* row, const int64_t* col, const int64_t* w) {
+  GLB_CUDA_TRY(cudaMalloc(&g->row, (size_t)(g->n + 1) * 8));
+  GLB_CUDA_TRY(cudaMalloc(&g->col, (size_t)std::max<long long>(g->m, 1) * 4));
+  if (w) GLB_CUDA_TRY(cudaMalloc(&g->wt, (size_t)std::max<long long>(g->m, 1) * 4));
+  DevCtrl* ctrl = (DevCtrl*)ensure(g->ws.ctrl, sizeof(DevCtrl));
+  GLB_CUDA_TRY(cudaMemsetAsync(ctrl, 0, sizeof(DevCtrl), g->stream));
+  unsigned long long* d_max = (unsigned long long*)&ctrl->aux[0];
+  upload_int64(g, row, g->n + 1, g->row, false, 0, 0, &ctrl->bad_input);
+  upload_int64(g, col, g->m, g->col, true, (unsigned long long)g->n, 2u, &ctrl->bad_input);
+  if (w) upload_int64(g, w, g->m, g->wt, true, 0x100000000ull, 4u, &ctrl->bad_input);
+  if (g->n > 0) {
+    unsigned grid = grid_for(g->n, kBlock, g->num_sms * 8);
+    k_check_rows<<<grid, kBlock, 0, g->stream>>>(g->row, g->n, g->m, &ctrl->bad_input, d_max);
+    GLB_CHECK_LAUNCH();
+  }
+  DevCtrl h;
+  GLB_CUDA_TRY(cudaMemcpyAsync(&h, ctrl, sizeof(DevCtrl), cudaMemcpyDeviceToHost, g->stream));
+  GLB_CUDA_TRY(cudaStreamSynchronize(g->stream));
+  if (h.bad_input & 1u)
+    throw Error{GLB_EINVAL, "row_offsets must start at 0, end at num_edges and be nondecreasing"};
+  if (h.bad_input & 2u) throw Error{GLB_EINVAL, "col_indices contains a node id out of range"};
+  if (h.bad_input & 4u)
+    throw Error{GLB_EINVAL, "edge weights must be nonnegative and below 2^32 on the device"};
+  g->max_degree = (int64_t)h.aux[0];
+}
+
+// ======================================================= degree analysis ===
+__global__ void k_degree_sq(const long long* __restrict__ row, long long n,
+                            unsigned long long* sumsq_hi, double* dummy) {
+  // sum of squared outdegrees, exact in 64 bits for degree < 2^32
+  unsigned long long acc = 0;
+  for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; v < n;
+       v += (long long)gridDim.x * blockDim.x) {
+    unsigned long long d = (unsigned long long)(row[v + 1] - row[v]);
+    acc += d * d;
+  }
+  for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+  if ((threadIdx.x & 31) == 0 && acc) atomicAdd(sumsq_hi, acc);
+}
+
+// degree d > 0 -> bin ceil(d*B/max) (1-based), degree 0 -> bin 1 (degrees.py:55-60)
+__global__ void k_histogram(const long long* __restrict__ row, long long n, int bins,
+                            unsigned long long max_deg, unsigned long long* counts) {
+  extern __shared__ unsigned long long s_cnt[];
+  bool smem = bins <= 4096;
+  if (smem)
+    for (int b = threadIdx.x; b < bins; b += blockDim.x) s_cnt[b] = 0;
+  __syncthreads();
+  for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; v < n;
+       v += (long long)gridDim.x * blockDim.x) {
+    unsigned long long d = (unsigned long long)(row[v + 1] - row[v]);
+    unsigned long long bin = 1;
+    if (max_deg > 0 && d > 0) {
+      unsigned __int128 num = (unsigned __int128)d * (unsigned)bins + (max_deg - 1);
+      bin = (unsigned long long)(num / max_deg);
+    }
+    if (smem)
+      atomicAdd(&s_cnt[bin - 1], 1ull);
+    else
+      atomicAdd(&counts[bin - 1], 1ull);
+  }
+  __syncthreads();
+  if (smem)
+    for (int b = threadIdx.x; b < bins; b += blockDim.x)
+      if (s_cnt[b]) atomicAdd(&counts[b], s_cnt[b]);
+}
+
+void degree_stats(glb_graph* g, int64_t* max_degree, int64_t* sum_degree, double* sum_sq) {
+  DevCtrl* ctrl = (DevCtrl*)ensure(g->ws.ctrl, sizeof(DevCtrl));
+  GLB_CUDA_TRY(cudaMemsetAsync(&ctrl->aux[1], 0, 8, g->stream));
+  if (g->n > 0) {
+    unsigned grid = grid_for(g->n, kBlock, g->num_sms * 8);
+    k_degree_sq<<<grid, kBlock, 0, g->stream>>>(g->row, g->n,
+                                                (unsigned long long*)&ctrl->aux[1], nullptr);
+    GLB_CHECK_LAUNCH();
+  }
+  unsigned long long sq = 0;
+  GLB_CUDA_TRY(cudaMemcpyAsync(&sq, &ctrl->aux[1], 8, cudaMemcpyDeviceToHost, g->stream));
+  GLB_CUDA_TRY(cudaStreamSynchronize(g->stream));
+  *max_degree = g->max_degree;
+  *sum_degree = g->m;
+  *sum_sq = (double)sq;
+}
+
+void histogram(glb_graph* g, const long long* row, long long n, unsigned long long max_deg,
+               int bins, int64_t* counts_out, int32_t* arg_max_bin, int64_t* mdt) {
+  DevBuf& buf = g->ws.misc;
+  // misc may hold upload staging; histogram needs its own small area
+  static_assert(sizeof(unsigned long long) == 8, "");
+  DevBuf tmp;
+  unsigned long long* d_counts = (unsigned long long*)ensure(tmp, (size_t)bins * 8);
+  (void)buf;
+  try {
+    GLB_CUDA_TRY(cudaMemsetAsync(d_counts, 0, (size_t)bins * 8, g->stream));
+    if (n > 0) {
+      unsigned grid = grid_for(n, kBlock, g->num_sms * 4);
+      size_t smem = bins <= 4096 ? (size_t)bins * 8 : 0;
+      k_histogram<<<grid, kBlock, smem, g->stream>>>(row, n, bins, max_deg, d_counts);
+      GLB_CHECK_LAUNCH();
+    }
+    std::vector<unsigned long long> h(bins);
+    GLB_CUDA_TRY(cudaMemcpyAsync(h.data(), d_counts, (size_t)bins * 8, cudaMemcpyDeviceToHost,
+                                 g->stream));
+    GLB_CUDA_TRY(cudaStreamSynchronize(g->stream));
+    free_buf(tmp);
+    // first argmax (degrees.py:62) and mdt = max(1, bin*max // B) (degrees.py:72-76)
+    int arg = 0;
+    for (int b = 0; b < bins; ++b) {
+      if (counts_out) counts_out[b] = (int64_t)h[b];
+      if (h[b] > h[arg]) arg = b;
+    }
+    if (arg_max_bin) *arg_max_bin = arg + 1;
+    if (mdt) {
+      unsigned __int128 num = (unsigned __int128)(arg + 1) * max_deg;
+      unsigned long long v = (unsigned long long)(num / (unsigned)bins);
+      *mdt = (int64_t)std::max<unsigned long long>(1, v);
+    }
+  } catch (...) {
+    free_buf(tmp);
+    throw;
+  }
+}
+
+// ========================================================= COO expansion ===
+// src[e] = v for e in [row[v], row[v+1]) -- np.repeat(arange(n), outdeg),
+// csr.py:168.  Thread / warp / CTA cooperative segment fill.
+__global__ void __launch_bounds__(kBlock) k_coo_src(const long long* __restrict__ row, long long n,
+                                                    uint32_t* __restrict__ src) {
+  __shared__ long long s_lo, s_hi;
+  __shared__ int s_owner;
+  __shared__ uint32_t s_v;
+  for (long long base = blockIdx.x * (long long)kBlock; base < n;
+       base += (long long)gridDim.x * kBlock) {
+    long long v = base + threadIdx.x;
+    long long lo = 0, hi = 0;
+    if (v < n) {
+      lo = row[v];
+      hi = row[v + 1];
+    }
+    // CTA level: segments >= 4096
+    while (true) {
+      if (threadIdx.x == 0) s_owner = -1;
+      __syncthreads();
+      if (hi - lo >= 4096) s_owner = threadIdx.x;
+      __syncthreads();
+      int o = s_owner;
+      if (o < 0) break;
+      if (threadIdx.x == o) {
+        s_lo = lo;
+        s_hi = hi;
+        s_v = (uint32_t)v;
+        lo = hi;
+      }
+      __syncthreads();
+      for (long long e = s_lo + threadIdx.x; e < s_hi; e += kBlock) src[e] = s_v;
+      __syncthreads();
+    }
+    // warp level: segments >= 32
+    unsigned ball;
+    while ((ball = __ballot_sync(0xffffffffu, hi - lo >= 32)) != 0) {
+      int leader = __ffs(ball) - 1;
+      long long wl = __shfl_sync(0xffffffffu, lo, leader);
+      long long wh = __shfl_sync(0xffffffffu, hi, leader);
+      uint32_t wv = (uint32_t)__shfl_sync(0xffffffffu, (unsigned long long)v, leader);
+      if ((int)lane_id() == leader) lo = hi;
+      for (long long e = wl + lane_id(); e < wh; e += 32) src[e] = wv;
+    }
+    for (long long e = lo; e < hi; ++e) src[e] = (uint32_t)v;
+  }
+}
+
+void coo_src(glb_graph* g, uint32_t* d_src) {
+  if (g->n == 0 || g->m == 0) return;
+  unsigned grid = grid_for(g->n, kBlock, g->num_sms * 8);
+  k_coo_src<<<grid, kBlock, 0, g->stream>>>(g->row, g->n, d_src);
+  GLB_CHECK_LAUNCH();
+}
+
+__global__ void k_widen_u32_to_i64(const uint32_t* __restrict__ s, long long* __restrict__ d,
+                                   long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    d[i] = (long long)s[i];
+}
+
+// ========================================================= node splitting ===
+// Per-node scan vector: {children, parent edges, excess edges, split nodes}.
+constexpr int kSplitIPT = 4;
+constexpr int kSplitTile = kBlock * kSplitIPT;
+
+__global__ void __launch_bounds__(kBlock) k_split_scan(const long long* __restrict__ row, long long n,
+                                                       long long mdt, LookbackState<4> lb,
+                                                       unsigned epoch, long long* __restrict__ cs,
+                                                       long long* __restrict__ new_row,
+                                                       long long* __restrict__ excess_pre,
+                                                       long long* totals) {
+  using TS = TileScan<4, kBlock>;
+  __shared__ typename TS::Storage st;
+  long long ntiles = (n + kSplitTile - 1) / kSplitTile;
+  for (long long t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    Vec<4> item[kSplitIPT];
+    Vec<4> sum;
+    long long first = t * kSplitTile + (long long)threadIdx.x * kSplitIPT;
+#pragma unroll
+    for (int k = 0; k < kSplitIPT; ++k) {
+      long long v = first + k;
+      if (v < n) {
+        long long d = row[v + 1] - row[v];
+        long long pieces = d > 0 ? (d + mdt - 1) / mdt : 1;  // max(1, ceil(d/mdt))
+        long long keep = d < mdt ? d : mdt;
+        item[k].w[0] = pieces - 1;
+        item[k].w[1] = keep;
+        item[k].w[2] = d - keep;
+        item[k].w[3] = d > mdt ? 1 : 0;
+      }
+      sum = sum + item[k];
+    }
+    Vec<4> incl;
+    Vec<4> ex = TS::run(st, lb, epoch, t, sum, incl);
+#pragma unroll
+    for (int k = 0; k < kSplitIPT; ++k) {
+      long long v = first + k;
+      if (v < n) {
+        cs[v] = ex.w[0];
+        new_row[v] = ex.w[1];
+        excess_pre[v] = ex.w[2];
+      }
+      ex = ex + item[k];
+    }
+    if (t == ntiles - 1 && threadIdx.x == 0) {
+      cs[n] = incl.w[0];
+      totals[0] = incl.w[0];
+      totals[1] = incl.w[1];
+      totals[2] = incl.w[2];
+      totals[3] = incl.w[3];
+    }
+  }
+}
+
+// Parent keeps its first mdt edges; children take the following mdt-chunks,
+// laid out after all parents' chunks (splitting.py:72-99).
+template <bool W>
+__global__ void __launch_bounds__(kBlock) k_split_fill(
+    const long long* __restrict__ row, const uint32_t* __restrict__ col,
+    const uint32_t* __restrict__ wt, long long n, long long m, long long mdt,
+    const long long* __restrict__ cs, const long long* __restrict__ excess_pre,
+    const long long* __restrict__ totals, long long* __restrict__ new_row,
+    uint32_t* __restrict__ new_col, uint32_t* __restrict__ new_w,
+    long long* __restrict__ parent_of) {
+  __shared__ long long s_src, s_dst, s_len;
+  __shared__ int s_owner;
+  const long long ptotal = totals[1];
+  const long long nchild = totals[0];
+  for (long long base = blockIdx.x * (long long)kBlock; base < n;
+       base += (long long)gridDim.x * kBlock) {
+    long long v = base + threadIdx.x;
+    // two segments per node: parent [row, row+keep) -> new_row[v];
+    // children [row+mdt, row1) -> ptotal + excess_pre[v]
+    long long src0 = 0, dst0 = 0, len0 = 0, src1 = 0, dst1 = 0, len1 = 0;
+    if (v < n) {
+      long long lo = row[v], hi = row[v + 1], d = hi - lo;
+      long long keep = d < mdt ? d : mdt;
+      src0 = lo;
+      dst0 = new_row[v];
+      len0 = keep;
+      src1 = lo + keep;
+      dst1 = ptotal + excess_pre[v];
+      len1 = d - keep;
+      long long c0 = cs[v], c1 = cs[v + 1];
+      for (long long k = 0; k < c1 - c0; ++k) {
+        new_row[n + c0 + k] = dst1 + k * mdt;
+        parent_of[c0 + k] = v;
+      }
+    }
+    if (v == 0) new_row[n + nchild] = m;
+#pragma unroll 1
+    for (int seg = 0; seg < 2; ++seg) {
+      long long s = seg ? src1 : src0, dd = seg ? dst1 : dst0, len = seg ? len1 : len0;
+      while (true) {
+        if (threadIdx.x == 0) s_owner = -1;
+        __syncthreads();
+        if (len >= 2048) s_owner = threadIdx.x;
+        __syncthreads();
+        int o = s_owner;
+        if (o < 0) break;
+        if (threadIdx.x == o) {
+          s_src = s;
+          s_dst = dd;
+          s_len = len;
+          len = 0;
+        }
+        __syncthreads();
+        for (long long k = threadIdx.x; k < s_len; k += kBlock) {
+          new_col[s_dst + k] = col[s_src + k];
+          if (W) new_w[s_dst + k] = wt[s_src + k];
+        }
+        __syncthreads();
+      }
+      unsigned ball;
+      while ((ball = __ballot_sync(0xffffffffu, len >= 32)) != 0) {
+        int leader = __ffs(ball) - 1;
+        long long ws = __shfl_sync(0xffffffffu, s, leader);
+        long long wd = __shfl_sync(0xffffffffu, dd, leader);
+        long long wl = __shfl_sync(0xffffffffu, len, leader);
+        if ((int)lane_id() == leader) len = 0;
+        for (long long k = lane_id(); k < wl; k += 32) {
+          new_col[wd + k] = col[ws + k];
+          if (W) new_w[wd + k] = wt[ws + k];
+        }
+      }
+      for (long long k = 0; k < len; ++k) {
+        new_col[dd + k] = col[s + k];
+        if (W) new_w[dd + k] = wt[s + k];
+      }
+    }
+  }
+}
+
+// Split graph on the device; returns totals {children, parent edges, excess, split nodes}.
+void split_device(glb_graph* g, long long mdt, long long totals_out[4]) {
+  Workspace& ws = g->ws;
+  long long n = g->n, m = g->m;
+  long long* cs = (long long*)ensure(ws.ns_cs, (size_t)(n + 1) * 8);
+  long long* exc = (long long*)ensure(ws.ns_tmp, (size_t)(n + 1) * 8 + 64);
+  long long* totals = exc + (n + 1);
+  // scan look-back state
+  long long ntiles = (n + kSplitTile - 1) / kSplitTile;
+  unsigned* flags = (unsigned*)ensure(ws.scan_flags, (size_t)std::max<long long>(ntiles, 1) * 4 + 4096);
+  size_t vbytes = (size_t)std::max<long long>(ntiles, 1) * sizeof(Vec<4>);
+  char* vals = (char*)ensure(ws.scan_vals, 2 * vbytes + 4096);
+  LookbackState<4> lb{flags, (Vec<4>*)vals, (Vec<4>*)(vals + vbytes)};
+  // parents' row offsets live in the first n entries of new_row; sized after the scan
+  long long* tmp_row = (long long*)ensure(ws.ns_row, (size_t)(n + 1) * 8);
+  GLB_CUDA_TRY(cudaMemsetAsync(totals, 0, 64, g->stream));
+  if (n > 0) {
+    unsigned epoch = ++g->scan_epoch;
+    int cap = max_resident_blocks((const void*)k_split_scan, kBlock, 0, g->num_sms);
+    unsigned grid = grid_for(ntiles, 1, cap);
+    k_split_scan<<<grid, kBlock, 0, g->stream>>>(g->row, n, mdt, lb, epoch, cs, tmp_row, exc,
+                                                 totals);
+    GLB_CHECK_LAUNCH();
+  } else {
+    GLB_CUDA_TRY(cudaMemsetAsync(cs, 0, 8, g->stream));
+  }
+  GLB_CUDA_TRY(cudaMemcpyAsync(totals_out, totals, 32, cudaMemcpyDeviceToHost, g->stream));
+  GLB_CUDA_TRY(cudaStreamSynchronize(g->stream));
+  long long nchild = totals_out[0];
+  long long new_n = n + nchild;
+  // grow new_row preserving the parent prefix already written
+  if (ws.ns_row.bytes < (size_t)(new_n + 1) * 8) {
+    DevBuf nb;
+    ensure(nb, (size_t)(new_n + 1) * 8);
+    GLB_CUDA_TRY(cudaMemcpyAsync(nb.p, ws.ns_row.p, (size_t)n * 8, cudaMemcpyDeviceToDevice,
+                                 g->stream));
+    GLB_CUDA_TRY(cudaStreamSynchronize(g->stream));
+    free_buf(ws.ns_row);
+    ws.ns_row = nb;
+  }
+  long long* new_row = (long long*)ws.ns_row.p;
+  uint32_t* new_col = (uint32_t*)ensure(ws.ns_col, (size_t)std::max<long long>(m, 1) * 4);
+  uint32_t* new_w = g->wt ? (uint32_t*)ensure(ws.ns_w, (size_t)std::max<long long>(m, 1) * 4) : nullptr;
+  long long* parent_of = (long long*)ensure(ws.ns_parent, (size_t)std::max<long long>(nchild, 1) * 8);
+  if (n > 0) {
+    unsigned grid = grid_for(n, kBlock, g->num_sms * 8);
+    if (g->wt)
+      k_split_fill<true><<<grid, kBlock, 0, g->stream>>>(g->row, g->col, g->wt, n, m, mdt, cs,
+                                                         exc, totals, new_row, new_col, new_w,
+                                                         parent_of);
+    else
+      k_split_fill<false><<<grid, kBlock, 0, g->stream>>>(g->row, g->col, g->wt, n, m, mdt, cs,
+                                                          exc, totals, new_row, new_col, new_w,
+                                                          parent_of);
+    GLB_CHECK_LAUNCH();
+  } else {
+    long long mm = m;
+    GLB_CUDA_TRY(cudaMemcpyAsync(new_row, &mm, 8, cudaMemcpyHostToDevice, g->stream));
+    GLB_CUDA_TRY(cudaStreamSynchronize(g->stream));
+  }
+}
+
+// =================================================== scan / find_offsets ===
+constexpr int kScanIPT = 8;
+constexpr int kScanTile = kBlock * kScanIPT;
+
+// Inclusive int64 scan with first-overflow detection (scan.py:19-65).
+__global__ void __launch_bounds__(kBlock) k_inclusive_scan(const long long* __restrict__ in,
+                                                           long long n, long long* __restrict__ out,
+                                                           LookbackState<1> lb, unsigned epoch,
+                                                           unsigned int* ovf) {
+  using TS = TileScan<1, kBlock>;
+  __shared__ typename TS::Storage st;
+  long long ntiles = (n + kScanTile - 1) / kScanTile;
+  for (long long t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    long long x[kScanIPT];
+    Vec<1> sum;
+    long long first = t * kScanTile + (long long)threadIdx.x * kScanIPT;
+#pragma unroll
+    for (int k = 0; k < kScanIPT; ++k) {
+      x[k] = first + k < n ? in[first + k] : 0;
+      sum.w[0] = (long long)((unsigned long long)sum.w[0] + (unsigned long long)x[k]);
+    }
+    Vec<1> incl;
+    Vec<1> ex = TS::run(st, lb, epoch, t, sum, incl);
+    long long run = ex.w[0];
+    bool bad = false;
+#pragma unroll
+    for (int k = 0; k < kScanIPT; ++k) {
+      long long nxt = (long long)((unsigned long long)run + (unsigned long long)x[k]);
+      // the first signed overflow is visible locally: operands agree in sign, result differs
+      bad |= ((run ^ nxt) & (x[k] ^ nxt)) < 0;
+      if (first + k < n) out[first + k] = nxt;
+      run = nxt;
+    }
+    if (bad) atomicOr(ovf, 1u);
+  }
+}
+
+// bisect_right(prefix, t*ept) per thread (workload.py:45-72)
+__global__ void k_find_offsets(const long long* __restrict__ prefix, long long size, long long ept,
+                               long long threads, long long* node_off, long long* edge_off) {
+  long long total = size > 0 ? prefix[size - 1] : 0;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < threads;
+       t += (long long)gridDim.x * blockDim.x) {
+    long long start = t * ept;
+    if (start >= total || (ept > 0 && start / ept != t)) {
+      node_off[t] = -1;
+      edge_off[t] = 0;
+      continue;
+    }
+    long long lo = 0, hi = size;  // first j with prefix[j] > start
+    while (lo < hi) {
+      long long mid = (lo + hi) >> 1;
+      if (prefix[mid] <= start)
+        lo = mid + 1;
+      else
+        hi = mid;
+    }
+    node_off[t] = lo;
+    edge_off[t] = start - (lo ? prefix[lo - 1] : 0);
+  }
+}
+
+}  // namespace glb
+
+// ================================================================ C-ABI ===
+using glb::Error;
+
+namespace {
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    GLB_CUDA_TRY(cudaSetDevice(dev));
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    f();
+    return GLB_OK;
+  } catch (const Error& e) {
+    glb::set_error(e.msg);
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    glb::set_error("host allocation failed");
+    return GLB_ENOMEM;
+  } catch (const std::exception& e) {
+    glb::set_error(e.what());
+    return GLB_ECUDA;
+  }
+}
+
+void require_device(int device) {
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0)
+    throw Error{GLB_ENODEV, "no CUDA device is visible"};
+  if (device < 0 || device >= count)
+    throw Error{GLB_EINVAL, "device ordinal " + std::to_string(device) + " out of range"};
+}
+}  // namespace
+
+extern "C" {
+
+const char* glb_last_error(void) { return glb::last_error(); }
+const char* glb_version(void) { return "graphlb_b200 0.1.0 (sm_100a)"; }
+
+int glb_device_count(int* count) {
+  return guarded([&] {
+    if (!count) throw Error{GLB_EINVAL, "count is NULL"};
+    int c = 0;
+    cudaError_t e = cudaGetDeviceCount(&c);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      c = 0;
+    }
+    *count = c;
+  });
+}
+
+int glb_graph_create(const int64_t* row_offsets, const int64_t* col, const int64_t* weights_or_null,
+                     int64_t n, int64_t m, int device, glb_graph** out) {
+  return guarded([&] {
+    if (!out) throw Error{GLB_EINVAL, "out is NULL"};
+    *out = nullptr;
+    if (n < 0 || m < 0) throw Error{GLB_EINVAL, "node and edge counts must be nonnegative"};
+    if (!row_offsets || (m > 0 && !col)) throw Error{GLB_EINVAL, "row_offsets/col_indices is NULL"};
+    if (n >= (int64_t)0xFFFFFFFFll) throw Error{GLB_EINVAL, "num_nodes must be below 2^32-1 on the device"};
+    require_device(device);
+    DeviceGuard dg(device);
+    glb_graph* g = new glb_graph();
+    try {
+      g->device = device;
+      g->n = n;
+      g->m = m;
+      g->weighted = weights_or_null != nullptr;
+      GLB_CUDA_TRY(cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking));
+      GLB_CUDA_TRY(cudaDeviceGetAttribute(&g->num_sms, cudaDevAttrMultiProcessorCount, device));
+      GLB_CUDA_TRY(cudaEventCreate(&g->ev[0]));
+      GLB_CUDA_TRY(cudaEventCreate(&g->ev[1]));
+      GLB_CUDA_TRY(cudaHostAlloc(&g->host_ctrl, 1 << 16, cudaHostAllocDefault));
+      glb::graph_upload(g, row_offsets, col, weights_or_null);
+    } catch (...) {
+      glb_graph_destroy(g);
+      throw;
+    }
+    *out = g;
+  });
+}
+
+int glb_graph_destroy(glb_graph* g) {
+  if (!g) return GLB_OK;
+  int prev = -1;
+  cudaGetDevice(&prev);
+  cudaSetDevice(g->device);
+  if (g->stream) cudaStreamSynchronize(g->stream);
+  cudaFree(g->row);
+  cudaFree(g->col);
+  cudaFree(g->wt);
+  glb::Workspace& ws = g->ws;
+  glb::DevBuf* bufs[] = {&ws.dist,   &ws.stamp,  &ws.q[0],     &ws.q[1],    &ws.q[2],
+                         &ws.q[3],   &ws.c_pre,  &ws.c_base,   &ws.c_node,  &ws.tile_first,
+                         &ws.scan_flags, &ws.scan_vals, &ws.stats, &ws.ctrl, &ws.ns_row,
+                         &ws.ns_col, &ws.ns_w,   &ws.ns_parent, &ws.ns_cs,  &ws.ns_tmp,
+                         &ws.ep_src, &ws.eq[0],  &ws.eq[1],    &ws.out64,   &ws.misc};
+  for (auto* b : bufs) glb::free_buf(*b);
+  for (auto e : g->ev_pool) cudaEventDestroy(e);
+  if (g->ev[0]) cudaEventDestroy(g->ev[0]);
+  if (g->ev[1]) cudaEventDestroy(g->ev[1]);
+  if (g->host_ctrl) cudaFreeHost(g->host_ctrl);
+  if (g->stream) cudaStreamDestroy(g->stream);
+  if (prev >= 0) cudaSetDevice(prev);
+  delete g;
+  return GLB_OK;
+}
+
+int glb_graph_info(const glb_graph* g, int64_t* n, int64_t* m, int* weighted, int* device) {
+  return guarded([&] {
+    if (!g) throw Error{GLB_EINVAL, "graph is NULL"};
+    if (n) *n = g->n;
+    if (m) *m = g->m;
+    if (weighted) *weighted = g->weighted ? 1 : 0;
+    if (device) *device = g->device;
+  });
+}
+
+int glb_graph_stream(const glb_graph* g, void** stream) {
+  return guarded([&] {
+    if (!g || !stream) throw Error{GLB_EINVAL, "graph/stream is NULL"};
+    *stream = (void*)g->stream;
+  });
+}
+
+int glb_degree_stats(glb_graph* g, int64_t* max_degree, int64_t* sum_degree, double* sum_sq) {
+  return guarded([&] {
+    if (!g || !max_degree || !sum_degree || !sum_sq) throw Error{GLB_EINVAL, "NULL argument"};
+    if (g->n < 1) throw Error{GLB_EINVAL, "degree statistics need at least one node"};
+    std::lock_guard<std::mutex> lk(g->mu);
+    DeviceGuard dg(g->device);
+    glb::degree_stats(g, max_degree, sum_degree, sum_sq);
+  });
+}
+
+int glb_histogram(glb_graph* g, int bins, int64_t* counts, int64_t* max_degree,
+                  int32_t* arg_max_bin, int64_t* mdt) {
+  return guarded([&] {
+    if (!g) throw Error{GLB_EINVAL, "graph is NULL"};
+    if (bins < 1) throw Error{GLB_EINVAL, "bins must be >= 1"};
+    std::lock_guard<std::mutex> lk(g->mu);
+    DeviceGuard dg(g->device);
+    if (max_degree) *max_degree = g->max_degree;
+    glb::histogram(g, g->row, g->n, (unsigned long long)g->max_degree, bins, counts, arg_max_bin,
+                   mdt);
+  });
+}
+
+int glb_split_graph(glb_graph* g, int64_t mdt, int64_t* new_n, int64_t* num_children,
+                    int64_t* new_row_offsets, int64_t* new_col, int64_t* new_weights,
+                    int64_t* parent_of, int64_t* children_start) {
+  return guarded([&] {
+    if (!g) throw Error{GLB_EINVAL, "graph is NULL"};
+    if (mdt < 1) throw Error{GLB_EINVAL, "mdt must be >= 1"};
+    std::lock_guard<std::mutex> lk(g->mu);
+    DeviceGuard dg(g->device);
+    long long tot[4];
+    glb::split_device(g, mdt, tot);
+    long long nn = g->n + tot[0];
+    if (new_n) *new_n = nn;
+    if (num_children) *num_children = tot[0];
+    if (!new_row_offsets) return;
+    glb::Workspace& ws = g->ws;
+    GLB_CUDA_TRY(cudaMemcpyAsync(new_row_offsets, ws.ns_row.p, (size_t)(nn + 1) * 8,
+                                 cudaMemcpyDeviceToHost, g->stream));
+    if (children_start)
+      GLB_CUDA_TRY(cudaMemcpyAsync(children_start, ws.ns_cs.p, (size_t)(g->n + 1) * 8,
+                                   cudaMemcpyDeviceToHost, g->stream));
+    if (parent_of && tot[0] > 0)
+      GLB_CUDA_TRY(cudaMemcpyAsync(parent_of, ws.ns_parent.p, (size_t)tot[0] * 8,
+                                   cudaMemcpyDeviceToHost, g->stream));
+    auto widen = [&](const uint32_t* src, int64_t* dst) {
+      if (g->m == 0) return;
+      long long* d = (long long*)glb::ensure(ws.out64, (size_t)g->m * 8);
+      unsigned grid = glb::grid_for(g->m, glb::kBlock, g->num_sms * 8);
+      glb::k_widen_u32_to_i64<<<grid, glb::kBlock, 0, g->stream>>>(src, d, g->m);
+      GLB_CHECK_LAUNCH();
+      GLB_CUDA_TRY(cudaMemcpyAsync(dst, d, (size_t)g->m * 8, cudaMemcpyDeviceToHost, g->stream));
+      GLB_CUDA_TRY(cudaStreamSynchronize(g->stream));
+    };
+    if (new_col) widen((const uint32_t*)ws.ns_col.p, new_col);
+    if (new_weights && g->wt) widen((const uint32_t*)ws.ns_w.p, new_weights);
+    GLB_CUDA_TRY(cudaStreamSynchronize(g->stream));
+  });
+}
+
+int glb_csr_to_coo(glb_graph* g, int64_t max_cells, int64_t* src_out) {
+  return guarded([&] {
+    if (!g) throw Error{GLB_EINVAL, "graph is NULL"};
+    long long required = (g->weighted ? 3 : 2) * g->m;
+    if (required > max_cells)
+      throw Error{GLB_ECOO_CAPACITY, "coordinate layout needs " + std::to_string(required) +
+                                         " cells but the budget allows " +
+                                         std::to_string(max_cells)};
+    std::lock_guard<std::mutex> lk(g->mu);
+    DeviceGuard dg(g->device);
+    if (g->m == 0) return;
+    uint32_t* src = (uint32_t*)glb::ensure(g->ws.ep_src, (size_t)g->m * 4);
+    glb::coo_src(g, src);
+    if (src_out) {
+      long long* d = (long long*)glb::ensure(g->ws.out64, (size_t)g->m * 8);
+      unsigned grid = glb::grid_for(g->m, glb::kBlock, g->num_sms * 8);
+      glb::k_widen_u32_to_i64<<<grid, glb::kBlock, 0, g->stream>>>(src, d, g->m);
+      GLB_CHECK_LAUNCH();
+      GLB_CUDA_TRY(cudaMemcpyAsync(src_out, d, (size_t)g->m * 8, cudaMemcpyDeviceToHost, g->stream));
+    }
+    GLB_CUDA_TRY(cudaStreamSynchronize(g->stream));
+  });
+}
+
+int glb_inclusive_scan(const int64_t* values, int64_t n, int64_t* out, int device) {
+  return guarded([&] {
+    if (n < 0) throw Error{GLB_EINVAL, "n must be nonnegative"};
+    if (n == 0) return;
+    if (!values || !out) throw Error{GLB_EINVAL, "NULL argument"};
+    require_device(device);
+    DeviceGuard dg(device);
+    cudaStream_t s;
+    GLB_CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    long long ntiles = (n + glb::kScanTile - 1) / glb::kScanTile;
+    size_t bytes = (size_t)n * 8 * 2 + (size_t)ntiles * (4 + 2 * sizeof(glb::Vec<1>)) + 256;
+    char* base = nullptr;
+    cudaError_t e = cudaMalloc(&base, bytes);
+    if (e != cudaSuccess) {
+      cudaStreamDestroy(s);
+      throw Error{GLB_ENOMEM, "device allocation for inclusive_scan failed"};
+    }
+    long long* d_in = (long long*)base;
+    long long* d_out = d_in + n;
+    unsigned* ovf = (unsigned*)(d_out + n);
+    unsigned* flags = ovf + 16;
+    glb::Vec<1>* aggs = (glb::Vec<1>*)(((uintptr_t)(flags + ntiles) + 63) & ~uintptr_t(63));
+    glb::Vec<1>* incls = aggs + ntiles;
+    unsigned hovf = 0;
+    try {
+      GLB_CUDA_TRY(cudaMemsetAsync(ovf, 0, (size_t)(16 + ntiles) * 4, s));
+      GLB_CUDA_TRY(cudaMemcpyAsync(d_in, values, (size_t)n * 8, cudaMemcpyHostToDevice, s));
+      int cap = glb::max_resident_blocks((const void*)glb::k_inclusive_scan, glb::kBlock, 0, 148);
+      int sms = 148;
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+      cap = glb::max_resident_blocks((const void*)glb::k_inclusive_scan, glb::kBlock, 0, sms);
+      unsigned grid = glb::grid_for(ntiles, 1, cap);
+      glb::k_inclusive_scan<<<grid, glb::kBlock, 0, s>>>(
+          d_in, n, d_out, glb::LookbackState<1>{flags, aggs, incls}, 1u, ovf);
+      GLB_CHECK_LAUNCH();
+      GLB_CUDA_TRY(cudaMemcpyAsync(out, d_out, (size_t)n * 8, cudaMemcpyDeviceToHost, s));
+      GLB_CUDA_TRY(cudaMemcpyAsync(&hovf, ovf, 4, cudaMemcpyDeviceToHost, s));
+      GLB_CUDA_TRY(cudaStreamSynchronize(s));
+    } catch (...) {
+      cudaFree(base);
+      cudaStreamDestroy(s);
+      throw;
+    }
+    cudaFree(base);
+    cudaStreamDestroy(s);
+    if (hovf) throw Error{GLB_EOVERFLOW, "prefix sum exceeds the 64-bit counter range"};
+  });
+}
+
+int glb_find_offsets(const int64_t* prefix, int64_t size, int64_t edges_per_thread, int64_t threads,
+                     int64_t* node_off, int64_t* edge_off, int device) {
+  return guarded([&] {
+    if (size < 0 || threads < 0) throw Error{GLB_EINVAL, "size/threads must be nonnegative"};
+    if (edges_per_thread < 1) throw Error{GLB_EINVAL, "edges_per_thread must be >= 1"};
+    if (threads == 0) return;
+    if ((size > 0 && !prefix) || !node_off || !edge_off) throw Error{GLB_EINVAL, "NULL argument"};
+    require_device(device);
+    DeviceGuard dg(device);
+    cudaStream_t s;
+    GLB_CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    size_t bytes = (size_t)(size + 2 * threads + 1) * 8;
+    long long* base = nullptr;
+    if (cudaMalloc(&base, bytes) != cudaSuccess) {
+      cudaStreamDestroy(s);
+      throw Error{GLB_ENOMEM, "device allocation for find_offsets failed"};
+    }
+    long long* d_pre = base;
+    long long* d_node = base + size;
+    long long* d_edge = d_node + threads;
+    try {
+      if (size > 0)
+        GLB_CUDA_TRY(cudaMemcpyAsync(d_pre, prefix, (size_t)size * 8, cudaMemcpyHostToDevice, s));
+      unsigned grid = glb::grid_for(threads, glb::kBlock, 148 * 8);
+      glb::k_find_offsets<<<grid, glb::kBlock, 0, s>>>(d_pre, size, edges_per_thread, threads,
+                                                       d_node, d_edge);
+      GLB_CHECK_LAUNCH();
+      GLB_CUDA_TRY(cudaMemcpyAsync(node_off, d_node, (size_t)threads * 8, cudaMemcpyDeviceToHost, s));
+      GLB_CUDA_TRY(cudaMemcpyAsync(edge_off, d_edge, (size_t)threads * 8, cudaMemcpyDeviceToHost, s));
+      GLB_CUDA_TRY(cudaStreamSynchronize(s));
+    } catch (...) {
+      cudaFree(base);
+      cudaStreamDestroy(s);
+      throw;
+    }
+    cudaFree(base);
+    cudaStreamDestroy(s);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,222 @@
+// glb_internal.cuh -- shared device/host internals of libgraphlb_b200.so.
+//
+// Device layout of a graph:
+//   row  : int64[n+1]   row offsets (kept 64-bit; csr.py:57 INDEX_DTYPE)
+//   col  : uint32[m]    destinations (narrowed from int64 on upload)
+//   wt   : uint32[m]    weights, or nullptr for an unweighted graph
+//   dist : uint32[n]    INF = 0xFFFFFFFF (u64 variant: INF = 2^63-1, engine.py:27)
+//   stamp: uint32[n]    "pushed in generation g" marks replacing the dedup
+//                       flag array + clear() of worklist.py:26-81
+//   queue: uint32[n]    node worklists (capacity n is overflow-free with dedup)
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/graphlb_b200.h"
+
+namespace glb {
+
+constexpr int kBlock = 256;  // threads per CTA for every relax kernel
+constexpr int kStatSlots = 32;  // spread of the per-launch counter atomics
+
+// ---------------------------------------------------------------- errors ---
+void set_error(const std::string& msg);
+struct Error {
+  int code;
+  std::string msg;
+};
+
+#define GLB_CUDA_TRY(expr)                                                       \
+  do {                                                                           \
+    cudaError_t _e = (expr);                                                     \
+    if (_e != cudaSuccess) {                                                     \
+      throw ::glb::Error{_e == cudaErrorMemoryAllocation ? GLB_ENOMEM : GLB_ECUDA, \
+                         std::string(#expr) + ": " + cudaGetErrorString(_e)};    \
+    }                                                                            \
+  } while (0)
+
+#define GLB_CHECK_LAUNCH() GLB_CUDA_TRY(cudaGetLastError())
+
+// ------------------------------------------------------- distance traits ---
+template <typename D>
+struct DistTraits;
+template <>
+struct DistTraits<uint32_t> {
+  static constexpr uint32_t kInf = 0xFFFFFFFFu;
+};
+template <>
+struct DistTraits<unsigned long long> {
+  static constexpr unsigned long long kInf = 0x7FFFFFFFFFFFFFFFull;
+};
+
+// ---------------------------------------------------- per-launch counters ---
+// One LaunchStats per kernel invocation; kStatSlots copies spread the atomics
+// (summed on the host).  Mirrors MetricsRecord (engine.py:142-174).
+struct StatSlot {
+  unsigned long long relax;
+  unsigned long long push;
+  unsigned long long work;
+  unsigned long long work_sq;
+  unsigned long long work_max;
+  unsigned long long pad[3];
+};
+struct LaunchStats {
+  StatSlot slot[kStatSlots];
+};
+
+// Device control block: queue sizes + scan outputs + error flags.
+struct DevCtrl {
+  unsigned int qcount[8];       // worklist cursors
+  unsigned int overflow;        // a u32 candidate reached INF -> re-run in u64
+  unsigned int bad_input;       // upload validation failure
+  long long wd_total;           // WD: active edges of this invocation
+  long long wd_items;           // WD: worklist items with remaining edges
+  long long aux[4];
+};
+
+// --------------------------------------------------------- device graph ---
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+};
+
+struct Workspace {
+  DevBuf dist, stamp, q[4];
+  DevBuf c_pre, c_base, c_node, tile_first;  // WD compacted frontier
+  DevBuf scan_flags, scan_vals;              // decoupled look-back state
+  DevBuf stats;                              // LaunchStats[kMaxLaunchSlots]
+  DevBuf ctrl;                               // DevCtrl
+  DevBuf ns_row, ns_col, ns_w, ns_parent, ns_cs, ns_tmp;  // NS split graph
+  DevBuf ep_src, eq[2];                      // EP COO src + edge worklists
+  DevBuf out64;                              // widened distances
+  DevBuf misc;
+};
+
+}  // namespace glb
+
+struct glb_graph {
+  int device = 0;
+  int64_t n = 0, m = 0;
+  bool weighted = false;
+  int64_t max_degree = 0;
+  cudaStream_t stream = nullptr;
+  int num_sms = 148;
+  long long* row = nullptr;
+  uint32_t* col = nullptr;
+  uint32_t* wt = nullptr;
+  glb::Workspace ws;
+  uint32_t stamp_epoch = 0;   // last stamp generation handed out
+  uint32_t scan_epoch = 0;    // last look-back epoch handed out
+  void* host_ctrl = nullptr;  // pinned DevCtrl + stats mirror
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  std::vector<cudaEvent_t> ev_pool;
+  std::vector<glb_record> last_records;  // records of the most recent glb_run
+  std::mutex mu;              // drivers are not re-entrant (common.py:5-6)
+};
+
+namespace glb {
+
+// -------------------------------------------------------- host helpers ---
+void* ensure(DevBuf& b, size_t bytes);  // grow-only device allocation
+void free_buf(DevBuf& b);
+int max_resident_blocks(const void* kernel, int block, size_t smem, int num_sms);
+
+inline unsigned int grid_for(long long items, int per_block, int cap) {
+  long long b = (items + per_block - 1) / per_block;
+  if (b < 1) b = 1;
+  if (b > cap) b = cap;
+  return (unsigned int)b;
+}
+
+// ------------------------------------------------------ device helpers ---
+__device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
+
+// Warp-aggregated append (one atomicAdd per converged group) -- the device
+// form of wl_push_node's cursor bump (worklist.py:107-130).
+__device__ __forceinline__ void q_append(uint32_t* q, unsigned int* cursor,
+                                         uint32_t item) {
+  unsigned mask = __activemask();
+  unsigned leader = __ffs(mask) - 1;
+  unsigned rank = __popc(mask & ((1u << lane_id()) - 1u));
+  unsigned base = 0;
+  if (lane_id() == leader) base = atomicAdd(cursor, (unsigned)__popc(mask));
+  base = __shfl_sync(mask, base, leader);
+  q[base + rank] = item;
+}
+
+// Dedup test-and-set: the first thread to stamp `v` with generation `gen`
+// wins (replaces Worklist.flags + clear(), worklist.py:68-75,107-130).
+__device__ __forceinline__ bool claim(uint32_t* stamp, uint32_t v, uint32_t gen) {
+  if (stamp[v] == gen) return false;
+  return atomicExch(stamp + v, gen) != gen;
+}
+
+// atomic_relax_min (engine.py:120-139): plain-load pre-check (sound because
+// cells only decrease), then atomicMin; true iff strictly decreased.
+__device__ __forceinline__ bool relax_min(uint32_t* dist, uint32_t v, uint32_t cand) {
+  if (cand >= dist[v]) return false;
+  return cand < atomicMin(dist + v, cand);
+}
+__device__ __forceinline__ bool relax_min(unsigned long long* dist, uint32_t v,
+                                          unsigned long long cand) {
+  if (cand >= dist[v]) return false;
+  return cand < atomicMin(dist + v, cand);
+}
+
+// Candidate distance with overflow detection for the u32 path.
+template <typename D>
+__device__ __forceinline__ bool make_cand(D dn, uint32_t w, D& cand, unsigned int* ovf) {
+  unsigned long long c = (unsigned long long)dn + (unsigned long long)w;
+  if (c >= (unsigned long long)DistTraits<D>::kInf) {
+    atomicOr(ovf, 1u);
+    return false;
+  }
+  cand = (D)c;
+  return true;
+}
+
+// Per-thread counters reduced per warp then spread across kStatSlots.
+struct ThreadCounters {
+  unsigned long long work = 0;
+  unsigned long long relax = 0;
+  unsigned long long push = 0;
+};
+
+__device__ __forceinline__ void flush_counters(LaunchStats* ls, const ThreadCounters& c) {
+  unsigned long long w = c.work, r = c.relax, p = c.push, sq = c.work * c.work, mx = c.work;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    w += __shfl_xor_sync(0xffffffffu, w, off);
+    r += __shfl_xor_sync(0xffffffffu, r, off);
+    p += __shfl_xor_sync(0xffffffffu, p, off);
+    sq += __shfl_xor_sync(0xffffffffu, sq, off);
+    unsigned long long o = __shfl_xor_sync(0xffffffffu, mx, off);
+    mx = o > mx ? o : mx;
+  }
+  __shared__ unsigned long long s_acc[5];
+  if (threadIdx.x < 5) s_acc[threadIdx.x] = 0;
+  __syncthreads();
+  if (lane_id() == 0) {
+    atomicAdd(&s_acc[0], w);
+    atomicAdd(&s_acc[1], r);
+    atomicAdd(&s_acc[2], p);
+    atomicAdd(&s_acc[3], sq);
+    atomicMax(&s_acc[4], mx);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    StatSlot& s = ls->slot[blockIdx.x % kStatSlots];
+    if (s_acc[0]) atomicAdd(&s.work, s_acc[0]);
+    if (s_acc[1]) atomicAdd(&s.relax, s_acc[1]);
+    if (s_acc[2]) atomicAdd(&s.push, s_acc[2]);
+    if (s_acc[3]) atomicAdd(&s.work_sq, s_acc[3]);
+    if (s_acc[4]) atomicMax(&s.work_max, s_acc[4]);
+  }
+}
+
+}  // namespace glb

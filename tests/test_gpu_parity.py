@@ -1,0 +1,250 @@
+"""GPU parity: every strategy's device result against the reference's answers.
+
+Bit-exact equality (levels and integer distances are integer data, no
+tolerance): golden vectors from the reference (tests/golden/) and, at sizes
+the reference cannot reach quickly, the pinned C oracle (oracle/).
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+import paper_1711_00231_b200 as pkg
+from paper_1711_00231_b200 import _lib
+from tests import graph_specs as gs
+
+pytestmark = pytest.mark.gpu
+
+TAGS = ("BS", "EP", "WD", "NS", "HP")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def need_gpu():
+    _lib.lib()  # ImportError (test error) if the CUDA library was not built
+    assert _lib.device_count() > 0, "no CUDA device visible to libgraphlb_b200.so"
+
+
+@pytest.mark.parametrize("loop", ["host", "graph"])
+def test_corpus_all_strategies_match_reference(golden, loop):
+    cfg = pkg.KernelConfig(loop=loop)
+    for gid, spec in gs.CORPUS.items():
+        g = gs.build(pkg, spec)
+        for src in gs.sources_for(g.num_nodes):
+            for algo in ("bfs", "sssp"):
+                exp = golden["corpus"][f"{gid}|{src}|{algo}"]
+                for tag in TAGS:
+                    r = pkg.run_strategy(tag, g, src, pkg.RelaxOp(algo), cfg)
+                    assert r.feasible
+                    got = r.dist.array
+                    bad = np.flatnonzero(got != exp)
+                    assert bad.size == 0, (gid, src, algo, tag, bad[:5], got[bad[:5]], exp[bad[:5]])
+
+
+def test_dist_bits_64_and_small_blocks(golden):
+    for gid in ("rmat10_s1", "rmat10_skew", "degrees", "quirks"):
+        g = gs.build(pkg, gs.CORPUS[gid])
+        for algo in ("bfs", "sssp"):
+            exp = golden["corpus"][f"{gid}|0|{algo}"]
+            for tag in TAGS:
+                for cfg in (pkg.KernelConfig(dist_bits=64), pkg.KernelConfig(block_size=4),
+                            pkg.KernelConfig(block_size=100000)):
+                    r = pkg.run_strategy(tag, g, 0, pkg.RelaxOp(algo), cfg)
+                    assert np.array_equal(r.dist.array, exp), (gid, algo, tag, cfg)
+            for mdt in (1, 2, 7, 1000):
+                for tag in ("NS", "HP"):
+                    r = pkg.run_strategy(tag, g, 0, pkg.RelaxOp(algo), pkg.KernelConfig(), mdt=mdt)
+                    assert np.array_equal(r.dist.array, exp) and r.mdt == mdt
+            r = pkg.run_hp(g, 0, pkg.RelaxOp(algo), pkg.KernelConfig(), fallback=False)
+            assert np.array_equal(r.dist.array, exp)
+
+
+def test_u32_overflow_promotes_to_u64(oracle):
+    # path with weights 2^31: distances pass 2^32 -> automatic 64-bit re-run
+    n = 6
+    w = np.full(n - 1, 1 << 31, dtype=np.int64)
+    g = pkg.CsrGraph.from_edges(n, np.arange(n - 1), np.arange(1, n), w)
+    exp = oracle.dijkstra(g.row_offsets, g.col_indices, g.weights, 0)
+    for tag in TAGS:
+        r = pkg.run_strategy(tag, g, 0, pkg.RelaxOp("sssp"), pkg.KernelConfig())
+        assert np.array_equal(r.dist.array, exp), tag
+        assert r.device["dist_bits"] == 64
+        with pytest.raises(OverflowError):
+            pkg.run_strategy(tag, g, 0, pkg.RelaxOp("sssp"), pkg.KernelConfig(dist_bits=32))
+
+
+def test_random_graphs_with_quirks(oracle):
+    rng = np.random.default_rng(123)
+    for trial in range(25):
+        n = int(rng.integers(1, 200))
+        m = int(rng.integers(0, 6 * n))
+        src = rng.integers(0, n, size=m)
+        # a few hubs, self-loops and parallel edges, zero weights
+        if m:
+            src[: m // 4] = rng.integers(0, max(1, n // 10), size=m // 4)
+        dst = rng.integers(0, n, size=m)
+        w = rng.integers(0, 9, size=m) if trial % 3 else None
+        g = pkg.CsrGraph.from_edges(n, src, dst, w)
+        s = int(rng.integers(0, n))
+        for algo in ("bfs", "sssp"):
+            exp = oracle.oracle_distances(g, s, algo)
+            for tag in TAGS:
+                for mdt in (None, 1, 3):
+                    if mdt is not None and tag not in ("NS", "HP"):
+                        continue
+                    r = pkg.run_strategy(tag, g, s, pkg.RelaxOp(algo), pkg.KernelConfig(), mdt=mdt)
+                    assert np.array_equal(r.dist.array, exp), (trial, algo, tag, mdt)
+
+
+def test_split_graph_device_matches_reference(golden):
+    sp = golden["split"]
+    for gid in ("rmat10_s1", "rmat10_skew", "degrees", "quirks", "er_empty"):
+        g = gs.build(pkg, gs.CORPUS[gid])
+        h = pkg.build_histogram(g, 10)
+        ref_h = sp[f"{gid}|hist10"]
+        assert np.array_equal(h.counts, ref_h[:10])
+        assert [h.max_degree, h.arg_max_bin, pkg.compute_mdt(h)] == ref_h[10:].tolist()
+        for key in [k for k in sp if k.startswith(gid + "|") and k.endswith("|row")]:
+            mdt = int(key.split("|")[1])
+            s = pkg.split_graph(g, mdt)
+            base = f"{gid}|{mdt}"
+            assert np.array_equal(s.graph.row_offsets, sp[base + "|row"]), base
+            assert np.array_equal(s.graph.col_indices, sp[base + "|col"]), base
+            if g.weights is not None:
+                assert np.array_equal(s.graph.weights, sp[base + "|w"]), base
+            assert np.array_equal(s.parent_of, sp[base + "|parent"]), base
+            assert np.array_equal(s.children_start, sp[base + "|cs"]), base
+    for name in ("split_7_4", "split_9_2", "split_mix_3"):
+        k = golden["kats"][name]
+        g = pkg.graph_from_degrees(k["degrees"], weighted=True, seed=4)
+        s = pkg.split_graph(g, k["mdt"])
+        assert np.diff(s.graph.row_offsets).tolist() == k["new_degrees"]
+        assert s.graph.col_indices.tolist() == k["col"] and s.graph.weights.tolist() == k["w"]
+        assert s.parent_of.tolist() == k["parent_of"]
+        assert s.children_start.tolist() == k["children_start"]
+        assert s.split_fraction == k["split_fraction"]
+
+
+def test_histogram_mdt_kats(golden):
+    k = golden["kats"]
+    h = pkg.build_histogram(pkg.graph_from_degrees([1, 1, 1, 9]), 3)
+    assert h.counts.tolist() == k["hist_1119_b3"]["counts"] and h.arg_max_bin == 1
+    assert pkg.compute_mdt(pkg.build_histogram(pkg.graph_from_degrees([1181] + [1] * 100), 10)) == 118
+    assert pkg.compute_mdt(pkg.build_histogram(pkg.graph_from_degrees(k["mdt_er23_shape"]["degrees"]), 10)) == 3
+    h = pkg.build_histogram(pkg.graph_from_degrees([0, 0, 0]), 4)
+    assert h.counts.tolist() == k["hist_all_zero"]["counts"] and pkg.compute_mdt(h) == 1
+    ds = pkg.degree_stats(pkg.star_graph(5))
+    assert [ds.max, ds.avg] == k["degree_stats_star5"][:2]
+    assert math.isclose(ds.stddev, k["degree_stats_star5"][2], rel_tol=1e-12)
+    r = pkg.run_ns(gs.build(pkg, gs.CORPUS["rmat10_s1"]), 0, pkg.RelaxOp("sssp"), pkg.KernelConfig())
+    assert r.mdt == k["ns_rmat10_s1"]["mdt"] and r.split_fraction == k["ns_rmat10_s1"]["split_fraction"]
+    r = pkg.run_hp(gs.build(pkg, gs.CORPUS["rmat10_s1"]), 0, pkg.RelaxOp("sssp"), pkg.KernelConfig())
+    assert r.mdt == k["hp_rmat10_s1"]["mdt"]
+
+
+def test_scan_and_find_offsets_on_device(golden):
+    sc = golden["scan"]
+    for key in [k for k in sc if k.endswith("|in")]:
+        assert np.array_equal(np.array(pkg.inclusive_scan(sc[key])), sc[key[:-3] + "|out"])
+    for key in [k for k in sc if k.endswith("|prefix")]:
+        base = key[: -len("|prefix")]
+        ept, threads = sc[base + "|meta"].tolist()
+        prefix = sc[key]
+        t = pkg.find_offsets(None, list(range(len(prefix))), prefix, ept, threads)
+        assert t.node_offsets == sc[base + "|node"].tolist()
+        assert t.edge_offsets == sc[base + "|edge"].tolist()
+    k = golden["kats"]
+    t = pkg.find_offsets(None, [0, 1], [5, 12], 3, 4)
+    assert t.node_offsets == k["find_offsets_fig2"]["node"]
+    assert t.edge_offsets == k["find_offsets_fig2"]["edge"]
+    t = pkg.find_offsets(None, [0, 1], [5, 12], 5, 8)
+    assert t.node_offsets == k["find_offsets_idle"]["node"]
+    assert pkg.inclusive_scan([5, 7]) == k["scan_5_7"]
+    with pytest.raises(OverflowError):
+        pkg.inclusive_scan([2**62, 2**62])
+    with pytest.raises(ValueError):
+        pkg.find_offsets(None, [0, 1, 2], [5, 12], 3, 4)
+
+
+def test_coo_and_ep_feasibility(golden):
+    coo = pkg.csr_to_coo(pkg.CsrGraph(2, 2, [0, 2, 2], [1, 0]))
+    assert coo.src.tolist() == golden["kats"]["coo_small"]["src"]
+    g = gs.build(pkg, gs.CORPUS["rmat12_s4"])
+    coo = pkg.csr_to_coo(g)
+    assert np.array_equal(coo.src, np.repeat(np.arange(g.num_nodes), g.outdegrees()))
+    with pytest.raises(pkg.CooCapacityError):
+        pkg.csr_to_coo(g, max_cells=10)
+    ger = pkg.generate_er(2000, 60000, seed=9)
+    r = pkg.run_ep(ger, 0, pkg.RelaxOp("sssp"), pkg.KernelConfig(), max_cells=100_000)
+    assert r.status == golden["kats"]["ep_cliff"]["status"] == pkg.INFEASIBLE_MEMORY
+    assert r.dist is None
+    for tag in ("BS", "WD", "NS", "HP"):
+        assert pkg.run_strategy(tag, ger, 0, pkg.RelaxOp("sssp"), pkg.KernelConfig(),
+                                max_cells=100_000).feasible
+
+
+def test_hp_subiteration_structure(golden):
+    k = golden["kats"]
+    g100 = pkg.CsrGraph.from_edges(2, [0] * 100, [1] * 100)
+    r = pkg.run_hp(g100, 0, pkg.RelaxOp("bfs"), pkg.KernelConfig(), mdt=5, fallback=False)
+    assert sum(1 for rec in r.records if rec.iteration == 0) == k["hp_100_mdt5_subiters"] == 20
+    fig = pkg.CsrGraph.from_edges(4, [0, 0] + [1] * 5 + [2] * 7, [1, 2] + [3] * 12)
+    r = pkg.run_hp(fig, 0, pkg.RelaxOp("bfs"), pkg.KernelConfig(), mdt=3, fallback=False)
+    per = [sum(1 for rec in r.records if rec.iteration == i) for i in range(max(x.iteration for x in r.records) + 1)]
+    assert per == k["hp_fig4_subiters_per_iter"]
+    r = pkg.run_hp(fig, 0, pkg.RelaxOp("bfs"), pkg.KernelConfig(), mdt=3, fallback=True)
+    assert [rec.strategy for rec in r.records] == k["hp_fig4_fallback_tags"]
+
+
+def test_records_and_counters():
+    g = pkg.generate_rmat(14, 8, seed=1, max_weight=255)
+    run = {t: pkg.run_strategy(t, g, 0, pkg.RelaxOp("bfs"), pkg.KernelConfig()) for t in TAGS}
+    levels = int(run["BS"].dist.array[run["BS"].dist.array != pkg.INF].max())
+    assert len(run["BS"].records) == levels + 1          # one launch per BFS level
+    deg = g.outdegrees()
+    reached = run["BS"].dist.array != pkg.INF
+    e_r = int(deg[reached].sum())
+    for t in ("BS", "WD"):                                 # BFS examines every reached edge once
+        assert sum(r.work_total() for r in run[t].records) == e_r, t
+    # chunked EP reserves once per destination range (SPEC acceptance 7)
+    ch = pkg.run_ep(g, 0, pkg.RelaxOp("sssp"), pkg.KernelConfig(), chunked=True)
+    un = pkg.run_ep(g, 0, pkg.RelaxOp("sssp"), pkg.KernelConfig(), chunked=False)
+    assert ch.dist == un.dist
+    assert sum(r.atomic_push_ops for r in ch.records) < sum(r.atomic_push_ops for r in un.records)
+    # imbalance ordering on skewed RMAT (SPEC acceptance 8, device counters)
+    sd = {t: sum(r.work_stddev() for r in pkg.run_strategy(t, g, 0, pkg.RelaxOp("sssp"),
+                                                            pkg.KernelConfig()).records) for t in TAGS}
+    assert sd["EP"] < sd["BS"] and sd["WD"] < sd["BS"] and sd["NS"] < sd["BS"], sd
+
+
+@pytest.fixture(scope="module")
+def c1_graph():
+    return pkg.generate_rmat(16, 16, seed=1, max_weight=255)
+
+
+def test_c1_all_strategies(c1_graph, oracle, golden):
+    g = c1_graph
+    for algo in ("bfs", "sssp"):
+        exp = oracle.oracle_distances(g, 0, algo)
+        if golden["big"]:
+            assert gs.dist_digest(exp) == golden["big"]["C1"][f"{algo}_digest"]
+        for tag in TAGS:
+            for loop in ("host", "graph"):
+                r = pkg.run_strategy(tag, g, 0, pkg.RelaxOp(algo), pkg.KernelConfig(loop=loop))
+                assert np.array_equal(r.dist.array, exp), (algo, tag, loop)
+
+
+@pytest.mark.slow
+def test_c2_rmat22_all_strategies(oracle, golden):
+    g = pkg.generate_rmat(22, 16, seed=1, max_weight=255)
+    big = golden["big"]
+    if big:
+        assert gs.digest(g) == big["C2"]["graph_digest"]
+    for algo in ("bfs", "sssp"):
+        exp = oracle.oracle_distances(g, 0, algo)
+        if big:
+            assert gs.dist_digest(exp) == big["C2"][f"{algo}_digest"]
+        for tag in TAGS:
+            r = pkg.run_strategy(tag, g, 0, pkg.RelaxOp(algo), pkg.KernelConfig(loop="graph"))
+            assert np.array_equal(r.dist.array, exp), (algo, tag)
+    g.release_device()
