@@ -125,6 +125,8 @@ typedef struct glb_record {
 const char* glb_last_error(void);
 const char* glb_version(void);
 int glb_device_count(int* count);
+/* number of CUDA kernels this library has launched in the process */
+uint64_t glb_kernel_launches(void);
 
 /* ---- graph (csr.py:42-118) ---- */
 /* Copies the host CSR (int64 row_offsets[n+1], col[m], weights[m] or NULL) into
@@ -141,6 +143,7 @@ int glb_graph_stream(const glb_graph* g, void** stream);
 
 /* ---- strategies (strategies/__init__.py:17-41) ---- */
 /* dist_out: caller-allocated int64[n]; INF is INT64_MAX (engine.py:27).
+ * dist_out may be NULL: the distances then stay in HBM (no device->host copy).
  * records may be NULL; *n_records is the capacity on input (ignored when
  * records is NULL) and stats->n_records the produced count on output.
  * EP over the COO budget returns GLB_OK with stats->status = GLB_ECOO_CAPACITY

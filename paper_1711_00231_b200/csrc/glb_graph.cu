@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstring>
 #include <mutex>
 #include <thread>
@@ -17,6 +18,8 @@ namespace glb {
 
 // ======================================================== error plumbing ===
 static thread_local std::string g_last_error;
+static std::atomic<unsigned long long> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 void set_error(const std::string& msg) { g_last_error = msg; }
 const char* last_error() { return g_last_error.c_str(); }
 
@@ -185,7 +188,7 @@ void graph_upload(glb_graph* g, const int64_t* row, const int64_t* col, const in
   upload_int64(g, row, g->n + 1, g->row, false, 0, 0, &ctrl->bad_input);
   upload_int64(g, col, g->m, g->col, true, (unsigned long long)g->n, 2u, &ctrl->bad_input);
   if (w) upload_int64(g, w, g->m, g->wt, true, 0x100000000ull, 4u, &ctrl->bad_input);
-  if (g->n > 0) {
+  {
     unsigned grid = grid_for(g->n, kBlock, g->num_sms * 8);
     k_check_rows<<<grid, kBlock, 0, g->stream>>>(g->row, g->n, g->m, &ctrl->bad_input, d_max);
     GLB_CHECK_LAUNCH();
@@ -664,6 +667,8 @@ extern "C" {
 
 const char* glb_last_error(void) { return glb::last_error(); }
 const char* glb_version(void) { return "graphlb_b200 0.1.0 (sm_100a)"; }
+
+uint64_t glb_kernel_launches(void) { return glb::g_launches.load(); }
 
 int glb_device_count(int* count) {
   return guarded([&] {

@@ -40,7 +40,14 @@ struct Error {
     }                                                                            \
   } while (0)
 
-#define GLB_CHECK_LAUNCH() GLB_CUDA_TRY(cudaGetLastError())
+// Every kernel launch site ends with GLB_CHECK_LAUNCH(): it surfaces launch
+// errors and counts the launch (glb_kernel_launches()).
+void count_launch();
+#define GLB_CHECK_LAUNCH()             \
+  do {                                 \
+    ::glb::count_launch();             \
+    GLB_CUDA_TRY(cudaGetLastError());  \
+  } while (0)
 
 // ------------------------------------------------------- distance traits ---
 template <typename D>

@@ -8,7 +8,7 @@
 //   k_ep_relax   edge-based (EP, edge_based.py:70-87): one thread per worklist
 //                edge over the COO source array; a successful relax appends
 //                the destination's whole out-edge range with ONE reservation
-//                (work chunking), written cooperatively by the warp.
+//                (work chunking), the ranges written cooperatively by warps.
 //   k_wd_scan +  workload decomposition (WD, workload.py:75-159): single-pass
 //   k_wd_relax   look-back scan of the frontier's remaining degrees (compacting
 //                away empty items and emitting the first item of every edge
@@ -17,6 +17,13 @@
 //   k_hp_window  hierarchical processing (HP, hierarchical.py:95-120): window
 //                [s*mdt, (s+1)*mdt) of every sublist node, dispatched at CTA /
 //                warp / thread granularity by window length.
+//
+// Every relaxation goes through relax_batch<K>: K independent edges per
+// thread are gathered first (col/weight loads), then their dist[dst] loads,
+// then the atomicMin / stamp claims, so a thread keeps K loads in flight
+// instead of one dependent chain.  Improved destinations go to a per-CTA
+// shared-memory queue flushed with ONE global reservation per CTA round --
+// the worklist cursor of worklist.py:107-130 without a global hot spot.
 //
 // Every kernel reads its worklist size from device memory (*nin) and strides
 // over it, so the same kernels run under the host loop and the device-driven
@@ -30,6 +37,52 @@
 
 namespace glb {
 
+// ------------------------------------------------------- CTA push queue ---
+constexpr int kQCap = 2048;
+struct BlockQ {          // control words; the items live in a separate smem array
+  uint32_t* items;       // kQCap entries
+  unsigned int count;
+  unsigned int base;
+};
+
+__device__ __forceinline__ void bq_init(BlockQ& q, uint32_t* items) {
+  if (threadIdx.x == 0) {
+    q.items = items;
+    q.count = 0;
+  }
+  __syncthreads();
+}
+
+// Warp-aggregated slot reservation in the CTA queue; overflow goes straight
+// to the global worklist.
+__device__ __forceinline__ void bq_push(BlockQ& q, uint32_t* qout, unsigned int* nout,
+                                        uint32_t v) {
+  const unsigned mask = __activemask();
+  const unsigned leader = __ffs(mask) - 1;
+  const unsigned rank = __popc(mask & ((1u << lane_id()) - 1u));
+  unsigned base = 0;
+  if (lane_id() == leader) base = atomicAdd(&q.count, (unsigned)__popc(mask));
+  base = __shfl_sync(mask, base, leader) + rank;
+  if (base < (unsigned)kQCap)
+    q.items[base] = v;
+  else
+    qout[atomicAdd(nout, 1u)] = v;
+}
+
+// All threads of the CTA: one global reservation, coalesced copy-out.
+__device__ __forceinline__ void bq_flush(BlockQ& q, uint32_t* qout, unsigned int* nout) {
+  __syncthreads();
+  const unsigned n = q.count < (unsigned)kQCap ? q.count : (unsigned)kQCap;
+  if (threadIdx.x == 0) q.base = n ? atomicAdd(nout, n) : 0u;
+  __syncthreads();
+  const unsigned b = q.base;
+  const uint32_t* items = q.items;
+  for (unsigned i = threadIdx.x; i < n; i += blockDim.x) qout[b + i] = items[i];
+  __syncthreads();
+  if (threadIdx.x == 0) q.count = 0;
+  __syncthreads();
+}
+
 // --------------------------------------------------------- relax helper ---
 template <typename D, bool W>
 struct Relaxer {
@@ -41,29 +94,98 @@ struct Relaxer {
   uint32_t* qout;
   unsigned int* nout;
   unsigned int* ovf;
+};
 
-  // Relax edge e out of a node at distance dn (dn != INF). Returns the
-  // destination when its distance strictly decreased.
-  __device__ __forceinline__ bool edge(long long e, D dn, ThreadCounters& c, uint32_t& v,
-                                       D& cand) const {
-    v = __ldcs(col + e);
-    ++c.work;
-    ++c.relax;
-    if (!make_cand<D>(dn, W ? __ldcs(wt + e) : 1u, cand, ovf)) return false;
-    return relax_min(dist, v, cand);
-  }
-  __device__ __forceinline__ void push(uint32_t v, ThreadCounters& c) const {
-    if (claim(stamp, v, gen)) {
-      q_append(qout, nout, v);
+// Relax up to K edges (bit k of `valid`: e[k] out of a node at distance
+// dn[k] != INF).  Returns the mask of edges whose atomicMin strictly lowered
+// dist[v[k]] to cand[k] (atomic_relax_min, engine.py:120-139); the ones that
+// also won the stamp claim were pushed to the CTA queue.
+template <int K, typename D, bool W>
+__device__ __forceinline__ unsigned relax_batch(const Relaxer<D, W>& rx, BlockQ& bq,
+                                                const long long (&e)[K], const D (&dn)[K],
+                                                unsigned valid, ThreadCounters& c,
+                                                uint32_t (&v)[K], D (&cand)[K]) {
+  uint32_t w[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k)
+    if (valid >> k & 1u) {
+      v[k] = __ldcs(rx.col + e[k]);
+      w[k] = W ? __ldcs(rx.wt + e[k]) : 1u;
+    }
+  D cur[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k)
+    if (valid >> k & 1u) cur[k] = rx.dist[v[k]];
+  unsigned want = 0;
+#pragma unroll
+  for (int k = 0; k < K; ++k)
+    if (valid >> k & 1u) {
+      ++c.work;
+      ++c.relax;
+      if (make_cand<D>(dn[k], w[k], cand[k], rx.ovf) && cand[k] < cur[k]) want |= 1u << k;
+    }
+  D old[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k)
+    if (want >> k & 1u) old[k] = atomicMin(rx.dist + v[k], cand[k]);
+  unsigned won = 0;
+#pragma unroll
+  for (int k = 0; k < K; ++k)
+    if ((want >> k & 1u) && cand[k] < old[k]) won |= 1u << k;
+  unsigned prev[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k)
+    if (won >> k & 1u) prev[k] = atomicExch(rx.stamp + v[k], rx.gen);
+#pragma unroll
+  for (int k = 0; k < K; ++k)
+    if ((won >> k & 1u) && prev[k] != rx.gen) {
+      bq_push(bq, rx.qout, rx.nout, v[k]);
       ++c.push;
     }
+  return won;
+}
+
+// Serial walk over [lo, hi) by one thread in batches of K.
+template <int K, typename D, bool W>
+__device__ __forceinline__ void relax_range_thread(const Relaxer<D, W>& rx, BlockQ& bq,
+                                                   long long lo, long long hi, D dn,
+                                                   ThreadCounters& c) {
+  for (long long b = lo; b < hi; b += K) {
+    long long e[K];
+    D d[K];
+    unsigned valid = 0;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      e[k] = b + k;
+      d[k] = dn;
+      if (b + k < hi) valid |= 1u << k;
+    }
+    uint32_t v[K];
+    D cand[K];
+    relax_batch<K>(rx, bq, e, d, valid, c, v, cand);
   }
-  __device__ __forceinline__ void edge_push(long long e, D dn, ThreadCounters& c) const {
-    uint32_t v;
-    D cand;
-    if (edge(e, dn, c, v, cand)) push(v, c);
+}
+
+// Cooperative walk over [lo, hi) by `width` threads (rank r), K per thread.
+template <int K, typename D, bool W>
+__device__ __forceinline__ void relax_range_coop(const Relaxer<D, W>& rx, BlockQ& bq,
+                                                 long long lo, long long hi, D dn, int r,
+                                                 int width, ThreadCounters& c) {
+  for (long long b = lo; b < hi; b += (long long)K * width) {
+    long long e[K];
+    D d[K];
+    unsigned valid = 0;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      e[k] = b + (long long)k * width + r;
+      d[k] = dn;
+      if (e[k] < hi) valid |= 1u << k;
+    }
+    uint32_t v[K];
+    D cand[K];
+    relax_batch<K>(rx, bq, e, d, valid, c, v, cand);
   }
-};
+}
 
 // ============================================================ BS (K1) ===
 template <typename D, bool W>
@@ -71,14 +193,19 @@ __global__ void __launch_bounds__(kBlock) k_bs_relax(const long long* __restrict
                                                      Relaxer<D, W> rx,
                                                      const uint32_t* __restrict__ qin,
                                                      const unsigned int* nin, LaunchStats* ls) {
+  __shared__ uint32_t s_q[kQCap];
+  __shared__ BlockQ bq;
+  bq_init(bq, s_q);
   ThreadCounters c;
   const unsigned n = *nin;
-  for (unsigned i = blockIdx.x * kBlock + threadIdx.x; i < n; i += gridDim.x * kBlock) {
-    uint32_t u = qin[i];
-    D du = rx.dist[u];
-    if (du == DistTraits<D>::kInf) continue;
-    long long lo = row[u], hi = row[u + 1];
-    for (long long e = lo; e < hi; ++e) rx.edge_push(e, du, c);
+  for (unsigned base = blockIdx.x * kBlock; base < n; base += gridDim.x * kBlock) {
+    const unsigned i = base + threadIdx.x;
+    if (i < n) {
+      const uint32_t u = qin[i];
+      const D du = rx.dist[u];
+      if (du != DistTraits<D>::kInf) relax_range_thread<4>(rx, bq, row[u], row[u + 1], du, c);
+    }
+    bq_flush(bq, rx.qout, rx.nout);
   }
   flush_counters(ls, c);
 }
@@ -91,83 +218,163 @@ __global__ void __launch_bounds__(kBlock) k_ns_relax(const long long* __restrict
                                                      long long n_orig, Relaxer<D, W> rx,
                                                      const uint32_t* __restrict__ qin,
                                                      const unsigned int* nin, LaunchStats* ls) {
+  __shared__ uint32_t s_q[kQCap];
+  __shared__ BlockQ bq;
+  bq_init(bq, s_q);
   ThreadCounters c;
   const unsigned n = *nin;
-  for (unsigned i = blockIdx.x * kBlock + threadIdx.x; i < n; i += gridDim.x * kBlock) {
-    uint32_t u = qin[i];
-    D du = rx.dist[u];
-    if (du == DistTraits<D>::kInf) continue;
-    long long lo = row[u], hi = row[u + 1];
-    for (long long e = lo; e < hi; ++e) {
-      uint32_t v;
-      D cand;
-      if (!rx.edge(e, du, c, v, cand)) continue;
-      rx.push(v, c);
-      if (v < n_orig) {
-        // reflect the parent's value onto its children (splitting.py:154-160)
-        const long long k1 = cs[v + 1];
-        for (long long k = cs[v]; k < k1; ++k) {
-          uint32_t child = (uint32_t)(n_orig + k);
-          ++c.relax;
-          relax_min(rx.dist, child, cand);
-          rx.push(child, c);
+  constexpr int K = 4;
+  for (unsigned base = blockIdx.x * kBlock; base < n; base += gridDim.x * kBlock) {
+    const unsigned i = base + threadIdx.x;
+    if (i < n) {
+      const uint32_t u = qin[i];
+      const D du = rx.dist[u];
+      if (du != DistTraits<D>::kInf) {
+        const long long lo = row[u], hi = row[u + 1];
+        for (long long b = lo; b < hi; b += K) {
+          long long e[K];
+          D d[K];
+          unsigned valid = 0;
+#pragma unroll
+          for (int k = 0; k < K; ++k) {
+            e[k] = b + k;
+            d[k] = du;
+            if (b + k < hi) valid |= 1u << k;
+          }
+          uint32_t v[K];
+          D cand[K];
+          unsigned won = relax_batch<K>(rx, bq, e, d, valid, c, v, cand);
+          // reflect each improved parent's value onto its children (splitting.py:154-160)
+#pragma unroll
+          for (int k = 0; k < K; ++k) {
+            if (!(won >> k & 1u) || v[k] >= n_orig) continue;
+            const long long k1 = cs[v[k] + 1];
+            for (long long ch = cs[v[k]]; ch < k1; ++ch) {
+              const uint32_t child = (uint32_t)(n_orig + ch);
+              ++c.relax;
+              relax_min(rx.dist, child, cand[k]);
+              if (claim(rx.stamp, child, rx.gen)) {
+                bq_push(bq, rx.qout, rx.nout, child);
+                ++c.push;
+              }
+            }
+          }
         }
       }
     }
+    bq_flush(bq, rx.qout, rx.nout);
   }
   flush_counters(ls, c);
 }
 
 // ============================================================ EP (K2) ===
+// Edge worklist; improved destinations reserve their whole out-edge range.
+// Ranges are collected per CTA (one global reservation per CTA round) and
+// written by warps, lanes on consecutive slots.
+constexpr int kEpRanges = 1024;
+struct EpRanges {
+  long long lo[kEpRanges];
+  unsigned int len[kEpRanges];
+  unsigned int off[kEpRanges];
+  unsigned int count;
+  unsigned int total;
+  unsigned int base;
+};
+
 template <typename D, bool W, bool CHUNKED>
 __global__ void __launch_bounds__(kBlock) k_ep_relax(const long long* __restrict__ row,
                                                      const uint32_t* __restrict__ src,
                                                      Relaxer<D, W> rx,
                                                      const uint32_t* __restrict__ qin,
                                                      const unsigned int* nin, LaunchStats* ls) {
+  __shared__ EpRanges rg;
+  if (threadIdx.x == 0) rg.count = rg.total = 0;
+  __syncthreads();
   ThreadCounters c;
   const unsigned n = *nin;
-  const unsigned lane = lane_id();
-  for (unsigned base = blockIdx.x * kBlock + (threadIdx.x & ~31u); base < n;
-       base += gridDim.x * kBlock) {
-    unsigned i = base + lane;
-    long long plo = 0;
-    unsigned pdeg = 0;
-    if (i < n) {
-      uint32_t e = qin[i];
-      ++c.work;
-      D du = rx.dist[__ldcs(src + e)];
-      if (du != DistTraits<D>::kInf) {
-        uint32_t v = __ldcs(rx.col + e);
+  constexpr int K = 4;
+  const unsigned stride = gridDim.x * kBlock;
+  for (unsigned base = blockIdx.x * kBlock; base < n; base += stride * K) {
+    uint32_t e[K], u[K], v[K], w[K];
+    D du[K], cur[K], cand[K];
+    unsigned valid = 0;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const unsigned i = base + k * stride + threadIdx.x;
+      if (i < n) {
+        valid |= 1u << k;
+        e[k] = qin[i];
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+      if (valid >> k & 1u) {
+        u[k] = __ldcs(src + e[k]);
+        v[k] = __ldcs(rx.col + e[k]);
+        w[k] = W ? __ldcs(rx.wt + e[k]) : 1u;
+      }
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+      if (valid >> k & 1u) {
+        du[k] = rx.dist[u[k]];
+        cur[k] = rx.dist[v[k]];
+      }
+    unsigned want = 0;
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+      if (valid >> k & 1u) {
+        ++c.work;
+        if (du[k] == DistTraits<D>::kInf) continue;
         ++c.relax;
-        D cand;
-        if (make_cand<D>(du, W ? __ldcs(rx.wt + e) : 1u, cand, rx.ovf) &&
-            relax_min(rx.dist, v, cand) && claim(rx.stamp, v, rx.gen)) {
-          plo = row[v];
-          pdeg = (unsigned)(row[v + 1] - plo);
-        }
+        if (make_cand<D>(du[k], w[k], cand[k], rx.ovf) && cand[k] < cur[k]) want |= 1u << k;
       }
-    }
-    unsigned slot = 0;
-    if (CHUNKED && pdeg > 0) {  // one reservation for the whole range (worklist.py:84-104)
-      slot = atomicAdd(rx.nout, pdeg);
-      ++c.push;
-    }
-    unsigned ball = __ballot_sync(0xffffffffu, pdeg > 0);
-    while (ball) {
-      int leader = __ffs(ball) - 1;
-      ball &= ball - 1;
-      long long lo = __shfl_sync(0xffffffffu, plo, leader);
-      unsigned dg = __shfl_sync(0xffffffffu, pdeg, leader);
-      unsigned sl = __shfl_sync(0xffffffffu, slot, leader);
-      for (unsigned k = lane; k < dg; k += 32) {
-        unsigned s = sl + k;
-        if (!CHUNKED) {
-          s = atomicAdd(rx.nout, 1u);
+    D old[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+      if (want >> k & 1u) old[k] = atomicMin(rx.dist + v[k], cand[k]);
+    unsigned prev[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+      if ((want >> k & 1u) && cand[k] < old[k]) prev[k] = atomicExch(rx.stamp + v[k], rx.gen);
+      else want &= ~(1u << k);
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      if (!(want >> k & 1u) || prev[k] == rx.gen) continue;
+      const long long lo = row[v[k]];
+      const unsigned len = (unsigned)(row[v[k] + 1] - lo);
+      if (len == 0) continue;
+      if (CHUNKED) {  // one reservation for the whole range (worklist.py:84-104)
+        ++c.push;
+        const unsigned slot = atomicAdd(&rg.count, 1u);
+        if (slot < (unsigned)kEpRanges) {
+          rg.lo[slot] = lo;
+          rg.len[slot] = len;
+          rg.off[slot] = atomicAdd(&rg.total, len);
+        } else {
+          const unsigned g = atomicAdd(rx.nout, len);
+          for (unsigned j = 0; j < len; ++j) rx.qout[g + j] = (uint32_t)(lo + j);
+        }
+      } else {  // one reservation per edge
+        for (unsigned j = 0; j < len; ++j) {
           ++c.push;
+          rx.qout[atomicAdd(rx.nout, 1u)] = (uint32_t)(lo + j);
         }
-        rx.qout[s] = (uint32_t)(lo + k);
       }
+    }
+    if (CHUNKED) {
+      __syncthreads();
+      const unsigned nr = rg.count < (unsigned)kEpRanges ? rg.count : (unsigned)kEpRanges;
+      if (threadIdx.x == 0) rg.base = rg.total ? atomicAdd(rx.nout, rg.total) : 0u;
+      __syncthreads();
+      const unsigned gb = rg.base;
+      for (unsigned r = threadIdx.x >> 5; r < nr; r += kBlock / 32) {
+        const long long lo = rg.lo[r];
+        const unsigned len = rg.len[r], off = gb + rg.off[r];
+        for (unsigned j = lane_id(); j < len; j += 32) rx.qout[off + j] = (uint32_t)(lo + j);
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) rg.count = rg.total = 0;
+      __syncthreads();
     }
   }
   flush_counters(ls, c);
@@ -202,15 +409,27 @@ __global__ void __launch_bounds__(kBlock) k_wd_scan(
     uint32_t v[kWdIPT];
     long long beg[kWdIPT], rem[kWdIPT];
     Vec<2> sum;
+    if (first + kWdIPT <= n) {  // 128-bit load of 4 worklist items
+      const uint4 q4 = *reinterpret_cast<const uint4*>(q + first);
+      v[0] = q4.x; v[1] = q4.y; v[2] = q4.z; v[3] = q4.w;
+    } else {
+#pragma unroll
+      for (int k = 0; k < kWdIPT; ++k) v[k] = first + k < n ? q[first + k] : 0u;
+    }
+    long long lo[kWdIPT], hi[kWdIPT];
+#pragma unroll
+    for (int k = 0; k < kWdIPT; ++k)
+      if (first + k < n) {
+        lo[k] = row[v[k]];
+        hi[k] = row[v[k] + 1];
+      }
 #pragma unroll
     for (int k = 0; k < kWdIPT; ++k) {
       rem[k] = 0;
       if (first + k < n) {
-        v[k] = q[first + k];
-        long long lo = row[v[k]], hi = row[v[k] + 1];
-        long long b = hi - lo < window ? hi - lo : window;
-        beg[k] = lo + b;
-        rem[k] = hi - lo - b;
+        long long b = hi[k] - lo[k] < window ? hi[k] - lo[k] : window;
+        beg[k] = lo[k] + b;
+        rem[k] = hi[k] - lo[k] - b;
       }
       sum.w[0] += rem[k];
       sum.w[1] += rem[k] > 0;
@@ -249,10 +468,13 @@ __global__ void __launch_bounds__(kBlock) k_wd_relax(Relaxer<D, W> rx,
                                                      const unsigned int* __restrict__ tile_first,
                                                      const DevCtrl* ctrl, LaunchStats* ls) {
   using BScan = cub::BlockScan<int, kBlock, cub::BLOCK_SCAN_WARP_SCANS>;
-  __shared__ __align__(16) int s_own[kWdTile];
+  static_assert(kQCap == kWdTile, "the CTA queue reuses the owner array");
+  __shared__ __align__(16) int s_own[kWdTile];  // owners, then the push queue
   __shared__ long long s_base[kWdTile + 1];
   __shared__ D s_dn[kWdTile + 1];
   __shared__ typename BScan::TempStorage s_scan;
+  __shared__ BlockQ bq;
+  bq_init(bq, reinterpret_cast<uint32_t*>(s_own));
   ThreadCounters c;
   const long long total = ctrl->wd_total;
   const long long nitems = ctrl->wd_items;
@@ -267,8 +489,8 @@ __global__ void __launch_bounds__(kBlock) k_wd_relax(Relaxer<D, W> rx,
     for (int k = threadIdx.x; k < kWdTile / 4; k += kBlock) own4[k] = make_int4(0, 0, 0, 0);
     __syncthreads();
     for (int k = threadIdx.x; k < cnt; k += kBlock) {
-      long long j = j0 + k;
-      long long pre = c_pre[j];
+      const long long j = j0 + k;
+      const long long pre = c_pre[j];
       s_base[k] = c_base[j];
       s_dn[k] = rx.dist[c_node[j]];  // dn read when the node is entered (workload.py:131,140)
       long long h = pre - e0;
@@ -280,7 +502,7 @@ __global__ void __launch_bounds__(kBlock) k_wd_relax(Relaxer<D, W> rx,
     int loc[kWdEPT];
     {
       const int4* p = reinterpret_cast<const int4*>(s_own + threadIdx.x * kWdEPT);
-      int4 a = p[0], bb = p[1];
+      const int4 a = p[0], bb = p[1];
       loc[0] = a.x; loc[1] = a.y; loc[2] = a.z; loc[3] = a.w;
       loc[4] = bb.x; loc[5] = bb.y; loc[6] = bb.z; loc[7] = bb.w;
     }
@@ -301,21 +523,29 @@ __global__ void __launch_bounds__(kBlock) k_wd_relax(Relaxer<D, W> rx,
       p[1] = make_int4(loc[4], loc[5], loc[6], loc[7]);
     }
     __syncthreads();
-#pragma unroll 4
+    // this thread's edges: e0 + k*kBlock + tid (lanes on consecutive edges)
+    long long e[kWdEPT];
+    D dn[kWdEPT];
+    unsigned valid = 0;
+#pragma unroll
     for (int k = 0; k < kWdEPT; ++k) {
-      int local = k * kBlock + threadIdx.x;
-      long long e = e0 + local;
-      if (e < e1) {
-        int o = s_own[local];
-        D dn = s_dn[o];
-        if (dn != DistTraits<D>::kInf) {
-          rx.edge_push(s_base[o] + e, dn, c);
-        } else {
+      const int local = k * kBlock + threadIdx.x;
+      const long long ee = e0 + local;
+      if (ee < e1) {
+        const int o = s_own[local];
+        dn[k] = s_dn[o];
+        e[k] = s_base[o] + ee;
+        if (dn[k] != DistTraits<D>::kInf)
+          valid |= 1u << k;
+        else
           ++c.work;
-        }
       }
     }
-    __syncthreads();
+    __syncthreads();  // owners consumed: s_own becomes the push queue
+    uint32_t v[kWdEPT];
+    D cand[kWdEPT];
+    relax_batch<kWdEPT>(rx, bq, e, dn, valid, c, v, cand);
+    bq_flush(bq, rx.qout, rx.nout);
   }
   flush_counters(ls, c);
 }
@@ -334,19 +564,22 @@ __global__ void __launch_bounds__(kBlock) k_hp_window(const long long* __restric
   __shared__ long long s_lo, s_hi;
   __shared__ D s_dn;
   __shared__ int s_owner;
+  __shared__ uint32_t s_q[kQCap];
+  __shared__ BlockQ bq;
+  bq_init(bq, s_q);
   ThreadCounters c;
   const long long n = *nin;
   for (long long base = blockIdx.x * (long long)kBlock; base < n;
        base += (long long)gridDim.x * kBlock) {
-    long long i = base + threadIdx.x;
+    const long long i = base + threadIdx.x;
     long long lo = 0, hi = 0;
     D dn = DistTraits<D>::kInf;
     if (i < n) {
-      uint32_t u = qin[i];
-      long long r0 = row[u], r1 = row[u + 1];
-      long long start = r0 + window;
+      const uint32_t u = qin[i];
+      const long long r0 = row[u], r1 = row[u + 1];
+      const long long start = r0 + window;
       if (start < r1) {
-        long long end = start + mdt < r1 ? start + mdt : r1;
+        const long long end = start + mdt < r1 ? start + mdt : r1;
         dn = rx.dist[u];
         if (dn != DistTraits<D>::kInf) {
           lo = start;
@@ -373,10 +606,8 @@ __global__ void __launch_bounds__(kBlock) k_hp_window(const long long* __restric
         lo = hi;
       }
       __syncthreads();
-      const long long clo = s_lo, chi = s_hi;
-      const D cdn = s_dn;
-      for (long long e = clo + threadIdx.x; e < chi; e += kBlock) rx.edge_push(e, cdn, c);
-      __syncthreads();
+      relax_range_coop<4>(rx, bq, s_lo, s_hi, s_dn, threadIdx.x, kBlock, c);
+      bq_flush(bq, rx.qout, rx.nout);
     }
     // warp granularity
     unsigned ball;
@@ -386,10 +617,11 @@ __global__ void __launch_bounds__(kBlock) k_hp_window(const long long* __restric
       const long long whi = __shfl_sync(0xffffffffu, hi, leader);
       const D wdn = __shfl_sync(0xffffffffu, dn, leader);
       if ((int)lane_id() == leader) lo = hi;
-      for (long long e = wlo + lane_id(); e < whi; e += 32) rx.edge_push(e, wdn, c);
+      relax_range_coop<2>(rx, bq, wlo, whi, wdn, lane_id(), 32, c);
     }
     // thread granularity
-    for (long long e = lo; e < hi; ++e) rx.edge_push(e, dn, c);
+    relax_range_thread<4>(rx, bq, lo, hi, dn, c);
+    bq_flush(bq, rx.qout, rx.nout);
   }
   flush_counters(ls, c);
 }

@@ -75,42 +75,67 @@ struct TileScan {
     Vec<NW> incl;
   };
 
+  __device__ __forceinline__ static Vec<NW> warp_sum(Vec<NW> v) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1)
+#pragma unroll
+      for (int i = 0; i < NW; ++i) v.w[i] += __shfl_xor_sync(0xffffffffu, v.w[i], off);
+    return v;
+  }
+
   __device__ __forceinline__ static Vec<NW> run(Storage& st, const LookbackState<NW>& lb,
                                                  unsigned epoch, long long tile,
                                                  const Vec<NW>& thread_sum,
                                                  Vec<NW>& tile_incl) {
     Vec<NW> thread_ex, block_total;
     BlockScan(st.scan).ExclusiveScan(thread_sum, thread_ex, Vec<NW>(), VecSum(), block_total);
-    if (threadIdx.x == 0) {
+    if (threadIdx.x < 32) {
+      const unsigned lane = threadIdx.x;
       Vec<NW> prefix;
       if (tile == 0) {
-        st_vec_cg(lb.incls, block_total);
-        __threadfence();
-        atomicExch(lb.flags, (epoch << 2) | kTileIncl);
+        if (lane == 0) {
+          st_vec_cg(lb.incls, block_total);
+          __threadfence();
+          atomicExch(lb.flags, (epoch << 2) | kTileIncl);
+        }
       } else {
-        st_vec_cg(lb.aggs + tile, block_total);
-        __threadfence();
-        atomicExch(lb.flags + tile, (epoch << 2) | kTileAgg);
+        if (lane == 0) {
+          st_vec_cg(lb.aggs + tile, block_total);
+          __threadfence();
+          atomicExch(lb.flags + tile, (epoch << 2) | kTileAgg);
+        }
+        // warp-parallel look-back: lane l inspects predecessor p - l
         long long p = tile - 1;
         while (true) {
-          unsigned f;
-          do {
-            f = *((volatile unsigned int*)(lb.flags + p));
-          } while ((f >> 2) != epoch);
-          __threadfence();
-          if ((f & 3u) == kTileIncl) {
-            prefix = ld_vec_cg(lb.incls + p) + prefix;
-            break;
+          const long long q = p - (long long)lane;
+          unsigned f = (epoch << 2) | kTileIncl;  // q < 0: virtual inclusive zero
+          if (q >= 0) {
+            do {
+              f = *((volatile unsigned int*)(lb.flags + q));
+            } while ((f >> 2) != epoch);
           }
-          prefix = ld_vec_cg(lb.aggs + p) + prefix;
-          --p;
+          __threadfence();
+          const unsigned incl_mask = __ballot_sync(0xffffffffu, (f & 3u) == kTileIncl);
+          const int stop = incl_mask ? __ffs(incl_mask) - 1 : 32;
+          Vec<NW> val;
+          if ((int)lane < stop)
+            val = ld_vec_cg(lb.aggs + q);
+          else if ((int)lane == stop && q >= 0)
+            val = ld_vec_cg(lb.incls + q);
+          prefix = prefix + warp_sum(val);
+          if (incl_mask) break;
+          p -= 32;
         }
-        st_vec_cg(lb.incls + tile, prefix + block_total);
-        __threadfence();
-        atomicExch(lb.flags + tile, (epoch << 2) | kTileIncl);
+        if (lane == 0) {
+          st_vec_cg(lb.incls + tile, prefix + block_total);
+          __threadfence();
+          atomicExch(lb.flags + tile, (epoch << 2) | kTileIncl);
+        }
       }
-      st.prefix = prefix;
-      st.incl = prefix + block_total;
+      if (lane == 0) {
+        st.prefix = prefix;
+        st.incl = prefix + block_total;
+      }
     }
     __syncthreads();
     Vec<NW> r = st.prefix + thread_ex;
