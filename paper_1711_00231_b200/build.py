@@ -21,6 +21,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
          "-Xptxas", "-warn-spills", "-diag-suppress", "20054"]
 SOURCES = ["glb_graph.cu", "glb_driver.cu"]
+EXTRA = os.environ.get("GLB_EXTRA_FLAGS", "").split()
 
 
 def _digest() -> str:
@@ -28,7 +29,7 @@ def _digest() -> str:
     for p in sorted(CSRC.glob("*")) + [HERE.parent / "include" / "graphlb_b200.h"]:
         h.update(p.name.encode())
         h.update(p.read_bytes())
-    h.update(" ".join(ARCH + FLAGS).encode())
+    h.update(" ".join(ARCH + FLAGS + EXTRA).encode())
     return h.hexdigest()
 
 
@@ -41,7 +42,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     objs = []
     for src in SOURCES:
         obj = BUILD / (Path(src).stem + ".o")
-        cmd = [NVCC, *ARCH, *FLAGS, "-c", str(CSRC / src), "-o", str(obj)]
+        cmd = [NVCC, *ARCH, *FLAGS, *EXTRA, "-c", str(CSRC / src), "-o", str(obj)]
         if verbose:
             print(" ".join(cmd), flush=True)
         subprocess.run(cmd, check=True)

@@ -1,0 +1,210 @@
+// glb_control.cuh -- the strategy drivers' host loops (node_based.py:33-80,
+// edge_based.py:58-100, workload.py:175-189, splitting.py:129-175,
+// hierarchical.py:54-136) restated as a device-side state machine.
+//
+// k_control_init picks the first step; k_control runs after every step: it
+// turns the step's counters into a record, rotates the worklists, advances
+// the stamp generation and decides the next step -- including HP's choice
+// between a window sub-iteration and the WD fallback.  Under the CUDA-graph
+// loop it also drives the conditional WHILE (continue?) and SWITCH (which
+// step kernels?) nodes, so a whole traversal runs without the host.
+#pragma once
+
+#include "glb_internal.cuh"
+
+namespace glb {
+
+__device__ __forceinline__ void ctl_simple_advance(DevCtrl* c) {
+  // wl_in.clear(); swap(wl_in, wl_out)  (node_based.py:75-79)
+  const unsigned produced = c->qcount[c->out];
+  c->qcount[c->in] = 0;
+  const int t = c->in;
+  c->in = c->out;
+  c->out = t;
+  c->gen += 1;
+  c->iteration += 1;
+  c->done = produced == 0;
+}
+
+__device__ __forceinline__ void hp_decide_sub(DevCtrl* c);
+
+__device__ __forceinline__ void hp_begin_super(DevCtrl* c) {
+  c->qcount[c->sup_out] = 0;
+  const unsigned n = c->qcount[c->sup_in];
+  if (c->hp_fallback && (long long)n < c->hp_threshold) {  // hierarchical.py:55-61
+    c->mode = kModeWD;
+    c->tag = GLB_TAG_WD_FALLBACK;
+    c->in = c->sup_in;
+    c->out = c->sup_out;
+    c->window = 0;
+    c->sub = -1;
+  } else {
+    c->cur = c->sup_in;
+    c->spare = 2;
+    c->s = 0;
+    hp_decide_sub(c);
+  }
+}
+
+__device__ __forceinline__ void hp_end_super(DevCtrl* c) {
+  // super_in.clear(); swap(super_in, super_out)  (hierarchical.py:134-137)
+  const unsigned produced = c->qcount[c->sup_out];
+  c->qcount[c->sup_in] = 0;
+  const int t = c->sup_in;
+  c->sup_in = c->sup_out;
+  c->sup_out = t;
+  c->gen += 1;
+  c->iteration += 1;
+  if (produced == 0) {
+    c->done = 1;
+    c->mode = kModeDone;
+  } else {
+    hp_begin_super(c);
+  }
+}
+
+__device__ __forceinline__ void hp_decide_sub(DevCtrl* c) {
+  const unsigned n = c->qcount[c->cur];
+  if (n == 0) {
+    hp_end_super(c);
+    return;
+  }
+  c->in = c->cur;
+  c->out = c->sup_out;
+  c->window = c->s * c->mdt;
+  c->sub = (int)c->s;
+  if (c->hp_fallback && c->s > 0 && (long long)n < c->hp_threshold) {  // hierarchical.py:67-81
+    c->mode = kModeWD;
+    c->tag = GLB_TAG_WD_FALLBACK;
+  } else {
+    c->mode = kModeHP;
+    c->tag = GLB_HP;
+    c->next = c->spare;
+    c->qcount[c->spare] = 0;
+  }
+}
+
+__device__ __forceinline__ void ctl_set_conditionals(DevCtrl* c, cudaGraphConditionalHandle h_loop,
+                                                     cudaGraphConditionalHandle h_mode,
+                                                     int graph_mode) {
+  if (graph_mode) {
+    cudaGraphSetConditional(h_loop, c->done ? 0u : 1u);
+    if (h_mode) cudaGraphSetConditional(h_mode, (unsigned)c->mode);
+  }
+}
+
+__device__ __forceinline__ void ctl_reset_timers(DevCtrl* c) {
+  c->t_relax.start = c->t_scan.start = ~0ull;
+  c->t_relax.end = c->t_scan.end = 0;
+  c->scan_ticket = c->relax_ticket = 0;
+}
+
+// The host has written the static fields (qptr, strategy, mdt, thresholds,
+// thread counts, record buffer, stamp generation base, scan epoch) and the
+// seed kernel has filled list 0.
+__global__ void k_control_init(DevCtrl* c, cudaGraphConditionalHandle h_loop,
+                               cudaGraphConditionalHandle h_mode, int graph_mode) {
+  if (threadIdx.x != 0) return;
+  const int strategy = c->strategy;
+  c->in = 0;
+  c->out = 1;
+  c->next = 2;
+  c->qcount[1] = c->qcount[2] = c->qcount[3] = 0;
+  c->gen += 1;
+  c->iteration = 0;
+  c->sub = -1;
+  c->window = 0;
+  c->done = c->qcount[0] == 0;
+  c->nrec = 0;
+  ctl_reset_timers(c);
+  switch (strategy) {
+    case GLB_WD:
+      c->mode = kModeWD;
+      c->tag = GLB_WD;
+      break;
+    case GLB_HP:
+      c->sup_in = 0;
+      c->sup_out = 1;
+      hp_begin_super(c);
+      break;
+    default:
+      c->mode = kModeRelax;
+      c->tag = strategy;
+      break;
+  }
+  if (c->done) c->mode = kModeDone;
+  ctl_set_conditionals(c, h_loop, h_mode, graph_mode);
+}
+
+// One warp: reduce the step's counters into a record, then transition.
+__global__ void k_control(DevCtrl* c, cudaGraphConditionalHandle h_loop,
+                          cudaGraphConditionalHandle h_mode, int graph_mode) {
+  const unsigned lane = threadIdx.x;
+  StatSlot& sl = c->ls->slot[lane];
+  unsigned long long w = sl.work, r = sl.relax, p = sl.push, mx = sl.work_max;
+  double sq = (double)sl.work_sq;
+  sl.work = sl.relax = sl.push = sl.work_sq = sl.work_max = 0;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    w += __shfl_xor_sync(0xffffffffu, w, off);
+    r += __shfl_xor_sync(0xffffffffu, r, off);
+    p += __shfl_xor_sync(0xffffffffu, p, off);
+    sq += __shfl_xor_sync(0xffffffffu, sq, off);
+    const unsigned long long o = __shfl_xor_sync(0xffffffffu, mx, off);
+    mx = o > mx ? o : mx;
+  }
+  if (lane != 0) return;
+  if (c->done) {  // nothing ran (already finished)
+    ctl_set_conditionals(c, h_loop, h_mode, graph_mode);
+    return;
+  }
+  const bool wd_empty = c->mode == kModeWD && c->wd_total == 0;
+  if (!wd_empty && c->nrec < c->rec_cap) {  // decompose_invocation returns None: no record
+    DevRecord& rec = c->recs[c->nrec];
+    rec.iteration = c->iteration;
+    rec.sub = c->sub;
+    rec.tag = c->tag;
+    rec.active = c->qcount[c->in];
+    rec.threads = c->mode == kModeHP ? c->hp_threads : c->relax_threads;
+    rec.work = (long long)w;
+    rec.relax = (long long)r;
+    rec.push = (long long)p;
+    rec.work_max = (long long)mx;
+    rec.work_sumsq = sq;
+    rec.k0 = c->t_relax.start;
+    rec.k1 = c->t_relax.end;
+    rec.o0 = c->mode == kModeWD ? c->t_scan.start : 0;
+    rec.o1 = c->mode == kModeWD ? c->t_scan.end : 0;
+  }
+  if (!wd_empty) c->nrec += 1;
+  if (c->mode == kModeWD) c->scan_epoch += 1;
+  ctl_reset_timers(c);
+  switch (c->strategy) {
+    case GLB_WD:
+      if (wd_empty) {  // active nodes have no out-edges (workload.py:181-183)
+        c->done = 1;
+      } else {
+        ctl_simple_advance(c);
+      }
+      break;
+    case GLB_HP:
+      if (c->mode == kModeWD) {
+        if (c->in != c->sup_in) c->qcount[c->in] = 0;
+        hp_end_super(c);
+      } else {  // window sub-iteration: unfinished nodes form the next sublist
+        if (c->cur != c->sup_in) c->qcount[c->cur] = 0;
+        c->cur = c->spare;
+        c->spare = c->cur == 2 ? 3 : 2;
+        c->s += 1;
+        hp_decide_sub(c);
+      }
+      break;
+    default:
+      ctl_simple_advance(c);
+      break;
+  }
+  if (c->done) c->mode = kModeDone;
+  ctl_set_conditionals(c, h_loop, h_mode, graph_mode);
+}
+
+}  // namespace glb

@@ -1,15 +1,25 @@
-// glb_driver.cu -- strategy drivers behind glb_run (run_strategy,
-// strategies/__init__.py:17-41).  Each driver restates the reference's host
-// loop ("while the worklist is non-empty: launch, swap") over device-resident
-// worklists; only the worklist sizes cross back to the host, once per launch.
+// glb_driver.cu -- glb_run (run_strategy, strategies/__init__.py:17-41).
+//
+// A run = per-run preprocessing (histogram/MDT, split, COO: the reference's
+// "setup overhead"), distance init + seed, then the strategy loop, then the
+// int64 distances.  The loop is the device state machine of glb_control.cuh
+// driven either
+//   * by the host (GLB_LOOP_HOST): launch the step's kernels + k_control,
+//     read the control block back, repeat -- exact per-launch CUDA events; or
+//   * by the device (GLB_LOOP_GRAPH): one CUDA graph whose conditional WHILE
+//     node repeats [step kernels, k_control] and whose SWITCH node picks the
+//     HP step kind, so the host launches the whole traversal once.
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
+#include <sstream>
 #include <vector>
 
+#include "glb_control.cuh"
 #include "glb_internal.cuh"
 #include "glb_relax.cuh"
 #include "glb_scan.cuh"
@@ -23,7 +33,7 @@ void histogram(glb_graph* g, const long long* row, long long n, unsigned long lo
 
 namespace {
 
-constexpr int kStatRing = 64;  // LaunchStats slots cycled by the host loop
+constexpr unsigned kMaxRecords = 1u << 16;
 
 struct OverflowRestart {};  // a u32 candidate reached INF: re-run in u64
 
@@ -33,17 +43,15 @@ double now_ms() {
       .count();
 }
 
-void* ensure_zero(DevBuf& b, size_t bytes, cudaStream_t s, bool* fresh = nullptr) {
-  bool grow = b.bytes < (bytes ? bytes : 16);
+void* ensure_zero(DevBuf& b, size_t bytes, cudaStream_t s) {
+  const bool grow = b.bytes < (bytes ? bytes : 16);
   void* p = ensure(b, bytes);
   if (grow) GLB_CUDA_TRY(cudaMemsetAsync(p, 0, b.bytes, s));
-  if (fresh) *fresh = grow;
   return p;
 }
 
 struct HostMirror {  // pinned layout of g->host_ctrl
   DevCtrl ctrl;
-  LaunchStats stats[2];
 };
 
 template <typename D, bool W>
@@ -52,18 +60,16 @@ class Runner {
   Runner(glb_graph* g, const glb_run_params& p, std::vector<glb_record>& recs)
       : g_(g), p_(p), recs_(recs), s_(g->stream) {}
 
-  // Returns the number of output distances written to dist_out.
   void run(int64_t* dist_out, glb_run_stats* st) {
-    double t_setup0 = now_ms();
+    const double t0 = now_ms();
     GLB_CUDA_TRY(cudaEventRecord(g_->ev[0], s_));
     n_out_ = g_->n;
     row_ = g_->row;
     col_ = g_->col;
     wt_ = g_->wt;
     n_all_ = g_->n;
-    mdt_ = 0;
     const int strat = p_.strategy;
-    if (strat == GLB_NS || strat == GLB_HP) {
+    if (strat == GLB_NS || strat == GLB_HP) {  // splitting.py:112-113, hierarchical.py:38-39
       if (p_.mdt > 0) {
         mdt_ = p_.mdt;
       } else {
@@ -85,34 +91,33 @@ class Runner {
       st->num_split_nodes = tot[3];
       st->split_fraction = g_->n ? (double)tot[3] / (double)g_->n : 0.0;
     }
-    if (strat == GLB_EP) {
+    if (strat == GLB_EP) {  // csr_to_coo inside run_ep (edge_based.py:41)
       src_ = (uint32_t*)ensure(g_->ws.ep_src, (size_t)std::max<long long>(g_->m, 1) * 4);
       coo_src(g_, src_);
     }
     alloc_state();
-    setup_ms_ = now_ms() - t_setup0;
+    setup_ms_ = now_ms() - t0;
 
-    switch (strat) {
-      case GLB_BS: loop_node(false); break;
-      case GLB_NS: loop_node(true); break;
-      case GLB_EP: loop_ep(); break;
-      case GLB_WD: loop_wd(); break;
-      case GLB_HP: loop_hp(); break;
-      default: throw Error{GLB_EINVAL, "unknown strategy"};
-    }
+    if (p_.loop_mode == GLB_LOOP_GRAPH)
+      loop_graph();
+    else
+      loop_host();
 
     long long* out = (long long*)ensure(g_->ws.out64, (size_t)std::max<long long>(n_out_, 1) * 8);
-    if (n_out_ > 0) {
-      k_dist_out<D><<<grid_for(n_out_, kBlock, g_->num_sms * 8), kBlock, 0, s_>>>(dist_, n_out_,
-                                                                                   out);
-      GLB_CHECK_LAUNCH();
-    }
+    k_dist_out<D><<<grid_for(n_out_, kBlock, g_->num_sms * 8), kBlock, 0, s_>>>(cells_, n_out_,
+                                                                                  out);
+    GLB_CHECK_LAUNCH();
     GLB_CUDA_TRY(cudaEventRecord(g_->ev[1], s_));
+    GLB_CUDA_TRY(cudaMemcpyAsync(&h_->ctrl, ctrl_, sizeof(DevCtrl), cudaMemcpyDeviceToHost, s_));
     if (n_out_ > 0 && dist_out)
       GLB_CUDA_TRY(cudaMemcpyAsync(dist_out, out, (size_t)n_out_ * 8, cudaMemcpyDeviceToHost, s_));
     GLB_CUDA_TRY(cudaStreamSynchronize(s_));
+    if (h_->ctrl.overflow) throw OverflowRestart{};
+    g_->stamp_epoch = h_->ctrl.gen;
+    g_->scan_epoch = h_->ctrl.scan_epoch;
     float dev_ms = 0;
     GLB_CUDA_TRY(cudaEventElapsedTime(&dev_ms, g_->ev[0], g_->ev[1]));
+    collect_records();
     finish(st, dev_ms);
   }
 
@@ -127,21 +132,33 @@ class Runner {
   const uint32_t* wt_ = nullptr;
   const long long* cs_ = nullptr;
   uint32_t* src_ = nullptr;
-  D* dist_ = nullptr;
+  unsigned long long* cells_ = nullptr;
   uint32_t* stamp_ = nullptr;
   uint32_t* q_[4] = {nullptr, nullptr, nullptr, nullptr};
   DevCtrl* ctrl_ = nullptr;
-  LaunchStats* ring_ = nullptr;
+  LaunchStats* ls_ = nullptr;
+  DevRecord* drecs_ = nullptr;
   HostMirror* h_ = nullptr;
-  int ring_next_ = 0;
+  // WD workspace
+  long long* c_pre_ = nullptr;
+  long long* c_base_ = nullptr;
+  D* c_dn_ = nullptr;
+  unsigned* tile_first_ = nullptr;
+  LookbackState<2> lb_{};
+  // grids
+  int cap_relax_ = 0, cap_scan_ = 0, cap_wd_ = 0, cap_hp_ = 0;
   double setup_ms_ = 0;
-  double kernel_ms_ = 0;
-  long long iterations_ = 0;
-  // per-launch timing events (pairs), reused from g->ev_pool
+  long long seed_count_ = 0;
+  // host-loop per-record event timing
+  struct EvPair {
+    cudaEvent_t k0, k1, o0, o1;
+    long long threads;
+  };
+  std::vector<EvPair> ev_of_rec_;
   size_t ev_used_ = 0;
 
   cudaEvent_t event() {
-    if (ev_used_ == g_->ev_pool.size()) {
+    while (ev_used_ >= g_->ev_pool.size()) {
       cudaEvent_t e;
       GLB_CUDA_TRY(cudaEventCreate(&e));
       g_->ev_pool.push_back(e);
@@ -149,325 +166,404 @@ class Runner {
     return g_->ev_pool[ev_used_++];
   }
 
+  int cap(const void* kernel) { return max_resident_blocks(kernel, kBlock, 0, g_->num_sms); }
+
+  const void* relax_kernel() const {
+    switch (p_.strategy) {
+      case GLB_BS: return (const void*)k_bs_relax<D, W>;
+      case GLB_NS: return (const void*)k_ns_relax<D, W>;
+      case GLB_EP:
+        return p_.chunked ? (const void*)k_ep_relax<D, W, true> : (const void*)k_ep_relax<D, W, false>;
+      default: return nullptr;
+    }
+  }
+
   void alloc_state() {
     Workspace& ws = g_->ws;
-    size_t nb = (size_t)std::max<long long>(n_all_, 1);
-    dist_ = (D*)ensure(ws.dist, nb * sizeof(D));
-    bool fresh = false;
-    stamp_ = (uint32_t*)ensure_zero(ws.stamp, nb * 4, s_, &fresh);
+    const size_t nb = (size_t)std::max<long long>(n_all_, 1);
+    cells_ = (unsigned long long*)ensure(ws.dist, nb * 8);
+    stamp_ = (uint32_t*)ensure_zero(ws.stamp, nb * 4, s_);
     if (g_->stamp_epoch > 0xF0000000u) {
       GLB_CUDA_TRY(cudaMemsetAsync(stamp_, 0, ws.stamp.bytes, s_));
       g_->stamp_epoch = 0;
     }
     if (p_.strategy == GLB_EP) {
-      size_t eb = (size_t)std::max<long long>(g_->m, 1) * 4;
+      const size_t eb = (size_t)std::max<long long>(g_->m, 1) * 4;
       q_[0] = (uint32_t*)ensure(ws.eq[0], eb);
       q_[1] = (uint32_t*)ensure(ws.eq[1], eb);
+      q_[2] = q_[3] = q_[1];
     } else {
-      int nq = p_.strategy == GLB_HP ? 4 : 2;
-      for (int i = 0; i < nq; ++i) q_[i] = (uint32_t*)ensure(ws.q[i], nb * 4);
+      for (int i = 0; i < 4; ++i)
+        q_[i] = (i < 2 || p_.strategy == GLB_HP) ? (uint32_t*)ensure(ws.q[i], nb * 4) : q_[1];
     }
+    if (p_.strategy == GLB_WD || p_.strategy == GLB_HP) {
+      c_pre_ = (long long*)ensure(ws.c_pre, nb * 8);
+      c_base_ = (long long*)ensure(ws.c_base, nb * 8);
+      c_dn_ = (D*)ensure(ws.c_node, nb * sizeof(D));
+      const long long max_tiles = (g_->m + kWdTile - 1) / kWdTile + 2;
+      tile_first_ = (unsigned*)ensure(ws.tile_first, (size_t)max_tiles * 4);
+      const long long stiles = ((long long)nb + kWdScanTile - 1) / kWdScanTile + 1;
+      unsigned* flags = (unsigned*)ensure_zero(ws.scan_flags, (size_t)stiles * 4 + 4096, s_);
+      const size_t vb = (size_t)stiles * sizeof(Vec<2>);
+      char* vals = (char*)ensure(ws.scan_vals, 2 * vb + 4096);
+      lb_ = LookbackState<2>{flags, (Vec<2>*)vals, (Vec<2>*)(vals + vb)};
+      cap_scan_ = cap((const void*)k_wd_scan<D>);
+      cap_wd_ = cap((const void*)k_wd_relax<D, W>);
+    }
+    if (p_.strategy == GLB_HP) cap_hp_ = std::max(cap((const void*)k_hp_window<D, W>), g_->num_sms);
+    if (relax_kernel()) cap_relax_ = std::max(cap(relax_kernel()), g_->num_sms);
+    pin_cells_in_l2(nb * 8);
     ctrl_ = (DevCtrl*)ensure(ws.ctrl, sizeof(DevCtrl));
-    ring_ = (LaunchStats*)ensure(ws.stats, sizeof(LaunchStats) * kStatRing);
+    ls_ = (LaunchStats*)ensure_zero(ws.stats, sizeof(LaunchStats), s_);
+    drecs_ = (DevRecord*)ensure(ws.recs, sizeof(DevRecord) * kMaxRecords);
     h_ = (HostMirror*)g_->host_ctrl;
-    GLB_CUDA_TRY(cudaMemsetAsync(ctrl_, 0, sizeof(DevCtrl), s_));
+
+    // static fields of the control block
+    DevCtrl c;
+    std::memset(&c, 0, sizeof(c));
+    for (int i = 0; i < 4; ++i) c.qptr[i] = q_[i];
+    c.strategy = p_.strategy;
+    c.mdt = mdt_;
+    c.hp_threshold = p_.block_size;
+    c.hp_fallback = p_.hp_fallback ? 1 : 0;
+    c.relax_threads =
+        (long long)(p_.strategy == GLB_WD || p_.strategy == GLB_HP ? cap_wd_ : cap_relax_) * kBlock;
+    c.hp_threads = (long long)cap_hp_ * kBlock;
+    c.gen = g_->stamp_epoch;
+    c.scan_epoch = g_->scan_epoch + 1;
+    c.rec_cap = kMaxRecords;
+    c.recs = drecs_;
+    c.ls = ls_;
+    h_->ctrl = c;
+    GLB_CUDA_TRY(cudaMemcpyAsync(ctrl_, &h_->ctrl, sizeof(DevCtrl), cudaMemcpyHostToDevice, s_));
+
     // distances: INF everywhere, then the seeds
     k_init_dist<D><<<grid_for((long long)nb, kBlock, g_->num_sms * 8), kBlock, 0, s_>>>(
-        dist_, (long long)nb);
+        cells_, (long long)nb);
     GLB_CHECK_LAUNCH();
-    long long src = p_.source;
+    const long long src = p_.source;
     long long klo = 0, khi = 0, elo = 0, ehi = 0;
-    bool edges = p_.strategy == GLB_EP;
+    const bool edges = p_.strategy == GLB_EP;
     long long seeds = 1;
-    if (p_.strategy == GLB_NS) {
+    if (p_.strategy == GLB_NS || edges) {
       long long h2[2];
-      GLB_CUDA_TRY(cudaMemcpyAsync(h2, cs_ + src, 16, cudaMemcpyDeviceToHost, s_));
+      GLB_CUDA_TRY(cudaMemcpyAsync(h2, (edges ? row_ : cs_) + src, 16, cudaMemcpyDeviceToHost, s_));
       GLB_CUDA_TRY(cudaStreamSynchronize(s_));
-      klo = g_->n + h2[0];
-      khi = g_->n + h2[1];
-      seeds = 1 + khi - klo;
-    }
-    if (edges) {
-      long long h2[2];
-      GLB_CUDA_TRY(cudaMemcpyAsync(h2, row_ + src, 16, cudaMemcpyDeviceToHost, s_));
-      GLB_CUDA_TRY(cudaStreamSynchronize(s_));
-      elo = h2[0];
-      ehi = h2[1];
-      seeds = ehi - elo;
+      if (edges) {
+        elo = h2[0];
+        ehi = h2[1];
+        seeds = ehi - elo;
+      } else {
+        klo = g_->n + h2[0];
+        khi = g_->n + h2[1];
+        seeds = 1 + khi - klo;
+      }
     }
     seed_count_ = seeds;
     k_seed<D><<<grid_for(std::max<long long>(seeds, 1), kBlock, g_->num_sms * 4), kBlock, 0, s_>>>(
-        dist_, q_[0], &ctrl_->qcount[0], src, klo, khi, elo, ehi, edges);
+        cells_, q_[0], &ctrl_->qcount[0], src, klo, khi, elo, ehi, edges);
     GLB_CHECK_LAUNCH();
   }
-  long long seed_count_ = 0;
 
-  LaunchStats* next_slot() {
-    LaunchStats* ls = ring_ + (ring_next_++ % kStatRing);
-    GLB_CUDA_TRY(cudaMemsetAsync(ls, 0, sizeof(LaunchStats), s_));
-    return ls;
+  // Keep the distance cells -- the randomly accessed array -- resident in L2
+  // (persisting access-policy window on the library stream; captured into
+  // the loop graph's kernel nodes).  Column / weight streams are loaded
+  // evict-first, so they do not displace it.
+  void pin_cells_in_l2(size_t bytes) {
+    if (!g_->l2_persist_max || !g_->l2_window_max || !getenv("GLB_L2_PERSIST")) return;
+    const size_t win = std::min(bytes, (size_t)g_->l2_window_max);
+    cudaStreamAttrValue attr;
+    std::memset(&attr, 0, sizeof(attr));
+    attr.accessPolicyWindow.base_ptr = (void*)cells_;
+    attr.accessPolicyWindow.num_bytes = win;
+    attr.accessPolicyWindow.hitRatio =
+        (float)std::min(1.0, (double)g_->l2_persist_max / (double)win);
+    attr.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    attr.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    if (cudaStreamSetAttribute(s_, cudaStreamAttributeAccessPolicyWindow, &attr) != cudaSuccess)
+      cudaGetLastError();  // advisory only
   }
 
-  Relaxer<D, W> relaxer(uint32_t gen, uint32_t* qout, unsigned* nout) {
+  Relaxer<D, W> relaxer() const {
     Relaxer<D, W> rx;
     rx.col = col_;
     rx.wt = wt_;
-    rx.dist = dist_;
+    rx.cells = cells_;
     rx.stamp = stamp_;
-    rx.gen = gen;
-    rx.qout = qout;
-    rx.nout = nout;
+    rx.gen = 0;
+    rx.qout = nullptr;
+    rx.nout = nullptr;
     rx.ovf = &ctrl_->overflow;
     return rx;
   }
 
-  int cap(const void* kernel) { return max_resident_blocks(kernel, kBlock, 0, g_->num_sms); }
+  // ------------------------------------------------------ step launches ---
+  void launch_relax(unsigned grid) {
+    const Relaxer<D, W> rx = relaxer();
+    switch (p_.strategy) {
+      case GLB_BS: k_bs_relax<D, W><<<grid, kBlock, 0, s_>>>(row_, rx, ctrl_); break;
+      case GLB_NS: k_ns_relax<D, W><<<grid, kBlock, 0, s_>>>(row_, cs_, g_->n, rx, ctrl_); break;
+      case GLB_EP:
+        if (p_.chunked)
+          k_ep_relax<D, W, true><<<grid, kBlock, 0, s_>>>(row_, src_, rx, ctrl_);
+        else
+          k_ep_relax<D, W, false><<<grid, kBlock, 0, s_>>>(row_, src_, rx, ctrl_);
+        break;
+      default: throw Error{GLB_EINVAL, "no relax kernel for this strategy"};
+    }
+    GLB_CHECK_LAUNCH();
+  }
+  void launch_wd_scan(unsigned grid) {
+    k_wd_scan<D><<<grid, kBlock, 0, s_>>>(row_, cells_, lb_, c_pre_, c_base_, c_dn_, tile_first_,
+                                          ctrl_);
+    GLB_CHECK_LAUNCH();
+  }
+  void launch_wd_relax(unsigned grid) {
+    k_wd_relax<D, W><<<grid, kBlock, 0, s_>>>(relaxer(), c_pre_, c_base_, c_dn_, tile_first_,
+                                               ctrl_);
+    GLB_CHECK_LAUNCH();
+  }
+  void launch_hp(unsigned grid) {
+    k_hp_window<D, W><<<grid, kBlock, 0, s_>>>(row_, relaxer(), ctrl_);
+    GLB_CHECK_LAUNCH();
+  }
+  void launch_control(cudaGraphConditionalHandle hl, cudaGraphConditionalHandle hm, int gm) {
+    k_control<<<1, 32, 0, s_>>>(ctrl_, hl, hm, gm);
+    GLB_CHECK_LAUNCH();
+  }
 
-  // Bring back the control block and the launch's counters (one round trip).
-  void sync_back(LaunchStats* ls) {
+  void read_ctrl() {
     GLB_CUDA_TRY(cudaMemcpyAsync(&h_->ctrl, ctrl_, sizeof(DevCtrl), cudaMemcpyDeviceToHost, s_));
-    if (ls)
-      GLB_CUDA_TRY(cudaMemcpyAsync(&h_->stats[0], ls, sizeof(LaunchStats), cudaMemcpyDeviceToHost,
-                                   s_));
     GLB_CUDA_TRY(cudaStreamSynchronize(s_));
     if (h_->ctrl.overflow) throw OverflowRestart{};
   }
 
-  void add_record(int it, int sub, int tag, long long active, long long threads, cudaEvent_t k0,
-                  cudaEvent_t k1, cudaEvent_t o0, cudaEvent_t o1) {
-    glb_record r;
-    std::memset(&r, 0, sizeof(r));
-    r.iteration = it;
-    r.sub_iteration = sub;
-    r.tag = tag;
-    r.active_items = active;
-    r.threads = threads;
-    const LaunchStats& ls = h_->stats[0];
-    double sq = 0;
-    for (int i = 0; i < kStatSlots; ++i) {
-      const StatSlot& s = ls.slot[i];
-      r.work_total += (int64_t)s.work;
-      r.relax_ops += (int64_t)s.relax;
-      r.push_ops += (int64_t)s.push;
-      sq += (double)s.work_sq;
-      r.work_max = std::max<int64_t>(r.work_max, (int64_t)s.work_max);
-    }
-    r.work_sumsq = sq;
-    float ms = 0;
-    if (k0 && k1 && cudaEventElapsedTime(&ms, k0, k1) == cudaSuccess) r.kernel_ms = ms;
-    if (o0 && o1 && cudaEventElapsedTime(&ms, o0, o1) == cudaSuccess) r.overhead_ms = ms;
-    kernel_ms_ += r.kernel_ms;
-    recs_.push_back(r);
-  }
-
-  uint32_t next_gen() { return ++g_->stamp_epoch; }
-
-  // ---------------------------------------------------------- BS / NS ---
-  void loop_node(bool ns) {
-    const void* kfn = ns ? (const void*)k_ns_relax<D, W> : (const void*)k_bs_relax<D, W>;
-    const int kcap = std::max(cap(kfn), g_->num_sms * 8);
-    int in = 0;
-    long long h_in = seed_count_;
-    int it = 0;
-    while (h_in > 0) {
-      const int out = in ^ 1;
-      uint32_t gen = next_gen();
-      GLB_CUDA_TRY(cudaMemsetAsync(&ctrl_->qcount[out], 0, 4, s_));
-      LaunchStats* ls = next_slot();
-      unsigned grid = grid_for(h_in, kBlock, kcap);
-      Relaxer<D, W> rx = relaxer(gen, q_[out], &ctrl_->qcount[out]);
-      cudaEvent_t k0 = event(), k1 = event();
-      GLB_CUDA_TRY(cudaEventRecord(k0, s_));
-      if (ns)
-        k_ns_relax<D, W><<<grid, kBlock, 0, s_>>>(row_, cs_, g_->n, rx, q_[in], &ctrl_->qcount[in],
-                                                  ls);
-      else
-        k_bs_relax<D, W><<<grid, kBlock, 0, s_>>>(row_, rx, q_[in], &ctrl_->qcount[in], ls);
-      GLB_CHECK_LAUNCH();
-      GLB_CUDA_TRY(cudaEventRecord(k1, s_));
-      sync_back(ls);
-      add_record(it, -1, ns ? GLB_NS : GLB_BS, h_in, (long long)grid * kBlock, k0, k1, nullptr,
-                 nullptr);
-      ev_used_ = 0;
-      h_in = h_->ctrl.qcount[out];
-      in = out;
-      ++it;
-    }
-    iterations_ = it;
-  }
-
-  // --------------------------------------------------------------- EP ---
-  void loop_ep() {
-    const void* kfn = p_.chunked ? (const void*)k_ep_relax<D, W, true>
-                                 : (const void*)k_ep_relax<D, W, false>;
-    const int kcap = std::max(cap(kfn), g_->num_sms * 8);
-    int in = 0;
-    long long h_in = seed_count_;
-    int it = 0;
-    while (h_in > 0) {
-      const int out = in ^ 1;
-      uint32_t gen = next_gen();
-      GLB_CUDA_TRY(cudaMemsetAsync(&ctrl_->qcount[out], 0, 4, s_));
-      LaunchStats* ls = next_slot();
-      unsigned grid = grid_for(h_in, kBlock, kcap);
-      Relaxer<D, W> rx = relaxer(gen, q_[out], &ctrl_->qcount[out]);
-      cudaEvent_t k0 = event(), k1 = event();
-      GLB_CUDA_TRY(cudaEventRecord(k0, s_));
-      if (p_.chunked)
-        k_ep_relax<D, W, true><<<grid, kBlock, 0, s_>>>(row_, src_, rx, q_[in],
-                                                        &ctrl_->qcount[in], ls);
-      else
-        k_ep_relax<D, W, false><<<grid, kBlock, 0, s_>>>(row_, src_, rx, q_[in],
-                                                         &ctrl_->qcount[in], ls);
-      GLB_CHECK_LAUNCH();
-      GLB_CUDA_TRY(cudaEventRecord(k1, s_));
-      sync_back(ls);
-      add_record(it, -1, GLB_EP, h_in, (long long)grid * kBlock, k0, k1, nullptr, nullptr);
-      ev_used_ = 0;
-      h_in = h_->ctrl.qcount[out];
-      in = out;
-      ++it;
-    }
-    iterations_ = it;
-  }
-
-  // --------------------------------------------------------------- WD ---
-  // One decomposition invocation (workload.py:75-159) over q_[in] with base
-  // offset `window`, pushing improved nodes to q_[out] (stamped `gen`).
-  // Returns false when the active nodes have no edges left (no record).
-  bool wd_invocation(int in, long long h_in, long long window, int out, uint32_t gen, int it,
-                     int sub, int tag) {
-    Workspace& ws = g_->ws;
-    size_t nb = (size_t)std::max<long long>(h_in, 1);
-    long long* c_pre = (long long*)ensure(ws.c_pre, (size_t)std::max<long long>(n_all_, 1) * 8);
-    long long* c_base = (long long*)ensure(ws.c_base, (size_t)std::max<long long>(n_all_, 1) * 8);
-    uint32_t* c_node = (uint32_t*)ensure(ws.c_node, (size_t)std::max<long long>(n_all_, 1) * 4);
-    long long max_tiles = (g_->m + kWdTile - 1) / kWdTile + 2;
-    unsigned* tile_first = (unsigned*)ensure(ws.tile_first, (size_t)max_tiles * 4);
-    long long stiles = ((long long)nb + kWdScanTile - 1) / kWdScanTile;
-    long long max_stiles = (std::max<long long>(n_all_, 1) + kWdScanTile - 1) / kWdScanTile + 1;
-    unsigned* flags = (unsigned*)ensure_zero(ws.scan_flags, (size_t)max_stiles * 4 + 4096, s_);
-    size_t vb = (size_t)max_stiles * sizeof(Vec<2>);
-    char* vals = (char*)ensure(ws.scan_vals, 2 * vb + 4096);
-    LookbackState<2> lb{flags, (Vec<2>*)vals, (Vec<2>*)(vals + vb)};
-    unsigned epoch = ++g_->scan_epoch;
-
-    cudaEvent_t o0 = event(), o1 = event(), k0 = event(), k1 = event();
-    GLB_CUDA_TRY(cudaEventRecord(o0, s_));
-    static int scan_cap = 0;
-    if (!scan_cap) scan_cap = cap((const void*)k_wd_scan);
-    k_wd_scan<<<grid_for(stiles, 1, scan_cap), kBlock, 0, s_>>>(
-        row_, q_[in], &ctrl_->qcount[in], window, lb, epoch, c_pre, c_base, c_node, tile_first,
-        ctrl_);
+  // ------------------------------------------------------- host loop ---
+  void loop_host() {
+    k_control_init<<<1, 32, 0, s_>>>(ctrl_, 0, 0, 0);
     GLB_CHECK_LAUNCH();
-    GLB_CUDA_TRY(cudaEventRecord(o1, s_));
-    LaunchStats* ls = next_slot();
-    Relaxer<D, W> rx = relaxer(gen, q_[out], &ctrl_->qcount[out]);
-    static int relax_cap = 0;
-    if (!relax_cap) relax_cap = cap((const void*)k_wd_relax<D, W>);
-    GLB_CUDA_TRY(cudaEventRecord(k0, s_));
-    k_wd_relax<D, W><<<relax_cap, kBlock, 0, s_>>>(rx, c_pre, c_base, c_node, tile_first, ctrl_, ls);
-    GLB_CHECK_LAUNCH();
-    GLB_CUDA_TRY(cudaEventRecord(k1, s_));
-    sync_back(ls);
-    if (h_->ctrl.wd_total == 0) return false;
-    add_record(it, sub, tag, h_in, (long long)relax_cap * kBlock, k0, k1, o0, o1);
-    return true;
-  }
-
-  void loop_wd() {
-    int in = 0;
-    long long h_in = seed_count_;
-    int it = 0;
-    while (h_in > 0) {
-      const int out = in ^ 1;
-      uint32_t gen = next_gen();
-      GLB_CUDA_TRY(cudaMemsetAsync(&ctrl_->qcount[out], 0, 4, s_));
-      bool ok = wd_invocation(in, h_in, 0, out, gen, it, -1, GLB_WD);
-      ev_used_ = 0;
-      if (!ok) break;  // active nodes have no out-edges (workload.py:181-183)
-      h_in = h_->ctrl.qcount[out];
-      in = out;
-      ++it;
-    }
-    iterations_ = it;
-  }
-
-  // --------------------------------------------------------------- HP ---
-  void loop_hp() {
-    const long long thr = p_.block_size;
-    const bool fb = p_.hp_fallback != 0;
-    const int kcap = std::max(cap((const void*)k_hp_window<D, W>), g_->num_sms * 8);
-    int sup_in = 0, sup_out = 1;
-    long long h_super = seed_count_;
-    int it = 0;
-    while (h_super > 0) {
-      uint32_t gen = next_gen();
-      GLB_CUDA_TRY(cudaMemsetAsync(&ctrl_->qcount[sup_out], 0, 4, s_));
-      if (fb && h_super < thr) {
-        wd_invocation(sup_in, h_super, 0, sup_out, gen, it, -1, GLB_TAG_WD_FALLBACK);
-      } else {
-        int cur = sup_in;
-        long long h_cur = h_super;
-        int spare = 2;
-        long long s = 0;
-        while (h_cur > 0) {
-          if (fb && s > 0 && h_cur < thr) {
-            wd_invocation(cur, h_cur, s * mdt_, sup_out, gen, it, (int)s, GLB_TAG_WD_FALLBACK);
-            break;
+    read_ctrl();
+    const bool timing = p_.record_timing != 0;
+    while (!h_->ctrl.done) {
+      const DevCtrl& c = h_->ctrl;
+      const long long n_in = c.qcount[c.in];
+      const unsigned nrec0 = c.nrec;
+      ev_used_ = ev_of_rec_.size() * 4;
+      EvPair ev{nullptr, nullptr, nullptr, nullptr, 0};
+      if (timing) {
+        ev.k0 = event();
+        ev.k1 = event();
+      }
+      switch (c.mode) {
+        case kModeRelax: {
+          const long long per = p_.strategy == GLB_EP ? 4LL * kBlock : kBlock;
+          const unsigned grid = grid_for(n_in, (int)per, cap_relax_);
+          ev.threads = (long long)grid * kBlock;
+          if (timing) GLB_CUDA_TRY(cudaEventRecord(ev.k0, s_));
+          launch_relax(grid);
+          if (timing) GLB_CUDA_TRY(cudaEventRecord(ev.k1, s_));
+          break;
+        }
+        case kModeWD: {
+          if (timing) {
+            ev.o0 = event();
+            ev.o1 = event();
+            GLB_CUDA_TRY(cudaEventRecord(ev.o0, s_));
           }
-          GLB_CUDA_TRY(cudaMemsetAsync(&ctrl_->qcount[spare], 0, 4, s_));
-          LaunchStats* ls = next_slot();
-          unsigned grid = grid_for(h_cur, kBlock, kcap);
-          Relaxer<D, W> rx = relaxer(gen, q_[sup_out], &ctrl_->qcount[sup_out]);
-          cudaEvent_t k0 = event(), k1 = event();
-          GLB_CUDA_TRY(cudaEventRecord(k0, s_));
-          k_hp_window<D, W><<<grid, kBlock, 0, s_>>>(row_, rx, q_[cur], &ctrl_->qcount[cur],
-                                                     s * mdt_, mdt_, q_[spare],
-                                                     &ctrl_->qcount[spare], ls);
-          GLB_CHECK_LAUNCH();
-          GLB_CUDA_TRY(cudaEventRecord(k1, s_));
-          sync_back(ls);
-          add_record(it, (int)s, GLB_HP, h_cur, (long long)grid * kBlock, k0, k1, nullptr,
-                     nullptr);
-          ev_used_ = 0;
-          h_cur = h_->ctrl.qcount[spare];
-          cur = spare;                   // the unfinished nodes form the next sublist
-          spare = (cur == 2) ? 3 : 2;    // sublists alternate (hierarchical.py:130-133)
-          ++s;
+          launch_wd_scan(grid_for(n_in, kWdScanTile, cap_scan_));
+          if (timing) GLB_CUDA_TRY(cudaEventRecord(ev.o1, s_));
+          if (timing) GLB_CUDA_TRY(cudaEventRecord(ev.k0, s_));
+          launch_wd_relax(cap_wd_);
+          if (timing) GLB_CUDA_TRY(cudaEventRecord(ev.k1, s_));
+          ev.threads = (long long)cap_wd_ * kBlock;
+          break;
+        }
+        case kModeHP: {
+          const unsigned grid = grid_for(n_in, kBlock, cap_hp_);
+          ev.threads = (long long)grid * kBlock;
+          if (timing) GLB_CUDA_TRY(cudaEventRecord(ev.k0, s_));
+          launch_hp(grid);
+          if (timing) GLB_CUDA_TRY(cudaEventRecord(ev.k1, s_));
+          break;
+        }
+        default: throw Error{GLB_ECUDA, "control block in an unknown mode"};
+      }
+      launch_control(0, 0, 0);
+      read_ctrl();
+      if (h_->ctrl.nrec > nrec0) ev_of_rec_.push_back(ev);
+    }
+  }
+
+  // ----------------------------------------------------- graph loop ---
+  std::string graph_key() const {
+    std::ostringstream k;
+    k << p_.strategy << '|' << sizeof(D) << '|' << W << '|' << p_.chunked << '|' << cap_relax_
+      << '|' << cap_scan_ << '|' << cap_wd_ << '|' << cap_hp_ << '|' << (const void*)row_ << '|'
+      << (const void*)col_ << '|' << (const void*)wt_ << '|' << (const void*)cs_ << '|'
+      << (const void*)src_ << '|' << (const void*)cells_ << '|' << (const void*)stamp_ << '|'
+      << (const void*)ctrl_ << '|' << (const void*)c_pre_ << '|' << (const void*)c_base_ << '|'
+      << (const void*)c_dn_ << '|' << (const void*)tile_first_ << '|'
+      << (const void*)lb_.flags << '|' << (const void*)lb_.aggs << '|' << g_->n;
+    return k.str();
+  }
+
+  void capture_into(cudaGraph_t graph, const cudaGraphNode_t* deps, size_t ndeps) {
+    GLB_CUDA_TRY(cudaStreamBeginCaptureToGraph(s_, graph, deps, nullptr, ndeps,
+                                               cudaStreamCaptureModeThreadLocal));
+  }
+  void end_capture() {
+    cudaGraph_t out = nullptr;
+    GLB_CUDA_TRY(cudaStreamEndCapture(s_, &out));
+  }
+  static cudaGraphNode_t only_node(cudaGraph_t graph) {
+    size_t n = 0;
+    GLB_CUDA_TRY(cudaGraphGetNodes(graph, nullptr, &n));
+    if (n != 1) throw Error{GLB_ECUDA, "unexpected node count while building the loop graph"};
+    cudaGraphNode_t node;
+    GLB_CUDA_TRY(cudaGraphGetNodes(graph, &node, &n));
+    return node;
+  }
+
+  cudaGraphExec_t build_graph() {
+    cudaGraph_t graph;
+    GLB_CUDA_TRY(cudaGraphCreate(&graph, 0));
+    try {
+      cudaGraphConditionalHandle h_loop = 0, h_mode = 0;
+      GLB_CUDA_TRY(cudaGraphConditionalHandleCreate(&h_loop, graph, 0, 0));
+      if (p_.strategy == GLB_HP)
+        GLB_CUDA_TRY(cudaGraphConditionalHandleCreate(&h_mode, graph, 0, 0));
+      capture_into(graph, nullptr, 0);
+      k_control_init<<<1, 32, 0, s_>>>(ctrl_, h_loop, h_mode, 1);
+      GLB_CHECK_LAUNCH();
+      end_capture();
+      cudaGraphNode_t init = only_node(graph);
+
+      alignas(cudaGraphNodeParams) unsigned char wbuf[sizeof(cudaGraphNodeParams)] = {};
+      cudaGraphNodeParams& wp = *reinterpret_cast<cudaGraphNodeParams*>(wbuf);
+      wp.type = cudaGraphNodeTypeConditional;
+      wp.conditional.handle = h_loop;
+      wp.conditional.type = cudaGraphCondTypeWhile;
+      wp.conditional.size = 1;
+      cudaGraphNode_t wnode;
+      GLB_CUDA_TRY(cudaGraphAddNode(&wnode, graph, &init, 1, &wp));
+      cudaGraph_t body = wp.conditional.phGraph_out[0];
+
+      if (p_.strategy == GLB_HP) {
+        alignas(cudaGraphNodeParams) unsigned char sbuf[sizeof(cudaGraphNodeParams)] = {};
+        cudaGraphNodeParams& sp = *reinterpret_cast<cudaGraphNodeParams*>(sbuf);
+        sp.type = cudaGraphNodeTypeConditional;
+        sp.conditional.handle = h_mode;
+        sp.conditional.type = cudaGraphCondTypeSwitch;
+        sp.conditional.size = 4;  // StepMode: done, relax, WD, HP
+        cudaGraphNode_t snode;
+        GLB_CUDA_TRY(cudaGraphAddNode(&snode, body, nullptr, 0, &sp));
+        cudaGraph_t b_wd = sp.conditional.phGraph_out[kModeWD];
+        cudaGraph_t b_hp = sp.conditional.phGraph_out[kModeHP];
+        capture_into(b_wd, nullptr, 0);
+        launch_wd_scan(cap_scan_);
+        launch_wd_relax(cap_wd_);
+        end_capture();
+        capture_into(b_hp, nullptr, 0);
+        launch_hp(cap_hp_);
+        end_capture();
+        capture_into(body, &snode, 1);
+      } else {
+        capture_into(body, nullptr, 0);
+        if (p_.strategy == GLB_WD) {
+          launch_wd_scan(cap_scan_);
+          launch_wd_relax(cap_wd_);
+        } else {
+          launch_relax(cap_relax_);
         }
       }
-      ev_used_ = 0;
-      // read the super-out size (already in h_ from the last sync_back)
-      GLB_CUDA_TRY(cudaMemcpyAsync(&h_->ctrl, ctrl_, sizeof(DevCtrl), cudaMemcpyDeviceToHost, s_));
-      GLB_CUDA_TRY(cudaStreamSynchronize(s_));
-      h_super = h_->ctrl.qcount[sup_out];
-      std::swap(sup_in, sup_out);
-      ++it;
+      launch_control(h_loop, h_mode, 1);
+      end_capture();
+      cudaGraphExec_t exec;
+      GLB_CUDA_TRY(cudaGraphInstantiate(&exec, graph, 0));
+      cudaGraphDestroy(graph);
+      return exec;
+    } catch (...) {
+      cudaStreamCaptureStatus cs;
+      if (cudaStreamIsCapturing(s_, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone) {
+        cudaGraph_t junk = nullptr;
+        cudaStreamEndCapture(s_, &junk);
+      }
+      cudaGetLastError();
+      cudaGraphDestroy(graph);
+      throw;
     }
-    iterations_ = it;
+  }
+
+  void loop_graph() {
+    const std::string key = graph_key();
+    cudaGraphExec_t exec = nullptr;
+    for (auto& kv : g_->gexec)
+      if (kv.first == key) exec = kv.second;
+    if (!exec) {
+      exec = build_graph();
+      g_->gexec.emplace_back(key, exec);
+    }
+    GLB_CUDA_TRY(cudaGraphLaunch(exec, s_));
+  }
+
+  // ---------------------------------------------------------- results ---
+  void collect_records() {
+    const unsigned n = std::min(h_->ctrl.nrec, kMaxRecords);
+    std::vector<DevRecord> dr(n);
+    if (n)
+      GLB_CUDA_TRY(cudaMemcpy(dr.data(), drecs_, sizeof(DevRecord) * n, cudaMemcpyDeviceToHost));
+    recs_.clear();
+    recs_.reserve(n);
+    for (unsigned i = 0; i < n; ++i) {
+      const DevRecord& d = dr[i];
+      glb_record r;
+      std::memset(&r, 0, sizeof(r));
+      r.iteration = d.iteration;
+      r.sub_iteration = d.sub;
+      r.tag = d.tag;
+      r.active_items = d.active;
+      r.threads = d.threads;
+      r.work_total = d.work;
+      r.work_max = d.work_max;
+      r.work_sumsq = d.work_sumsq;
+      r.relax_ops = d.relax;
+      r.push_ops = d.push;
+      r.kernel_ms = d.k1 > d.k0 && d.k0 != ~0ull ? (double)(d.k1 - d.k0) * 1e-6 : 0.0;
+      r.overhead_ms = d.o0 && d.o1 > d.o0 && d.o0 != ~0ull ? (double)(d.o1 - d.o0) * 1e-6 : 0.0;
+      if (i < ev_of_rec_.size()) {  // host loop: CUDA-event times and the exact grid
+        const EvPair& e = ev_of_rec_[i];
+        float ms = 0;
+        if (e.k0 && cudaEventElapsedTime(&ms, e.k0, e.k1) == cudaSuccess) r.kernel_ms = ms;
+        if (e.o0 && cudaEventElapsedTime(&ms, e.o0, e.o1) == cudaSuccess) r.overhead_ms = ms;
+        cudaGetLastError();
+        r.threads = e.threads;
+      }
+      recs_.push_back(r);
+    }
   }
 
   void finish(glb_run_stats* st, float dev_ms) {
     st->status = GLB_OK;
     st->dist_bits = (int)(sizeof(D) * 8);
-    st->iterations = iterations_;
+    st->iterations = h_->ctrl.iteration;
     st->launches = (int64_t)recs_.size();
     st->mdt = mdt_;
     st->sub_iterations = 0;
     st->relax_ops = st->push_ops = st->edges_examined = st->active_items = 0;
+    double kms = 0;
     for (const glb_record& r : recs_) {
       if (r.tag == GLB_HP) ++st->sub_iterations;
       st->relax_ops += r.relax_ops;
       st->push_ops += r.push_ops;
       st->edges_examined += r.work_total;
       st->active_items += r.active_items;
+      kms += r.kernel_ms;
     }
     st->device_ms = dev_ms;
-    st->kernel_ms = kernel_ms_;
-    st->overhead_ms = std::max(0.0, (double)dev_ms - kernel_ms_);
+    st->kernel_ms = kms;
+    st->overhead_ms = std::max(0.0, (double)dev_ms - kms);
     st->setup_ms = setup_ms_;
-    st->n_records = (int64_t)recs_.size();
+    st->n_records = (int64_t)h_->ctrl.nrec;
   }
 };
 
@@ -484,6 +580,29 @@ void run_typed(glb_graph* g, const glb_run_params& p, int64_t* dist_out, glb_run
   }
 }
 
+// An aborted run leaves stamps / look-back flags of generations the handle
+// never recorded; clear both so the next run cannot mistake them for its own.
+void reset_epochs(glb_graph* g) {
+  cudaStreamSynchronize(g->stream);
+  cudaGetLastError();
+  if (g->ws.stamp.p) cudaMemsetAsync(g->ws.stamp.p, 0, g->ws.stamp.bytes, g->stream);
+  if (g->ws.scan_flags.p) cudaMemsetAsync(g->ws.scan_flags.p, 0, g->ws.scan_flags.bytes, g->stream);
+  g->stamp_epoch = 0;
+  g->scan_epoch = 0;
+  cudaStreamSynchronize(g->stream);
+}
+
+template <typename D>
+void run_guarded(glb_graph* g, const glb_run_params& p, int64_t* dist_out, glb_run_stats* st,
+                 std::vector<glb_record>& recs) {
+  try {
+    run_typed<D>(g, p, dist_out, st, recs);
+  } catch (...) {
+    reset_epochs(g);
+    throw;
+  }
+}
+
 }  // namespace
 
 void run(glb_graph* g, const glb_run_params& p, int64_t* dist_out, glb_run_stats* st,
@@ -491,19 +610,24 @@ void run(glb_graph* g, const glb_run_params& p, int64_t* dist_out, glb_run_stats
   std::memset(st, 0, sizeof(*st));
   st->split_fraction = -1.0;
   if (p.dist_bits == 64) {
-    run_typed<unsigned long long>(g, p, dist_out, st, recs);
+    try {
+      run_guarded<unsigned long long>(g, p, dist_out, st, recs);
+    } catch (const OverflowRestart&) {
+      throw Error{GLB_EOVERFLOW, "distance exceeds the 63-bit range"};
+    }
     return;
   }
   try {
-    run_typed<uint32_t>(g, p, dist_out, st, recs);
+    run_guarded<uint32_t>(g, p, dist_out, st, recs);
   } catch (const OverflowRestart&) {
     if (p.dist_bits == 32) throw Error{GLB_EOVERFLOW, "distance exceeds the 32-bit range"};
     recs.clear();
+    const double sf = st->split_fraction;
     std::memset(st, 0, sizeof(*st));
-    st->split_fraction = -1.0;
+    st->split_fraction = sf;
     GLB_CUDA_TRY(cudaStreamSynchronize(g->stream));
     try {
-      run_typed<unsigned long long>(g, p, dist_out, st, recs);
+      run_guarded<unsigned long long>(g, p, dist_out, st, recs);
     } catch (const OverflowRestart&) {
       throw Error{GLB_EOVERFLOW, "distance exceeds the 63-bit range"};
     }
@@ -529,9 +653,11 @@ extern "C" int glb_run(glb_graph* g, const glb_run_params* params, int64_t* dist
     if (p.block_size < 1) throw glb::Error{GLB_EINVAL, "block_size must be >= 1"};
     if (p.dist_bits != 0 && p.dist_bits != 32 && p.dist_bits != 64)
       throw glb::Error{GLB_EINVAL, "dist_bits must be 0, 32 or 64"};
+    if (p.loop_mode != GLB_LOOP_HOST && p.loop_mode != GLB_LOOP_GRAPH)
+      throw glb::Error{GLB_EINVAL, "loop_mode must be GLB_LOOP_HOST or GLB_LOOP_GRAPH"};
     std::memset(stats, 0, sizeof(*stats));
     if (p.strategy == GLB_EP) {
-      long long required = (g->weighted ? 3 : 2) * g->m;
+      const long long required = (g->weighted ? 3 : 2) * g->m;
       if (required > p.max_cells) {  // csr.py:155-167 -> edge_based.py:41-46
         stats->status = GLB_ECOO_CAPACITY;
         stats->split_fraction = -1.0;
@@ -553,7 +679,7 @@ extern "C" int glb_run(glb_graph* g, const glb_run_params* params, int64_t* dist
     }
     if (prev >= 0) cudaSetDevice(prev);
     if (records) {
-      int64_t k = std::min<int64_t>(records_capacity, (int64_t)recs.size());
+      const int64_t k = std::min<int64_t>(records_capacity, (int64_t)recs.size());
       if (k > 0) std::memcpy(records, recs.data(), (size_t)k * sizeof(glb_record));
     }
     stats->n_records = (int64_t)recs.size();
@@ -575,8 +701,8 @@ extern "C" int glb_run_records(glb_graph* g, int64_t offset, glb_record* records
     return GLB_EINVAL;
   }
   std::lock_guard<std::mutex> lk(g->mu);
-  int64_t total = (int64_t)g->last_records.size();
-  int64_t k = offset >= total ? 0 : std::min<int64_t>(capacity, total - offset);
+  const int64_t total = (int64_t)g->last_records.size();
+  const int64_t k = offset >= total ? 0 : std::min<int64_t>(capacity, total - offset);
   if (k > 0) std::memcpy(records, g->last_records.data() + offset, (size_t)k * sizeof(glb_record));
   *written = k;
   return GLB_OK;

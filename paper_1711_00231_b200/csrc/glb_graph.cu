@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <thread>
@@ -13,6 +14,7 @@
 
 #include "glb_internal.cuh"
 #include "glb_scan.cuh"
+#include "glb_tiles.cuh"
 
 namespace glb {
 
@@ -218,26 +220,40 @@ __global__ void k_degree_sq(const long long* __restrict__ row, long long n,
   if ((threadIdx.x & 31) == 0 && acc) atomicAdd(sumsq_hi, acc);
 }
 
-// degree d > 0 -> bin ceil(d*B/max) (1-based), degree 0 -> bin 1 (degrees.py:55-60)
+// degree d > 0 -> bin ceil(d*B/max) (1-based), degree 0 -> bin 1 (degrees.py:55-60).
+// Lanes holding the same bin are merged with __match_any before the shared
+// atomic, so a 10-bin histogram does not serialise 32 lanes on one word.
 __global__ void k_histogram(const long long* __restrict__ row, long long n, int bins,
                             unsigned long long max_deg, unsigned long long* counts) {
   extern __shared__ unsigned long long s_cnt[];
-  bool smem = bins <= 4096;
+  const bool smem = bins <= 4096;
+  const bool narrow = max_deg <= (0x7FFFFFFFFFFFFFFFull / ((unsigned long long)bins + 1));
   if (smem)
     for (int b = threadIdx.x; b < bins; b += blockDim.x) s_cnt[b] = 0;
   __syncthreads();
-  for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; v < n;
-       v += (long long)gridDim.x * blockDim.x) {
-    unsigned long long d = (unsigned long long)(row[v + 1] - row[v]);
-    unsigned long long bin = 1;
-    if (max_deg > 0 && d > 0) {
-      unsigned __int128 num = (unsigned __int128)d * (unsigned)bins + (max_deg - 1);
-      bin = (unsigned long long)(num / max_deg);
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long base = blockIdx.x * (long long)blockDim.x; base < n; base += stride) {
+    const long long v = base + threadIdx.x;
+    unsigned long long bin = 0;  // 0 = no node
+    if (v < n) {
+      const unsigned long long d = (unsigned long long)(row[v + 1] - row[v]);
+      bin = 1;
+      if (max_deg > 0 && d > 0) {
+        if (narrow)
+          bin = (d * (unsigned)bins + (max_deg - 1)) / max_deg;
+        else
+          bin = (unsigned long long)(((unsigned __int128)d * (unsigned)bins + (max_deg - 1)) /
+                                     max_deg);
+      }
     }
-    if (smem)
-      atomicAdd(&s_cnt[bin - 1], 1ull);
-    else
-      atomicAdd(&counts[bin - 1], 1ull);
+    const unsigned peers = __match_any_sync(0xffffffffu, bin);
+    if (bin != 0 && (int)lane_id() == __ffs(peers) - 1) {
+      const unsigned long long c = (unsigned long long)__popc(peers);
+      if (smem)
+        atomicAdd(&s_cnt[bin - 1], c);
+      else
+        atomicAdd(&counts[bin - 1], c);
+    }
   }
   __syncthreads();
   if (smem)
@@ -264,16 +280,11 @@ void degree_stats(glb_graph* g, int64_t* max_degree, int64_t* sum_degree, double
 
 void histogram(glb_graph* g, const long long* row, long long n, unsigned long long max_deg,
                int bins, int64_t* counts_out, int32_t* arg_max_bin, int64_t* mdt) {
-  DevBuf& buf = g->ws.misc;
-  // misc may hold upload staging; histogram needs its own small area
-  static_assert(sizeof(unsigned long long) == 8, "");
-  DevBuf tmp;
-  unsigned long long* d_counts = (unsigned long long*)ensure(tmp, (size_t)bins * 8);
-  (void)buf;
-  try {
+  unsigned long long* d_counts = (unsigned long long*)ensure(g->ws.hist, (size_t)bins * 8);
+  {
     GLB_CUDA_TRY(cudaMemsetAsync(d_counts, 0, (size_t)bins * 8, g->stream));
     if (n > 0) {
-      unsigned grid = grid_for(n, kBlock, g->num_sms * 4);
+      unsigned grid = grid_for(n, kBlock, g->num_sms * 8);
       size_t smem = bins <= 4096 ? (size_t)bins * 8 : 0;
       k_histogram<<<grid, kBlock, smem, g->stream>>>(row, n, bins, max_deg, d_counts);
       GLB_CHECK_LAUNCH();
@@ -282,7 +293,6 @@ void histogram(glb_graph* g, const long long* row, long long n, unsigned long lo
     GLB_CUDA_TRY(cudaMemcpyAsync(h.data(), d_counts, (size_t)bins * 8, cudaMemcpyDeviceToHost,
                                  g->stream));
     GLB_CUDA_TRY(cudaStreamSynchronize(g->stream));
-    free_buf(tmp);
     // first argmax (degrees.py:62) and mdt = max(1, bin*max // B) (degrees.py:72-76)
     int arg = 0;
     for (int b = 0; b < bins; ++b) {
@@ -295,64 +305,43 @@ void histogram(glb_graph* g, const long long* row, long long n, unsigned long lo
       unsigned long long v = (unsigned long long)(num / (unsigned)bins);
       *mdt = (int64_t)std::max<unsigned long long>(1, v);
     }
-  } catch (...) {
-    free_buf(tmp);
-    throw;
   }
 }
 
 // ========================================================= COO expansion ===
 // src[e] = v for e in [row[v], row[v+1]) -- np.repeat(arange(n), outdeg),
-// csr.py:168.  Thread / warp / CTA cooperative segment fill.
+// csr.py:168.  Edge tiles: coalesced writes, no per-node serial loops.
 __global__ void __launch_bounds__(kBlock) k_coo_src(const long long* __restrict__ row, long long n,
+                                                    long long m,
+                                                    const unsigned int* __restrict__ tile_node,
                                                     uint32_t* __restrict__ src) {
-  __shared__ long long s_lo, s_hi;
-  __shared__ int s_owner;
-  __shared__ uint32_t s_v;
-  for (long long base = blockIdx.x * (long long)kBlock; base < n;
-       base += (long long)gridDim.x * kBlock) {
-    long long v = base + threadIdx.x;
-    long long lo = 0, hi = 0;
-    if (v < n) {
-      lo = row[v];
-      hi = row[v + 1];
+  __shared__ __align__(16) int s_head[kEdgeTile];
+  __shared__ uint32_t s_v[kEdgeTile];
+  __shared__ typename cub::BlockScan<int, kBlock>::TempStorage ts;
+  const long long ntiles = (m + kEdgeTile - 1) / kEdgeTile;
+  for (long long b = blockIdx.x; b < ntiles; b += gridDim.x) {
+    const long long e0 = b * kEdgeTile, e1 = e0 + kEdgeTile < m ? e0 + kEdgeTile : m;
+    const long long v0 = tile_node[b];
+    const long long v1 = b + 1 < ntiles ? (long long)tile_node[b + 1] : n - 1;
+    tile_heads(row, v0, v1, e0, e1, s_head, ts, [&](long long v, int h) { s_v[h] = (uint32_t)v; });
+#pragma unroll
+    for (int k = 0; k < kEdgeEPT; ++k) {
+      const int local = k * kBlock + threadIdx.x;
+      if (e0 + local < e1) src[e0 + local] = s_v[s_head[local]];
     }
-    // CTA level: segments >= 4096
-    while (true) {
-      if (threadIdx.x == 0) s_owner = -1;
-      __syncthreads();
-      if (hi - lo >= 4096) s_owner = threadIdx.x;
-      __syncthreads();
-      int o = s_owner;
-      if (o < 0) break;
-      if (threadIdx.x == o) {
-        s_lo = lo;
-        s_hi = hi;
-        s_v = (uint32_t)v;
-        lo = hi;
-      }
-      __syncthreads();
-      for (long long e = s_lo + threadIdx.x; e < s_hi; e += kBlock) src[e] = s_v;
-      __syncthreads();
-    }
-    // warp level: segments >= 32
-    unsigned ball;
-    while ((ball = __ballot_sync(0xffffffffu, hi - lo >= 32)) != 0) {
-      int leader = __ffs(ball) - 1;
-      long long wl = __shfl_sync(0xffffffffu, lo, leader);
-      long long wh = __shfl_sync(0xffffffffu, hi, leader);
-      uint32_t wv = (uint32_t)__shfl_sync(0xffffffffu, (unsigned long long)v, leader);
-      if ((int)lane_id() == leader) lo = hi;
-      for (long long e = wl + lane_id(); e < wh; e += 32) src[e] = wv;
-    }
-    for (long long e = lo; e < hi; ++e) src[e] = (uint32_t)v;
+    __syncthreads();
   }
 }
 
 void coo_src(glb_graph* g, uint32_t* d_src) {
   if (g->n == 0 || g->m == 0) return;
-  unsigned grid = grid_for(g->n, kBlock, g->num_sms * 8);
-  k_coo_src<<<grid, kBlock, 0, g->stream>>>(g->row, g->n, d_src);
+  const long long ntiles = (g->m + kEdgeTile - 1) / kEdgeTile;
+  unsigned* tile_node = (unsigned*)ensure(g->ws.ns_tmp, (size_t)(ntiles + 1) * 4);
+  k_tile_nodes<<<grid_for(g->n, kBlock, g->num_sms * 8), kBlock, 0, g->stream>>>(g->row, g->n,
+                                                                                 tile_node);
+  GLB_CHECK_LAUNCH();
+  k_coo_src<<<grid_for(ntiles, 1, g->num_sms * 4), kBlock, 0, g->stream>>>(g->row, g->n, g->m,
+                                                                           tile_node, d_src);
   GLB_CHECK_LAUNCH();
 }
 
@@ -418,81 +407,59 @@ __global__ void __launch_bounds__(kBlock) k_split_scan(const long long* __restri
 }
 
 // Parent keeps its first mdt edges; children take the following mdt-chunks,
-// laid out after all parents' chunks (splitting.py:72-99).
+// laid out after all parents' chunks (splitting.py:72-99).  Edge e of node v
+// at local offset j moves to new_row[v] + j (j < mdt) or to
+// ptotal + excess_pre[v] + (j - mdt): one coalesced pass over the edge tiles.
 template <bool W>
-__global__ void __launch_bounds__(kBlock) k_split_fill(
+__global__ void __launch_bounds__(kBlock) k_split_scatter(
     const long long* __restrict__ row, const uint32_t* __restrict__ col,
     const uint32_t* __restrict__ wt, long long n, long long m, long long mdt,
-    const long long* __restrict__ cs, const long long* __restrict__ excess_pre,
-    const long long* __restrict__ totals, long long* __restrict__ new_row,
-    uint32_t* __restrict__ new_col, uint32_t* __restrict__ new_w,
-    long long* __restrict__ parent_of) {
-  __shared__ long long s_src, s_dst, s_len;
-  __shared__ int s_owner;
+    const unsigned int* __restrict__ tile_node, const long long* __restrict__ new_row,
+    const long long* __restrict__ excess_pre, const long long* __restrict__ totals,
+    uint32_t* __restrict__ new_col, uint32_t* __restrict__ new_w) {
+  __shared__ __align__(16) int s_head[kEdgeTile];
+  __shared__ uint32_t s_v[kEdgeTile];
+  __shared__ typename cub::BlockScan<int, kBlock>::TempStorage ts;
   const long long ptotal = totals[1];
-  const long long nchild = totals[0];
-  for (long long base = blockIdx.x * (long long)kBlock; base < n;
-       base += (long long)gridDim.x * kBlock) {
-    long long v = base + threadIdx.x;
-    // two segments per node: parent [row, row+keep) -> new_row[v];
-    // children [row+mdt, row1) -> ptotal + excess_pre[v]
-    long long src0 = 0, dst0 = 0, len0 = 0, src1 = 0, dst1 = 0, len1 = 0;
-    if (v < n) {
-      long long lo = row[v], hi = row[v + 1], d = hi - lo;
-      long long keep = d < mdt ? d : mdt;
-      src0 = lo;
-      dst0 = new_row[v];
-      len0 = keep;
-      src1 = lo + keep;
-      dst1 = ptotal + excess_pre[v];
-      len1 = d - keep;
-      long long c0 = cs[v], c1 = cs[v + 1];
-      for (long long k = 0; k < c1 - c0; ++k) {
-        new_row[n + c0 + k] = dst1 + k * mdt;
-        parent_of[c0 + k] = v;
+  const long long ntiles = (m + kEdgeTile - 1) / kEdgeTile;
+  for (long long b = blockIdx.x; b < ntiles; b += gridDim.x) {
+    const long long e0 = b * kEdgeTile, e1 = e0 + kEdgeTile < m ? e0 + kEdgeTile : m;
+    const long long v0 = tile_node[b];
+    const long long v1 = b + 1 < ntiles ? (long long)tile_node[b + 1] : n - 1;
+    tile_heads(row, v0, v1, e0, e1, s_head, ts, [&](long long v, int h) { s_v[h] = (uint32_t)v; });
+#pragma unroll
+    for (int k = 0; k < kEdgeEPT; ++k) {
+      const int local = k * kBlock + threadIdx.x;
+      const long long e = e0 + local;
+      if (e < e1) {
+        const uint32_t v = s_v[s_head[local]];
+        const long long j = e - __ldg(row + v);
+        const long long dst =
+            j < mdt ? __ldg(new_row + v) + j : ptotal + __ldg(excess_pre + v) + (j - mdt);
+        new_col[dst] = __ldcs(col + e);
+        if (W) new_w[dst] = __ldcs(wt + e);
       }
     }
-    if (v == 0) new_row[n + nchild] = m;
-#pragma unroll 1
-    for (int seg = 0; seg < 2; ++seg) {
-      long long s = seg ? src1 : src0, dd = seg ? dst1 : dst0, len = seg ? len1 : len0;
-      while (true) {
-        if (threadIdx.x == 0) s_owner = -1;
-        __syncthreads();
-        if (len >= 2048) s_owner = threadIdx.x;
-        __syncthreads();
-        int o = s_owner;
-        if (o < 0) break;
-        if (threadIdx.x == o) {
-          s_src = s;
-          s_dst = dd;
-          s_len = len;
-          len = 0;
-        }
-        __syncthreads();
-        for (long long k = threadIdx.x; k < s_len; k += kBlock) {
-          new_col[s_dst + k] = col[s_src + k];
-          if (W) new_w[s_dst + k] = wt[s_src + k];
-        }
-        __syncthreads();
-      }
-      unsigned ball;
-      while ((ball = __ballot_sync(0xffffffffu, len >= 32)) != 0) {
-        int leader = __ffs(ball) - 1;
-        long long ws = __shfl_sync(0xffffffffu, s, leader);
-        long long wd = __shfl_sync(0xffffffffu, dd, leader);
-        long long wl = __shfl_sync(0xffffffffu, len, leader);
-        if ((int)lane_id() == leader) len = 0;
-        for (long long k = lane_id(); k < wl; k += 32) {
-          new_col[wd + k] = col[ws + k];
-          if (W) new_w[wd + k] = wt[ws + k];
-        }
-      }
-      for (long long k = 0; k < len; ++k) {
-        new_col[dd + k] = col[s + k];
-        if (W) new_w[dd + k] = wt[s + k];
-      }
+    __syncthreads();
+  }
+}
+
+// Child row offsets and parent_of for every split node.
+__global__ void k_split_children(const long long* __restrict__ row, long long n, long long m,
+                                 long long mdt, const long long* __restrict__ cs,
+                                 const long long* __restrict__ excess_pre,
+                                 const long long* __restrict__ totals, long long* __restrict__ new_row,
+                                 long long* __restrict__ parent_of) {
+  const long long ptotal = totals[1];
+  for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; v < n;
+       v += (long long)gridDim.x * blockDim.x) {
+    const long long c0 = cs[v], c1 = cs[v + 1];
+    const long long base = ptotal + excess_pre[v];
+    for (long long k = 0; k < c1 - c0; ++k) {
+      new_row[n + c0 + k] = base + k * mdt;
+      parent_of[c0 + k] = v;
     }
+    if (v == 0) new_row[n + totals[0]] = m;
   }
 }
 
@@ -541,15 +508,25 @@ void split_device(glb_graph* g, long long mdt, long long totals_out[4]) {
   uint32_t* new_w = g->wt ? (uint32_t*)ensure(ws.ns_w, (size_t)std::max<long long>(m, 1) * 4) : nullptr;
   long long* parent_of = (long long*)ensure(ws.ns_parent, (size_t)std::max<long long>(nchild, 1) * 8);
   if (n > 0) {
-    unsigned grid = grid_for(n, kBlock, g->num_sms * 8);
-    if (g->wt)
-      k_split_fill<true><<<grid, kBlock, 0, g->stream>>>(g->row, g->col, g->wt, n, m, mdt, cs,
-                                                         exc, totals, new_row, new_col, new_w,
-                                                         parent_of);
-    else
-      k_split_fill<false><<<grid, kBlock, 0, g->stream>>>(g->row, g->col, g->wt, n, m, mdt, cs,
-                                                          exc, totals, new_row, new_col, new_w,
-                                                          parent_of);
+    const long long etiles = (m + kEdgeTile - 1) / kEdgeTile;
+    if (m > 0) {
+      unsigned* tile_node = (unsigned*)ensure(ws.tile_node, (size_t)(etiles + 1) * 4);
+      k_tile_nodes<<<grid_for(n, kBlock, g->num_sms * 8), kBlock, 0, g->stream>>>(g->row, n,
+                                                                                 tile_node);
+      GLB_CHECK_LAUNCH();
+      const unsigned egrid = grid_for(etiles, 1, g->num_sms * 4);
+      if (g->wt)
+        k_split_scatter<true><<<egrid, kBlock, 0, g->stream>>>(g->row, g->col, g->wt, n, m, mdt,
+                                                               tile_node, new_row, exc, totals,
+                                                               new_col, new_w);
+      else
+        k_split_scatter<false><<<egrid, kBlock, 0, g->stream>>>(g->row, g->col, g->wt, n, m, mdt,
+                                                                tile_node, new_row, exc, totals,
+                                                                new_col, new_w);
+      GLB_CHECK_LAUNCH();
+    }
+    k_split_children<<<grid_for(n, kBlock, g->num_sms * 8), kBlock, 0, g->stream>>>(
+        g->row, n, m, mdt, cs, exc, totals, new_row, parent_of);
     GLB_CHECK_LAUNCH();
   } else {
     long long mm = m;
@@ -701,6 +678,20 @@ int glb_graph_create(const int64_t* row_offsets, const int64_t* col, const int64
       g->weighted = weights_or_null != nullptr;
       GLB_CUDA_TRY(cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking));
       GLB_CUDA_TRY(cudaDeviceGetAttribute(&g->num_sms, cudaDevAttrMultiProcessorCount, device));
+      // Opt-in L2 persistence for the distance cells (GLB_L2_PERSIST=1).  It
+      // carves the persisting set out of the 126 MB L2 for every kernel, and
+      // measured slower on C2 than plain evict-first streaming, so it is off
+      // by default.
+      if (getenv("GLB_L2_PERSIST") &&
+          (cudaDeviceGetAttribute(&g->l2_persist_max, cudaDevAttrMaxPersistingL2CacheSize,
+                                  device) != cudaSuccess ||
+           cudaDeviceGetAttribute(&g->l2_window_max, cudaDevAttrMaxAccessPolicyWindowSize,
+                                  device) != cudaSuccess ||
+           cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)g->l2_persist_max) !=
+               cudaSuccess)) {
+        cudaGetLastError();
+        g->l2_persist_max = g->l2_window_max = 0;
+      }
       GLB_CUDA_TRY(cudaEventCreate(&g->ev[0]));
       GLB_CUDA_TRY(cudaEventCreate(&g->ev[1]));
       GLB_CUDA_TRY(cudaHostAlloc(&g->host_ctrl, 1 << 16, cudaHostAllocDefault));
@@ -727,7 +718,10 @@ int glb_graph_destroy(glb_graph* g) {
                          &ws.q[3],   &ws.c_pre,  &ws.c_base,   &ws.c_node,  &ws.tile_first,
                          &ws.scan_flags, &ws.scan_vals, &ws.stats, &ws.ctrl, &ws.ns_row,
                          &ws.ns_col, &ws.ns_w,   &ws.ns_parent, &ws.ns_cs,  &ws.ns_tmp,
-                         &ws.ep_src, &ws.eq[0],  &ws.eq[1],    &ws.out64,   &ws.misc};
+                         &ws.ep_src, &ws.eq[0],  &ws.eq[1],    &ws.out64,   &ws.misc,
+                         &ws.recs,   &ws.hist,   &ws.tile_node};
+  for (auto& kv : g->gexec) cudaGraphExecDestroy(kv.second);
+  g->gexec.clear();
   for (auto* b : bufs) glb::free_buf(*b);
   for (auto e : g->ev_pool) cudaEventDestroy(e);
   if (g->ev[0]) cudaEventDestroy(g->ev[0]);

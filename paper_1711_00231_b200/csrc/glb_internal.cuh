@@ -61,6 +61,34 @@ struct DistTraits<unsigned long long> {
   static constexpr unsigned long long kInf = 0x7FFFFFFFFFFFFFFFull;
 };
 
+// Distance cells.  With 32-bit distances a cell packs (dist << 32 | gen):
+// one 64-bit atomicMin both lowers the distance (engine.py:120-139) and
+// reports, through the old generation, whether this node was already pushed
+// to this iteration's out-list -- the dedup flag of worklist.py:107-130
+// folded into the relaxation atomic.  Equal distances keep the older
+// generation, so only a strict improvement can claim the push.  64-bit
+// distances (the overflow re-run) keep a separate stamp array instead.
+template <typename D>
+struct Cell;
+template <>
+struct Cell<uint32_t> {
+  static constexpr bool kPacked = true;
+  __host__ __device__ static constexpr unsigned long long make(uint32_t d, uint32_t gen) {
+    return ((unsigned long long)d << 32) | gen;
+  }
+  __device__ static uint32_t dist(unsigned long long c) { return (uint32_t)(c >> 32); }
+  __device__ static uint32_t gen(unsigned long long c) { return (uint32_t)c; }
+};
+template <>
+struct Cell<unsigned long long> {
+  static constexpr bool kPacked = false;
+  __host__ __device__ static constexpr unsigned long long make(unsigned long long d, uint32_t) {
+    return d;
+  }
+  __device__ static unsigned long long dist(unsigned long long c) { return c; }
+  __device__ static uint32_t gen(unsigned long long) { return 0; }
+};
+
 // ---------------------------------------------------- per-launch counters ---
 // One LaunchStats per kernel invocation; kStatSlots copies spread the atomics
 // (summed on the host).  Mirrors MetricsRecord (engine.py:142-174).
@@ -76,7 +104,28 @@ struct LaunchStats {
   StatSlot slot[kStatSlots];
 };
 
-// Device control block: queue sizes + scan outputs + error flags.
+// Step modes of the device-side strategy state machine (k_control).
+enum StepMode : int { kModeDone = 0, kModeRelax = 1, kModeWD = 2, kModeHP = 3 };
+
+struct StepTimer {  // %globaltimer ns, min over CTA starts / max over CTA ends
+  unsigned long long start;
+  unsigned long long end;
+};
+
+// One kernel invocation as recorded on the device by k_control
+// (MetricsRecord, engine.py:142-174).
+struct DevRecord {
+  int iteration, sub, tag, pad;
+  long long active, threads, work, relax, push, work_max;
+  double work_sumsq;
+  unsigned long long k0, k1, o0, o1;  // relax kernel / scan kernel timers
+};
+
+// Device control block: worklist cursors, the current step's frame (which
+// lists it reads and writes, stamp generation, HP window) and the strategy
+// state machine.  Written by k_control_init / k_control, read by every step
+// kernel at launch, so the same kernels run under the host loop and inside
+// the device-driven CUDA graph.
 struct DevCtrl {
   unsigned int qcount[8];       // worklist cursors
   unsigned int overflow;        // a u32 candidate reached INF -> re-run in u64
@@ -84,6 +133,25 @@ struct DevCtrl {
   long long wd_total;           // WD: active edges of this invocation
   long long wd_items;           // WD: worklist items with remaining edges
   long long aux[4];
+  uint32_t* qptr[4];            // worklist buffers
+  // ---- current step
+  int in, out, next, mode;      // lists read / pushed / carried (HP), StepMode
+  unsigned int gen;             // dedup stamp generation of the out list
+  int iteration, sub, tag;      // record fields
+  long long window, mdt;        // HP window start s*mdt (also WD-fallback base)
+  unsigned int scan_epoch;      // look-back epoch of the next WD scan
+  int done;
+  unsigned long long scan_ticket, relax_ticket;  // dynamic tile tickets of the WD step
+  // ---- HP super-iteration state (hierarchical.py:54-136)
+  int sup_in, sup_out, cur, spare;
+  long long s;
+  long long hp_threshold;       // KernelConfig.block_size
+  int hp_fallback, strategy;
+  long long relax_threads, hp_threads;  // launched threads (record field)
+  StepTimer t_relax, t_scan;
+  unsigned int nrec, rec_cap;
+  DevRecord* recs;
+  struct LaunchStats* ls;
 };
 
 // --------------------------------------------------------- device graph ---
@@ -101,7 +169,10 @@ struct Workspace {
   DevBuf ns_row, ns_col, ns_w, ns_parent, ns_cs, ns_tmp;  // NS split graph
   DevBuf ep_src, eq[2];                      // EP COO src + edge worklists
   DevBuf out64;                              // widened distances
+  DevBuf recs;                               // DevRecord[kMaxRecords]
   DevBuf misc;
+  DevBuf hist;                               // histogram counts
+  DevBuf tile_node;                          // first node of every edge tile
 };
 
 }  // namespace glb
@@ -113,6 +184,8 @@ struct glb_graph {
   int64_t max_degree = 0;
   cudaStream_t stream = nullptr;
   int num_sms = 148;
+  int l2_persist_max = 0;      // cudaDevAttrMaxPersistingL2CacheSize (0: unsupported)
+  int l2_window_max = 0;       // cudaDevAttrMaxAccessPolicyWindowSize
   long long* row = nullptr;
   uint32_t* col = nullptr;
   uint32_t* wt = nullptr;
@@ -123,6 +196,7 @@ struct glb_graph {
   cudaEvent_t ev[2] = {nullptr, nullptr};
   std::vector<cudaEvent_t> ev_pool;
   std::vector<glb_record> last_records;  // records of the most recent glb_run
+  std::vector<std::pair<std::string, cudaGraphExec_t>> gexec;  // instantiated loops
   std::mutex mu;              // drivers are not re-entrant (common.py:5-6)
 };
 
@@ -163,16 +237,19 @@ __device__ __forceinline__ bool claim(uint32_t* stamp, uint32_t v, uint32_t gen)
   return atomicExch(stamp + v, gen) != gen;
 }
 
-// atomic_relax_min (engine.py:120-139): plain-load pre-check (sound because
-// cells only decrease), then atomicMin; true iff strictly decreased.
-__device__ __forceinline__ bool relax_min(uint32_t* dist, uint32_t v, uint32_t cand) {
-  if (cand >= dist[v]) return false;
-  return cand < atomicMin(dist + v, cand);
-}
-__device__ __forceinline__ bool relax_min(unsigned long long* dist, uint32_t v,
-                                          unsigned long long cand) {
-  if (cand >= dist[v]) return false;
-  return cand < atomicMin(dist + v, cand);
+// atomic_relax_min (engine.py:120-139) on a cell: plain-load pre-check
+// (sound because cells only decrease), then atomicMin.  Returns true iff the
+// distance strictly decreased; *first tells whether this is the first such
+// decrease in generation `gen` (packed cells) -- the caller pushes then.
+template <typename D>
+__device__ __forceinline__ bool relax_cell(unsigned long long* cells, uint32_t v, D cand,
+                                           uint32_t gen, bool* first) {
+  const unsigned long long cur = cells[v];
+  if (cand >= Cell<D>::dist(cur)) return false;
+  const unsigned long long old = atomicMin(cells + v, Cell<D>::make(cand, gen));
+  if (cand >= Cell<D>::dist(old)) return false;
+  *first = Cell<D>::gen(old) != gen;
+  return true;
 }
 
 // Candidate distance with overflow detection for the u32 path.

@@ -35,6 +35,13 @@
 #include "glb_internal.cuh"
 #include "glb_scan.cuh"
 
+#ifndef GLB_PRECHECK
+#define GLB_PRECHECK 1  // plain-load filter before the relaxation atomic
+#endif
+#ifndef GLB_RELAX_MINB
+#define GLB_RELAX_MINB 3  // CTAs per SM the WD / HP relax kernels are register-capped for
+#endif
+
 namespace glb {
 
 // ------------------------------------------------------- CTA push queue ---
@@ -88,13 +95,43 @@ template <typename D, bool W>
 struct Relaxer {
   const uint32_t* __restrict__ col;
   const uint32_t* __restrict__ wt;
-  D* dist;
-  uint32_t* stamp;
+  unsigned long long* cells;  // Cell<D> distance cells
+  uint32_t* stamp;            // push dedup for unpacked (64-bit) cells
   uint32_t gen;
   uint32_t* qout;
   unsigned int* nout;
   unsigned int* ovf;
+
+  __device__ __forceinline__ D dist(uint32_t u) const { return Cell<D>::dist(cells[u]); }
+  // push claim after a strict decrease (first = packed-cell verdict)
+  __device__ __forceinline__ bool claim_push(uint32_t v, bool first) const {
+    if (Cell<D>::kPacked) return first;
+    return claim(stamp, v, gen);
+  }
 };
+
+// Bind the per-step fields (out list, its cursor, stamp generation) from the
+// control block written by k_control.
+template <typename D, bool W>
+__device__ __forceinline__ Relaxer<D, W> bind(Relaxer<D, W> rx, DevCtrl* ctrl) {
+  rx.gen = ctrl->gen;
+  rx.qout = ctrl->qptr[ctrl->out];
+  rx.nout = &ctrl->qcount[ctrl->out];
+  return rx;
+}
+
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void timer_begin(StepTimer& t) {
+  if (threadIdx.x == 0) atomicMin(&t.start, gtime());
+}
+__device__ __forceinline__ void timer_end(StepTimer& t) {
+  __syncthreads();
+  if (threadIdx.x == 0) atomicMax(&t.end, gtime());
+}
 
 // Relax up to K edges (bit k of `valid`: e[k] out of a node at distance
 // dn[k] != INF).  Returns the mask of edges whose atomicMin strictly lowered
@@ -112,11 +149,12 @@ __device__ __forceinline__ unsigned relax_batch(const Relaxer<D, W>& rx, BlockQ&
       v[k] = __ldcs(rx.col + e[k]);
       w[k] = W ? __ldcs(rx.wt + e[k]) : 1u;
     }
+  unsigned want = 0;
+#if GLB_PRECHECK
   D cur[K];
 #pragma unroll
   for (int k = 0; k < K; ++k)
-    if (valid >> k & 1u) cur[k] = rx.dist[v[k]];
-  unsigned want = 0;
+    if (valid >> k & 1u) cur[k] = rx.dist(v[k]);
 #pragma unroll
   for (int k = 0; k < K; ++k)
     if (valid >> k & 1u) {
@@ -124,21 +162,39 @@ __device__ __forceinline__ unsigned relax_batch(const Relaxer<D, W>& rx, BlockQ&
       ++c.relax;
       if (make_cand<D>(dn[k], w[k], cand[k], rx.ovf) && cand[k] < cur[k]) want |= 1u << k;
     }
-  D old[K];
+#else
 #pragma unroll
   for (int k = 0; k < K; ++k)
-    if (want >> k & 1u) old[k] = atomicMin(rx.dist + v[k], cand[k]);
-  unsigned won = 0;
+    if (valid >> k & 1u) {
+      ++c.work;
+      ++c.relax;
+      if (make_cand<D>(dn[k], w[k], cand[k], rx.ovf)) want |= 1u << k;
+    }
+#endif
+  unsigned long long old[K];
 #pragma unroll
   for (int k = 0; k < K; ++k)
-    if ((want >> k & 1u) && cand[k] < old[k]) won |= 1u << k;
-  unsigned prev[K];
+    if (want >> k & 1u) old[k] = atomicMin(rx.cells + v[k], Cell<D>::make(cand[k], rx.gen));
+  unsigned won = 0, first = 0;
 #pragma unroll
   for (int k = 0; k < K; ++k)
-    if (won >> k & 1u) prev[k] = atomicExch(rx.stamp + v[k], rx.gen);
+    if ((want >> k & 1u) && cand[k] < Cell<D>::dist(old[k])) {
+      won |= 1u << k;
+      if (Cell<D>::gen(old[k]) != rx.gen) first |= 1u << k;
+    }
+  if (!Cell<D>::kPacked) {
+    unsigned prev[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+      if (won >> k & 1u) prev[k] = atomicExch(rx.stamp + v[k], rx.gen);
+    first = 0;
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+      if ((won >> k & 1u) && prev[k] != rx.gen) first |= 1u << k;
+  }
 #pragma unroll
   for (int k = 0; k < K; ++k)
-    if ((won >> k & 1u) && prev[k] != rx.gen) {
+    if (first >> k & 1u) {
       bq_push(bq, rx.qout, rx.nout, v[k]);
       ++c.push;
     }
@@ -190,24 +246,27 @@ __device__ __forceinline__ void relax_range_coop(const Relaxer<D, W>& rx, BlockQ
 // ============================================================ BS (K1) ===
 template <typename D, bool W>
 __global__ void __launch_bounds__(kBlock) k_bs_relax(const long long* __restrict__ row,
-                                                     Relaxer<D, W> rx,
-                                                     const uint32_t* __restrict__ qin,
-                                                     const unsigned int* nin, LaunchStats* ls) {
+                                                     Relaxer<D, W> rx0, DevCtrl* ctrl) {
   __shared__ uint32_t s_q[kQCap];
   __shared__ BlockQ bq;
+  const unsigned n = ctrl->qcount[ctrl->in];
+  if (blockIdx.x * kBlock >= n) return;  // idle CTA: no barriers, no atomics
+  timer_begin(ctrl->t_relax);
   bq_init(bq, s_q);
+  const Relaxer<D, W> rx = bind(rx0, ctrl);
+  const uint32_t* __restrict__ qin = ctrl->qptr[ctrl->in];
   ThreadCounters c;
-  const unsigned n = *nin;
   for (unsigned base = blockIdx.x * kBlock; base < n; base += gridDim.x * kBlock) {
     const unsigned i = base + threadIdx.x;
     if (i < n) {
       const uint32_t u = qin[i];
-      const D du = rx.dist[u];
+      const D du = rx.dist(u);
       if (du != DistTraits<D>::kInf) relax_range_thread<4>(rx, bq, row[u], row[u + 1], du, c);
     }
     bq_flush(bq, rx.qout, rx.nout);
   }
-  flush_counters(ls, c);
+  flush_counters(ctrl->ls, c);
+  timer_end(ctrl->t_relax);
 }
 
 // ============================================================ NS (K9) ===
@@ -215,20 +274,23 @@ __global__ void __launch_bounds__(kBlock) k_bs_relax(const long long* __restrict
 template <typename D, bool W>
 __global__ void __launch_bounds__(kBlock) k_ns_relax(const long long* __restrict__ row,
                                                      const long long* __restrict__ cs,
-                                                     long long n_orig, Relaxer<D, W> rx,
-                                                     const uint32_t* __restrict__ qin,
-                                                     const unsigned int* nin, LaunchStats* ls) {
+                                                     long long n_orig, Relaxer<D, W> rx0,
+                                                     DevCtrl* ctrl) {
   __shared__ uint32_t s_q[kQCap];
   __shared__ BlockQ bq;
+  const unsigned n = ctrl->qcount[ctrl->in];
+  if (blockIdx.x * kBlock >= n) return;  // idle CTA: no barriers, no atomics
+  timer_begin(ctrl->t_relax);
   bq_init(bq, s_q);
+  const Relaxer<D, W> rx = bind(rx0, ctrl);
+  const uint32_t* __restrict__ qin = ctrl->qptr[ctrl->in];
   ThreadCounters c;
-  const unsigned n = *nin;
   constexpr int K = 4;
   for (unsigned base = blockIdx.x * kBlock; base < n; base += gridDim.x * kBlock) {
     const unsigned i = base + threadIdx.x;
     if (i < n) {
       const uint32_t u = qin[i];
-      const D du = rx.dist[u];
+      const D du = rx.dist(u);
       if (du != DistTraits<D>::kInf) {
         const long long lo = row[u], hi = row[u + 1];
         for (long long b = lo; b < hi; b += K) {
@@ -252,8 +314,9 @@ __global__ void __launch_bounds__(kBlock) k_ns_relax(const long long* __restrict
             for (long long ch = cs[v[k]]; ch < k1; ++ch) {
               const uint32_t child = (uint32_t)(n_orig + ch);
               ++c.relax;
-              relax_min(rx.dist, child, cand[k]);
-              if (claim(rx.stamp, child, rx.gen)) {
+              bool first = false;
+              if (relax_cell<D>(rx.cells, child, cand[k], rx.gen, &first) &&
+                  rx.claim_push(child, first)) {
                 bq_push(bq, rx.qout, rx.nout, child);
                 ++c.push;
               }
@@ -264,7 +327,8 @@ __global__ void __launch_bounds__(kBlock) k_ns_relax(const long long* __restrict
     }
     bq_flush(bq, rx.qout, rx.nout);
   }
-  flush_counters(ls, c);
+  flush_counters(ctrl->ls, c);
+  timer_end(ctrl->t_relax);
 }
 
 // ============================================================ EP (K2) ===
@@ -284,14 +348,16 @@ struct EpRanges {
 template <typename D, bool W, bool CHUNKED>
 __global__ void __launch_bounds__(kBlock) k_ep_relax(const long long* __restrict__ row,
                                                      const uint32_t* __restrict__ src,
-                                                     Relaxer<D, W> rx,
-                                                     const uint32_t* __restrict__ qin,
-                                                     const unsigned int* nin, LaunchStats* ls) {
+                                                     Relaxer<D, W> rx0, DevCtrl* ctrl) {
   __shared__ EpRanges rg;
+  const unsigned n = ctrl->qcount[ctrl->in];
+  if (blockIdx.x * kBlock >= n) return;  // idle CTA
+  timer_begin(ctrl->t_relax);
   if (threadIdx.x == 0) rg.count = rg.total = 0;
   __syncthreads();
+  const Relaxer<D, W> rx = bind(rx0, ctrl);
+  const uint32_t* __restrict__ qin = ctrl->qptr[ctrl->in];
   ThreadCounters c;
-  const unsigned n = *nin;
   constexpr int K = 4;
   const unsigned stride = gridDim.x * kBlock;
   for (unsigned base = blockIdx.x * kBlock; base < n; base += stride * K) {
@@ -316,8 +382,8 @@ __global__ void __launch_bounds__(kBlock) k_ep_relax(const long long* __restrict
 #pragma unroll
     for (int k = 0; k < K; ++k)
       if (valid >> k & 1u) {
-        du[k] = rx.dist[u[k]];
-        cur[k] = rx.dist[v[k]];
+        du[k] = rx.dist(u[k]);
+        cur[k] = rx.dist(v[k]);
       }
     unsigned want = 0;
 #pragma unroll
@@ -328,18 +394,20 @@ __global__ void __launch_bounds__(kBlock) k_ep_relax(const long long* __restrict
         ++c.relax;
         if (make_cand<D>(du[k], w[k], cand[k], rx.ovf) && cand[k] < cur[k]) want |= 1u << k;
       }
-    D old[K];
+    unsigned long long old[K];
 #pragma unroll
     for (int k = 0; k < K; ++k)
-      if (want >> k & 1u) old[k] = atomicMin(rx.dist + v[k], cand[k]);
-    unsigned prev[K];
-#pragma unroll
-    for (int k = 0; k < K; ++k)
-      if ((want >> k & 1u) && cand[k] < old[k]) prev[k] = atomicExch(rx.stamp + v[k], rx.gen);
-      else want &= ~(1u << k);
+      if (want >> k & 1u) old[k] = atomicMin(rx.cells + v[k], Cell<D>::make(cand[k], rx.gen));
+    bool pushk[K];
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-      if (!(want >> k & 1u) || prev[k] == rx.gen) continue;
+      pushk[k] = false;
+      if ((want >> k & 1u) && cand[k] < Cell<D>::dist(old[k]))
+        pushk[k] = rx.claim_push(v[k], Cell<D>::gen(old[k]) != rx.gen);
+    }
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      if (!pushk[k]) continue;
       const long long lo = row[v[k]];
       const unsigned len = (unsigned)(row[v[k] + 1] - lo);
       if (len == 0) continue;
@@ -377,59 +445,74 @@ __global__ void __launch_bounds__(kBlock) k_ep_relax(const long long* __restrict
       __syncthreads();
     }
   }
-  flush_counters(ls, c);
+  flush_counters(ctrl->ls, c);
+  timer_end(ctrl->t_relax);
 }
 
 // ====================================================== WD (K4 + K5/K6) ===
-constexpr int kWdIPT = 4;                    // frontier items per thread in the scan
-constexpr int kWdScanTile = kBlock * kWdIPT;  // 1024 items per scan tile
+constexpr int kWdIPT = 8;                    // frontier items per thread in the scan
+constexpr int kWdScanTile = kBlock * kWdIPT;  // 2048 items per scan tile
 constexpr int kWdEPT = 8;                    // edges per thread per relax tile
 constexpr int kWdTile = kBlock * kWdEPT;     // 2048 edges per relax tile
 
 // Remaining degree of every frontier item (minus the HP base offset
 // min(window, deg), hierarchical.py:69-72), scanned as {edges, non-empty}.
 // Non-empty items are compacted to j = exclusive count: c_pre[j] = first
-// active edge, c_base[j] = CSR index of that edge minus c_pre[j], c_node[j].
+// active edge, c_base[j] = CSR index of that edge minus c_pre[j], c_dn[j] =
+// the node's distance when the invocation starts (a later decrease re-pushes
+// the node, so reading it here instead of per edge is confluent).
 // tile_first[b] = item holding active edge b*kWdTile.
+template <typename D>
 __global__ void __launch_bounds__(kBlock) k_wd_scan(
-    const long long* __restrict__ row, const uint32_t* __restrict__ q, const unsigned int* nin,
-    long long window, LookbackState<2> lb, unsigned epoch, long long* __restrict__ c_pre,
-    long long* __restrict__ c_base, uint32_t* __restrict__ c_node,
-    unsigned int* __restrict__ tile_first, DevCtrl* ctrl) {
+    const long long* __restrict__ row, const unsigned long long* __restrict__ cells,
+    LookbackState<2> lb, long long* __restrict__ c_pre, long long* __restrict__ c_base,
+    D* __restrict__ c_dn, unsigned int* __restrict__ tile_first, DevCtrl* ctrl) {
   using TS = TileScan<2, kBlock>;
   __shared__ typename TS::Storage st;
-  const long long n = *nin;
+  __shared__ long long s_tile;
+  const long long n = ctrl->qcount[ctrl->in];
   const long long ntiles = (n + kWdScanTile - 1) / kWdScanTile;
-  if (ntiles == 0 && blockIdx.x == 0 && threadIdx.x == 0) {
-    ctrl->wd_total = 0;
-    ctrl->wd_items = 0;
+  if (ntiles == 0) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      ctrl->wd_total = 0;
+      ctrl->wd_items = 0;
+    }
+    return;
   }
-  for (long long t = blockIdx.x; t < ntiles; t += gridDim.x) {
-    long long first = t * kWdScanTile + (long long)threadIdx.x * kWdIPT;
+  if (blockIdx.x >= ntiles) return;  // idle CTA
+  timer_begin(ctrl->t_scan);
+  const uint32_t* __restrict__ q = ctrl->qptr[ctrl->in];
+  const long long window = ctrl->window;
+  const unsigned epoch = ctrl->scan_epoch;
+  // Tiles are handed out in ticket order, so every predecessor of a tile is
+  // already owned by a running (or finished) CTA: the look-back always makes
+  // progress, whatever the residency.
+  while (true) {
+    if (threadIdx.x == 0) s_tile = (long long)atomicAdd(&ctrl->scan_ticket, 1ull);
+    __syncthreads();
+    const long long t = s_tile;
+    if (t >= ntiles) break;
+    const long long first = t * kWdScanTile + (long long)threadIdx.x * kWdIPT;
     uint32_t v[kWdIPT];
     long long beg[kWdIPT], rem[kWdIPT];
     Vec<2> sum;
-    if (first + kWdIPT <= n) {  // 128-bit load of 4 worklist items
-      const uint4 q4 = *reinterpret_cast<const uint4*>(q + first);
-      v[0] = q4.x; v[1] = q4.y; v[2] = q4.z; v[3] = q4.w;
+    if (first + kWdIPT <= n) {  // two 128-bit loads of worklist items
+      const uint4 a = *reinterpret_cast<const uint4*>(q + first);
+      const uint4 b = *reinterpret_cast<const uint4*>(q + first + 4);
+      v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+      v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
     } else {
 #pragma unroll
       for (int k = 0; k < kWdIPT; ++k) v[k] = first + k < n ? q[first + k] : 0u;
     }
-    long long lo[kWdIPT], hi[kWdIPT];
-#pragma unroll
-    for (int k = 0; k < kWdIPT; ++k)
-      if (first + k < n) {
-        lo[k] = row[v[k]];
-        hi[k] = row[v[k] + 1];
-      }
 #pragma unroll
     for (int k = 0; k < kWdIPT; ++k) {
       rem[k] = 0;
       if (first + k < n) {
-        long long b = hi[k] - lo[k] < window ? hi[k] - lo[k] : window;
-        beg[k] = lo[k] + b;
-        rem[k] = hi[k] - lo[k] - b;
+        const long long lo = row[v[k]], hi = row[v[k] + 1];
+        const long long b = hi - lo < window ? hi - lo : window;
+        beg[k] = lo + b;
+        rem[k] = hi - lo - b;
       }
       sum.w[0] += rem[k];
       sum.w[1] += rem[k] > 0;
@@ -439,10 +522,10 @@ __global__ void __launch_bounds__(kBlock) k_wd_scan(
 #pragma unroll
     for (int k = 0; k < kWdIPT; ++k) {
       if (rem[k] > 0) {
-        long long j = ex.w[1], pre = ex.w[0];
+        const long long j = ex.w[1], pre = ex.w[0];
         c_pre[j] = pre;
         c_base[j] = beg[k] - pre;
-        c_node[j] = v[k];
+        c_dn[j] = Cell<D>::dist(cells[v[k]]);  // dn of the node (workload.py:131,140)
         for (long long b = (pre + kWdTile - 1) / kWdTile; b * kWdTile < pre + rem[k]; ++b)
           tile_first[b] = (unsigned)j;
         ex.w[0] += rem[k];
@@ -454,6 +537,7 @@ __global__ void __launch_bounds__(kBlock) k_wd_scan(
       ctrl->wd_items = incl.w[1];
     }
   }
+  timer_end(ctrl->t_scan);
 }
 
 struct MaxOp {
@@ -461,12 +545,12 @@ struct MaxOp {
 };
 
 template <typename D, bool W>
-__global__ void __launch_bounds__(kBlock) k_wd_relax(Relaxer<D, W> rx,
+__global__ void __launch_bounds__(kBlock, GLB_RELAX_MINB) k_wd_relax(Relaxer<D, W> rx0,
                                                      const long long* __restrict__ c_pre,
                                                      const long long* __restrict__ c_base,
-                                                     const uint32_t* __restrict__ c_node,
+                                                     const D* __restrict__ c_dn,
                                                      const unsigned int* __restrict__ tile_first,
-                                                     const DevCtrl* ctrl, LaunchStats* ls) {
+                                                     DevCtrl* ctrl) {
   using BScan = cub::BlockScan<int, kBlock, cub::BLOCK_SCAN_WARP_SCANS>;
   static_assert(kQCap == kWdTile, "the CTA queue reuses the owner array");
   __shared__ __align__(16) int s_own[kWdTile];  // owners, then the push queue
@@ -474,12 +558,20 @@ __global__ void __launch_bounds__(kBlock) k_wd_relax(Relaxer<D, W> rx,
   __shared__ D s_dn[kWdTile + 1];
   __shared__ typename BScan::TempStorage s_scan;
   __shared__ BlockQ bq;
-  bq_init(bq, reinterpret_cast<uint32_t*>(s_own));
-  ThreadCounters c;
+  __shared__ long long s_tile;
   const long long total = ctrl->wd_total;
   const long long nitems = ctrl->wd_items;
   const long long ntiles = (total + kWdTile - 1) / kWdTile;
-  for (long long b = blockIdx.x; b < ntiles; b += gridDim.x) {
+  if (blockIdx.x >= ntiles) return;  // idle CTA
+  timer_begin(ctrl->t_relax);
+  bq_init(bq, reinterpret_cast<uint32_t*>(s_own));
+  const Relaxer<D, W> rx = bind(rx0, ctrl);
+  ThreadCounters c;
+  while (true) {  // edge tiles in ticket order: the last wave self-balances
+    if (threadIdx.x == 0) s_tile = (long long)atomicAdd(&ctrl->relax_ticket, 1ull);
+    __syncthreads();
+    const long long b = s_tile;
+    if (b >= ntiles) break;
     const long long e0 = b * kWdTile;
     const long long e1 = e0 + kWdTile < total ? e0 + kWdTile : total;
     const long long j0 = tile_first[b];
@@ -492,7 +584,7 @@ __global__ void __launch_bounds__(kBlock) k_wd_relax(Relaxer<D, W> rx,
       const long long j = j0 + k;
       const long long pre = c_pre[j];
       s_base[k] = c_base[j];
-      s_dn[k] = rx.dist[c_node[j]];  // dn read when the node is entered (workload.py:131,140)
+      s_dn[k] = c_dn[j];
       long long h = pre - e0;
       if (h < 0) h = 0;
       if (h < kWdTile) s_own[h] = k;
@@ -542,33 +634,58 @@ __global__ void __launch_bounds__(kBlock) k_wd_relax(Relaxer<D, W> rx,
       }
     }
     __syncthreads();  // owners consumed: s_own becomes the push queue
-    uint32_t v[kWdEPT];
-    D cand[kWdEPT];
-    relax_batch<kWdEPT>(rx, bq, e, dn, valid, c, v, cand);
+    // two half-batches keep the register footprint at 4 CTAs / SM
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+      constexpr int H = kWdEPT / 2;
+      long long eh[H];
+      D dh[H];
+#pragma unroll
+      for (int k = 0; k < H; ++k) {
+        eh[k] = e[half * H + k];
+        dh[k] = dn[half * H + k];
+      }
+      uint32_t v[H];
+      D cand[H];
+      relax_batch<H>(rx, bq, eh, dh, (valid >> (half * H)) & ((1u << H) - 1u), c, v, cand);
+    }
     bq_flush(bq, rx.qout, rx.nout);
   }
-  flush_counters(ls, c);
+  flush_counters(ctrl->ls, c);
+  timer_end(ctrl->t_relax);
 }
 
 // ============================================================ HP (K10) ===
-constexpr long long kHpCtaThreshold = 1024;  // window length handled by a whole CTA
-constexpr long long kHpWarpThreshold = 32;   // ... by a warp; shorter: one thread
+// Window [s*mdt, (s+1)*mdt) of every sublist node, binned by window length:
+// windows >= kHpCtaThreshold take the whole CTA; all shorter windows of the
+// CTA's 256 nodes are flattened by a block scan and relaxed cooperatively
+// (each thread finds its edge's node by binary search over the 256 window
+// offsets in shared memory), so lanes walk consecutive edges.
+constexpr long long kHpCtaThreshold = 2048;
 
 template <typename D, bool W>
-__global__ void __launch_bounds__(kBlock) k_hp_window(const long long* __restrict__ row,
-                                                      Relaxer<D, W> rx,
-                                                      const uint32_t* __restrict__ qin,
-                                                      const unsigned int* nin, long long window,
-                                                      long long mdt, uint32_t* qnext,
-                                                      unsigned int* nnext, LaunchStats* ls) {
+__global__ void __launch_bounds__(kBlock, GLB_RELAX_MINB) k_hp_window(const long long* __restrict__ row,
+                                                      Relaxer<D, W> rx0, DevCtrl* ctrl) {
+  using BScan = cub::BlockScan<int, kBlock, cub::BLOCK_SCAN_WARP_SCANS>;
+  __shared__ uint32_t s_q[kQCap];
+  __shared__ BlockQ bq;
+  __shared__ typename BScan::TempStorage s_scan;
+  __shared__ int s_off[kBlock];
+  __shared__ long long s_edge[kBlock];
+  __shared__ D s_dnv[kBlock];
   __shared__ long long s_lo, s_hi;
   __shared__ D s_dn;
   __shared__ int s_owner;
-  __shared__ uint32_t s_q[kQCap];
-  __shared__ BlockQ bq;
+  const long long n = ctrl->qcount[ctrl->in];
+  if (blockIdx.x * (long long)kBlock >= n) return;  // idle CTA
+  timer_begin(ctrl->t_relax);
   bq_init(bq, s_q);
+  const Relaxer<D, W> rx = bind(rx0, ctrl);
+  const uint32_t* __restrict__ qin = ctrl->qptr[ctrl->in];
+  uint32_t* qnext = ctrl->qptr[ctrl->next];
+  unsigned int* nnext = &ctrl->qcount[ctrl->next];
+  const long long window = ctrl->window, mdt = ctrl->mdt;
   ThreadCounters c;
-  const long long n = *nin;
   for (long long base = blockIdx.x * (long long)kBlock; base < n;
        base += (long long)gridDim.x * kBlock) {
     const long long i = base + threadIdx.x;
@@ -580,7 +697,7 @@ __global__ void __launch_bounds__(kBlock) k_hp_window(const long long* __restric
       const long long start = r0 + window;
       if (start < r1) {
         const long long end = start + mdt < r1 ? start + mdt : r1;
-        dn = rx.dist[u];
+        dn = rx.dist(u);
         if (dn != DistTraits<D>::kInf) {
           lo = start;
           hi = end;
@@ -591,7 +708,7 @@ __global__ void __launch_bounds__(kBlock) k_hp_window(const long long* __restric
         }
       }
     }
-    // CTA granularity
+    // CTA granularity for long windows
     while (true) {
       if (threadIdx.x == 0) s_owner = -1;
       __syncthreads();
@@ -609,47 +726,67 @@ __global__ void __launch_bounds__(kBlock) k_hp_window(const long long* __restric
       relax_range_coop<4>(rx, bq, s_lo, s_hi, s_dn, threadIdx.x, kBlock, c);
       bq_flush(bq, rx.qout, rx.nout);
     }
-    // warp granularity
-    unsigned ball;
-    while ((ball = __ballot_sync(0xffffffffu, hi - lo >= kHpWarpThreshold)) != 0) {
-      const int leader = __ffs(ball) - 1;
-      const long long wlo = __shfl_sync(0xffffffffu, lo, leader);
-      const long long whi = __shfl_sync(0xffffffffu, hi, leader);
-      const D wdn = __shfl_sync(0xffffffffu, dn, leader);
-      if ((int)lane_id() == leader) lo = hi;
-      relax_range_coop<2>(rx, bq, wlo, whi, wdn, lane_id(), 32, c);
+    // fine-grained gather of the remaining windows
+    int len = (int)(hi - lo), off, total;
+    BScan(s_scan).ExclusiveSum(len, off, total);
+    s_off[threadIdx.x] = off;
+    s_edge[threadIdx.x] = lo - off;
+    s_dnv[threadIdx.x] = dn;
+    __syncthreads();
+    constexpr int K = 4;
+    for (int f0 = 0; f0 < total; f0 += K * kBlock) {
+      long long e[K];
+      D d[K];
+      unsigned valid = 0;
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const int f = f0 + k * kBlock + threadIdx.x;
+        if (f < total) {
+          int o = 0;  // last window whose offset <= f
+#pragma unroll
+          for (int step = kBlock / 2; step > 0; step >>= 1)
+            if (s_off[o + step] <= f) o += step;
+          e[k] = s_edge[o] + f;
+          d[k] = s_dnv[o];
+          valid |= 1u << k;
+        }
+      }
+      uint32_t v[K];
+      D cand[K];
+      relax_batch<K>(rx, bq, e, d, valid, c, v, cand);
     }
-    // thread granularity
-    relax_range_thread<4>(rx, bq, lo, hi, dn, c);
     bq_flush(bq, rx.qout, rx.nout);
   }
-  flush_counters(ls, c);
+  flush_counters(ctrl->ls, c);
+  timer_end(ctrl->t_relax);
 }
 
 // ============================================================ setup ===
 template <typename D>
-__global__ void k_init_dist(D* dist, long long n) {
+__global__ void k_init_dist(unsigned long long* cells, long long n) {
+  const unsigned long long inf = Cell<D>::make(DistTraits<D>::kInf, 0);
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x)
-    dist[i] = DistTraits<D>::kInf;
+    cells[i] = inf;
 }
 
 // Seed the first worklist: the source (+ its NS children at distance 0,
 // splitting.py:123-126) for node worklists, or the source's out-edge range for
 // the EP edge worklist (edge_based.py:55).
 template <typename D>
-__global__ void k_seed(D* dist, uint32_t* q, unsigned int* nq, long long src, long long kid_lo,
-                       long long kid_hi, long long edge_lo, long long edge_hi, bool edges) {
-  long long tid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  long long stride = (long long)gridDim.x * blockDim.x;
-  if (tid == 0) dist[src] = 0;
+__global__ void k_seed(unsigned long long* cells, uint32_t* q, unsigned int* nq, long long src,
+                       long long kid_lo, long long kid_hi, long long edge_lo, long long edge_hi,
+                       bool edges) {
+  const long long tid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  if (tid == 0) cells[src] = Cell<D>::make(0, 0);
   if (edges) {
     for (long long e = edge_lo + tid; e < edge_hi; e += stride) q[e - edge_lo] = (uint32_t)e;
     if (tid == 0) *nq = (unsigned)(edge_hi - edge_lo);
   } else {
     if (tid == 0) q[0] = (uint32_t)src;
     for (long long k = kid_lo + tid; k < kid_hi; k += stride) {
-      dist[k] = 0;
+      cells[k] = Cell<D>::make(0, 0);
       q[1 + k - kid_lo] = (uint32_t)k;
     }
     if (tid == 0) *nq = (unsigned)(1 + kid_hi - kid_lo);
@@ -657,10 +794,11 @@ __global__ void k_seed(D* dist, uint32_t* q, unsigned int* nq, long long src, lo
 }
 
 template <typename D>
-__global__ void k_dist_out(const D* __restrict__ dist, long long n, long long* __restrict__ out) {
+__global__ void k_dist_out(const unsigned long long* __restrict__ cells, long long n,
+                           long long* __restrict__ out) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x) {
-    D d = dist[i];
+    const D d = Cell<D>::dist(cells[i]);
     out[i] = d == DistTraits<D>::kInf ? 0x7FFFFFFFFFFFFFFFll : (long long)d;
   }
 }
