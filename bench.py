@@ -59,11 +59,14 @@ def parse():
 
 
 # ------------------------------------------------------------------ workload
-def workload(args):
+def workload(args, device=0):
+    """The benchmark graph, generated in HBM by the CUDA R-MAT generator
+    (bit-identical to graphlb.generate_rmat; tests pin it) and copied back for
+    the CPU oracle / baseline."""
     import paper_1711_00231_b200 as pkg
 
     t0 = time.time()
-    g = pkg.generate_rmat(args.scale, args.edge_factor, seed=1, max_weight=255)
+    g = pkg.generate_rmat(args.scale, args.edge_factor, seed=1, max_weight=255, device=device)
     return g, time.time() - t0
 
 
@@ -212,7 +215,7 @@ def ours(args):
     else:
         torch.cuda.set_device(0)
     dev = local if world > 1 else 0
-    g, gen_s = workload(args)
+    g, gen_s = workload(args, dev)
     runner = DeviceRunner(g, dev)
 
     # parity of the benchmarked configuration against the pinned oracle
@@ -332,7 +335,7 @@ def ours(args):
             "metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
-            "data": "synthetic (RMAT generated in-process, bit-identical to graphlb.generate_rmat)",
+            "data": "synthetic (RMAT generated on the GPU, bit-identical to graphlb.generate_rmat)",
             "config": dict(workload_desc(args, g), parallelism=f"replicas{world}" if world > 1 else "single",
                            E_r=e_r, N_r=n_r, gen_s=round(gen_s, 1)),
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
@@ -359,6 +362,23 @@ def cpu_baseline(g, args, e_r):
 
 
 # ------------------------------------------------------------ reference arm
+def _has_gpu() -> bool:
+    try:
+        from paper_1711_00231_b200 import _lib
+
+        return _lib.device_count() > 0
+    except Exception:
+        return False
+
+
+def _host_workload(args):
+    import paper_1711_00231_b200 as pkg
+
+    t0 = time.time()
+    g = pkg.generate_rmat(args.scale, args.edge_factor, seed=1, max_weight=255)
+    return g, time.time() - t0
+
+
 def reference(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -367,7 +387,7 @@ def reference(args):
     from oracle import oracle
 
     oracle.build()
-    g, gen_s = workload(args)
+    g, gen_s = workload(args) if _has_gpu() else _host_workload(args)
     threads = os.cpu_count() or 1
     w = g.weights if args.algo == "sssp" else None
     times = []

@@ -135,6 +135,15 @@ uint64_t glb_kernel_launches(void);
 int glb_graph_create(const int64_t* row_offsets, const int64_t* col,
                      const int64_t* weights_or_null, int64_t n, int64_t m,
                      int device, glb_graph** out);
+/* R-MAT straight into HBM, draw-for-draw identical to generate_rmat
+ * (generators.py:23-58) + CsrGraph.from_edges (csr.py:97-118) under numpy's
+ * PCG64: state/inc are default_rng(seed).bit_generator.state (hi, lo words);
+ * t_a, t_ab, t_abc are a, a+b, a+b+c as computed by the reference. */
+int glb_graph_create_rmat(int scale, int64_t edge_factor, double t_a, double t_ab, double t_abc,
+                          const uint64_t* state_hi_lo, const uint64_t* inc_hi_lo, int weighted,
+                          int64_t max_weight, int device, glb_graph** out);
+/* Device CSR back to host int64 arrays (any pointer may be NULL). */
+int glb_graph_download(glb_graph* g, int64_t* row_offsets, int64_t* col, int64_t* weights);
 int glb_graph_destroy(glb_graph* g);
 int glb_graph_info(const glb_graph* g, int64_t* n, int64_t* m, int* weighted,
                    int* device);

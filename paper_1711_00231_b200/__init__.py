@@ -30,6 +30,7 @@ from .graph import (
     CooCapacityError,
     CooGraph,
     CsrGraph,
+    DeviceCsrGraph,
     csr_to_coo,
     generate_er,
     generate_rmat,

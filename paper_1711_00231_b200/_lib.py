@@ -72,6 +72,11 @@ SIGNATURES = {
     "glb_graph_create": (ctypes.c_int, [_p64, _p64, _p64, _i64, _i64, ctypes.c_int,
                                         ctypes.POINTER(ctypes.c_void_p)]),
     "glb_graph_destroy": (ctypes.c_int, [ctypes.c_void_p]),
+    "glb_graph_create_rmat": (ctypes.c_int, [ctypes.c_int, _i64, ctypes.c_double, ctypes.c_double,
+                                             ctypes.c_double, ctypes.POINTER(ctypes.c_uint64),
+                                             ctypes.POINTER(ctypes.c_uint64), ctypes.c_int, _i64,
+                                             ctypes.c_int, ctypes.POINTER(ctypes.c_void_p)]),
+    "glb_graph_download": (ctypes.c_int, [ctypes.c_void_p, _p64, _p64, _p64]),
     "glb_graph_info": (ctypes.c_int, [ctypes.c_void_p, _p64, _p64,
                                       ctypes.POINTER(ctypes.c_int),
                                       ctypes.POINTER(ctypes.c_int)]),

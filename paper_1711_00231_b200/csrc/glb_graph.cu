@@ -180,6 +180,10 @@ static void upload_int64(glb_graph* g, const int64_t* host, long long count, voi
   cudaEventDestroy(done[1]);
 }
 
+void rmat_device(glb_graph* g, int scale, long long edge_factor, double t_a, double t_ab,
+                 double t_abc, const unsigned long long state[2], const unsigned long long inc[2],
+                 bool weighted, long long max_weight);
+
 void graph_upload(glb_graph* g, const int64_t* row, const int64_t* col, const int64_t* w) {
   GLB_CUDA_TRY(cudaMalloc(&g->row, (size_t)(g->n + 1) * 8));
   GLB_CUDA_TRY(cudaMalloc(&g->col, (size_t)std::max<long long>(g->m, 1) * 4));
@@ -701,6 +705,80 @@ int glb_graph_create(const int64_t* row_offsets, const int64_t* col, const int64
       throw;
     }
     *out = g;
+  });
+}
+
+int glb_graph_create_rmat(int scale, int64_t edge_factor, double t_a, double t_ab, double t_abc,
+                          const uint64_t* state_hi_lo, const uint64_t* inc_hi_lo, int weighted,
+                          int64_t max_weight, int device, glb_graph** out) {
+  return guarded([&] {
+    if (!out || !state_hi_lo || !inc_hi_lo) throw Error{GLB_EINVAL, "NULL argument"};
+    *out = nullptr;
+    if (scale < 1 || scale > 31) throw Error{GLB_EINVAL, "scale must be in [1, 31]"};
+    if (edge_factor < 0) throw Error{GLB_EINVAL, "edge_factor must be nonnegative"};
+    if (((unsigned long long)edge_factor << scale) >= 0xFFFFFFFFull)
+      throw Error{GLB_EINVAL, "the device generator needs fewer than 2^32 edges"};
+    if (weighted && (max_weight < 1 || max_weight >= 0xFFFFFFFFll))
+      throw Error{GLB_EINVAL, "max_weight must be in [1, 2^32-1)"};
+    require_device(device);
+    DeviceGuard dg(device);
+    glb_graph* g = new glb_graph();
+    try {
+      g->device = device;
+      g->n = 1ll << scale;
+      g->m = edge_factor << scale;
+      g->weighted = weighted != 0;
+      GLB_CUDA_TRY(cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking));
+      GLB_CUDA_TRY(cudaDeviceGetAttribute(&g->num_sms, cudaDevAttrMultiProcessorCount, device));
+      GLB_CUDA_TRY(cudaEventCreate(&g->ev[0]));
+      GLB_CUDA_TRY(cudaEventCreate(&g->ev[1]));
+      GLB_CUDA_TRY(cudaHostAlloc(&g->host_ctrl, 1 << 16, cudaHostAllocDefault));
+      const unsigned long long st[2] = {state_hi_lo[0], state_hi_lo[1]};
+      const unsigned long long ic[2] = {inc_hi_lo[0], inc_hi_lo[1]};
+      glb::rmat_device(g, scale, edge_factor, t_a, t_ab, t_abc, st, ic, weighted != 0, max_weight);
+      glb::DevCtrl* ctrl = (glb::DevCtrl*)glb::ensure(g->ws.ctrl, sizeof(glb::DevCtrl));
+      GLB_CUDA_TRY(cudaMemsetAsync(ctrl, 0, sizeof(glb::DevCtrl), g->stream));
+      glb::k_check_rows<<<glb::grid_for(g->n, glb::kBlock, g->num_sms * 8), glb::kBlock, 0,
+                          g->stream>>>(g->row, g->n, g->m, &ctrl->bad_input,
+                                       (unsigned long long*)&ctrl->aux[0]);
+      GLB_CHECK_LAUNCH();
+      long long mx = 0;
+      GLB_CUDA_TRY(cudaMemcpyAsync(&mx, &ctrl->aux[0], 8, cudaMemcpyDeviceToHost, g->stream));
+      GLB_CUDA_TRY(cudaStreamSynchronize(g->stream));
+      g->max_degree = mx;
+    } catch (...) {
+      glb_graph_destroy(g);
+      throw;
+    }
+    *out = g;
+  });
+}
+
+int glb_graph_download(glb_graph* g, int64_t* row_offsets, int64_t* col, int64_t* weights) {
+  return guarded([&] {
+    if (!g) throw Error{GLB_EINVAL, "graph is NULL"};
+    std::lock_guard<std::mutex> lk(g->mu);
+    DeviceGuard dg(g->device);
+    if (row_offsets)
+      GLB_CUDA_TRY(cudaMemcpyAsync(row_offsets, g->row, (size_t)(g->n + 1) * 8,
+                                   cudaMemcpyDeviceToHost, g->stream));
+    auto widen = [&](const uint32_t* src, int64_t* dst) {
+      if (g->m == 0 || !dst) return;
+      const long long chunk = 1ll << 26;
+      long long* d = (long long*)glb::ensure(g->ws.out64, (size_t)std::min<long long>(g->m, chunk) * 8);
+      for (long long off = 0; off < g->m; off += chunk) {
+        const long long len = std::min<long long>(chunk, g->m - off);
+        glb::k_widen_u32_to_i64<<<glb::grid_for(len, glb::kBlock, g->num_sms * 8), glb::kBlock, 0,
+                                  g->stream>>>(src + off, d, len);
+        GLB_CHECK_LAUNCH();
+        GLB_CUDA_TRY(cudaMemcpyAsync(dst + off, d, (size_t)len * 8, cudaMemcpyDeviceToHost,
+                                     g->stream));
+        GLB_CUDA_TRY(cudaStreamSynchronize(g->stream));
+      }
+    };
+    widen(g->col, col);
+    if (g->wt) widen(g->wt, weights);
+    GLB_CUDA_TRY(cudaStreamSynchronize(g->stream));
   });
 }
 

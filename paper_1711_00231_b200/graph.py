@@ -215,6 +215,61 @@ def _uniform_weights(rng: np.random.Generator, m: int, max_weight: int) -> np.nd
     return rng.integers(1, max_weight + 1, size=m, dtype=INDEX_DTYPE)
 
 
+class DeviceCsrGraph:
+    """A CSR graph that lives only in HBM (no host arrays), e.g. a scale-27
+    R-MAT built by ``generate_rmat(..., device=d, download=False)``.  Runs
+    through every strategy like a CsrGraph; ``to_host()`` copies it back."""
+
+    def __init__(self, handle, num_nodes: int, num_edges: int, weighted: bool, device: int):
+        self.num_nodes = num_nodes
+        self.num_edges = num_edges
+        self._weighted = weighted
+        self._device = device
+        self._handles = {device: handle}
+        weakref.finalize(self, _destroy_handles, self._handles)
+
+    @property
+    def is_weighted(self) -> bool:
+        return self._weighted
+
+    def device_graph(self, device: int | None = None):
+        dev = self._device if device is None else int(device)
+        if dev != self._device:
+            raise ValueError(f"graph lives on device {self._device}, not {dev}")
+        return self._handles[dev]
+
+    def release_device(self) -> None:
+        _destroy_handles(self._handles)
+
+    def to_host(self) -> CsrGraph:
+        row = np.empty(self.num_nodes + 1, dtype=INDEX_DTYPE)
+        col = np.empty(self.num_edges, dtype=INDEX_DTYPE)
+        w = np.empty(self.num_edges, dtype=INDEX_DTYPE) if self._weighted else None
+        _lib.check(_lib.lib().glb_graph_download(self._handles[self._device], _lib.ptr64(row),
+                                                 _lib.ptr64(col), _lib.ptr64(w)),
+                   "glb_graph_download")
+        g = CsrGraph(self.num_nodes, self.num_edges, row, col, w)
+        return g
+
+
+def _rmat_device(scale, edge_factor, a, b, c, seed, weighted, max_weight, device, download):
+    st = np.random.default_rng(seed).bit_generator.state["state"]
+    mask = (1 << 64) - 1
+    state = (ctypes.c_uint64 * 2)(st["state"] >> 64, st["state"] & mask)
+    inc = (ctypes.c_uint64 * 2)(st["inc"] >> 64, st["inc"] & mask)
+    h = ctypes.c_void_p()
+    _lib.check(_lib.lib().glb_graph_create_rmat(scale, edge_factor, float(a), float(a + b),
+                                                float(a + b + c), state, inc, 1 if weighted else 0,
+                                                int(max_weight), int(device), ctypes.byref(h)),
+               "glb_graph_create_rmat")
+    dg = DeviceCsrGraph(h.value, 1 << scale, edge_factor << scale, weighted, int(device))
+    if not download:
+        return dg
+    g = dg.to_host()
+    g._handles[int(device)] = dg._handles.pop(int(device))  # keep the HBM copy
+    return g
+
+
 def generate_rmat(
     scale: int,
     edge_factor: int,
@@ -222,11 +277,17 @@ def generate_rmat(
     seed: int = 0,
     weighted: bool = True,
     max_weight: int = DEFAULT_MAX_WEIGHT,
+    device: int | None = None,
+    download: bool = True,
 ) -> CsrGraph:
     """R-MAT graph with 2**scale nodes and edge_factor * 2**scale edges.
 
     Same draw order as generators.py:23-58: ``scale`` blocks of m uniforms
-    (one quadrant decision per level for every edge), then m weights.
+    (one quadrant decision per level for every edge), then m weights.  With
+    ``device`` set, the graph is generated directly in HBM by the CUDA
+    library (same PCG64 stream, identical arrays) and, unless ``download`` is
+    False, copied back so the result is a regular CsrGraph already resident
+    on that device.
     """
     a, b, c, d = params
     if abs(a + b + c + d - 1.0) > 1e-9:
@@ -237,6 +298,9 @@ def generate_rmat(
         raise ValueError("scale must be >= 1")
     if edge_factor < 0:
         raise ValueError("edge_factor must be nonnegative")
+    if device is not None:
+        return _rmat_device(scale, edge_factor, a, b, c, seed, weighted, max_weight, device,
+                            download)
     n = 1 << scale
     m = edge_factor * n
     rng = np.random.default_rng(seed)

@@ -248,3 +248,29 @@ def test_c2_rmat22_all_strategies(oracle, golden):
             r = pkg.run_strategy(tag, g, 0, pkg.RelaxOp(algo), pkg.KernelConfig(loop="graph"))
             assert np.array_equal(r.dist.array, exp), (algo, tag)
     g.release_device()
+
+
+def test_device_rmat_generator_matches_numpy(golden):
+    # bit-identical to the reference generator (and to the numpy path)
+    d = golden["generators"]
+    specs = dict(d["extra_specs"])
+    specs.update({k: v for k, v in gs.CORPUS.items() if v["kind"] == "rmat"})
+    for gid, spec in specs.items():
+        if spec["kind"] != "rmat":
+            continue
+        kw = dict(seed=spec["seed"], weighted=spec.get("weighted", True))
+        if "max_weight" in spec:
+            kw["max_weight"] = spec["max_weight"]
+        if "params" in spec:
+            kw["params"] = tuple(spec["params"])
+        g = pkg.generate_rmat(spec["scale"], spec["edge_factor"], device=0, **kw)
+        assert gs.digest(g) == d["digests"][gid], gid
+    # odd weights exercise the Lemire rejection threshold (2^32 mod W != 1)
+    for w in (3, 7, 1000, 65535):
+        a = pkg.generate_rmat(11, 8, seed=5, max_weight=w)
+        b = pkg.generate_rmat(11, 8, seed=5, max_weight=w, device=0)
+        assert gs.digest(a) == gs.digest(b), w
+    dg = pkg.generate_rmat(12, 8, seed=3, device=0, download=False)
+    r = pkg.run_wd(dg, 0, pkg.RelaxOp("sssp"), pkg.KernelConfig())
+    h = pkg.generate_rmat(12, 8, seed=3)
+    assert np.array_equal(r.dist.array, pkg.run_wd(h, 0, pkg.RelaxOp("sssp"), pkg.KernelConfig()).dist.array)
