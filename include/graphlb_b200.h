@@ -165,6 +165,27 @@ int glb_run(glb_graph* g, const glb_run_params* params, int64_t* dist_out,
 int glb_run_records(glb_graph* g, int64_t offset, glb_record* records,
                     int64_t capacity, int64_t* written);
 
+/* ---- sharded runs: 1-D vertex partition across ranks ----
+ * Every rank holds the graph over the GLOBAL id space with only its own rows
+ * (glb_graph_restrict) and runs BS / WD / HP locally; per iteration:
+ *   glb_shard_local  -> run to the iteration boundary, split the improved
+ *                       vertices by owner: send_buf (device, u64 entries
+ *                       dist << 32 | v) grouped by owner, counts per owner;
+ *   (host exchanges the buckets, e.g. NCCL all-to-all)
+ *   glb_shard_apply  -> relax the received entries (device buffer);
+ *   glb_shard_advance-> swap worklists; *frontier = local frontier size
+ *                       (global termination: all-reduce of frontiers);
+ *   glb_shard_finish -> int64 distances of the owned range [lo, hi). */
+int glb_graph_partition(glb_graph* g, int parts, int64_t* bounds);
+int glb_graph_restrict(glb_graph* g, int64_t v_lo, int64_t v_hi);
+int glb_shard_begin(glb_graph* g, const glb_run_params* params, const int64_t* bounds,
+                    int parts, int rank);
+int glb_shard_local(glb_graph* g, int64_t* send_counts, void* send_buf,
+                    int64_t send_capacity, int64_t* local_next);
+int glb_shard_apply(glb_graph* g, const void* recv_buf, int64_t nrecv);
+int glb_shard_advance(glb_graph* g, int64_t* frontier);
+int glb_shard_finish(glb_graph* g, int64_t* dist_owned, glb_run_stats* stats);
+
 /* ---- degree analysis (degrees.py) ---- */
 int glb_degree_stats(glb_graph* g, int64_t* max_degree, int64_t* sum_degree,
                      double* sum_sq_degree);

@@ -77,6 +77,14 @@ SIGNATURES = {
                                              ctypes.POINTER(ctypes.c_uint64), ctypes.c_int, _i64,
                                              ctypes.c_int, ctypes.POINTER(ctypes.c_void_p)]),
     "glb_graph_download": (ctypes.c_int, [ctypes.c_void_p, _p64, _p64, _p64]),
+    "glb_graph_partition": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, _p64]),
+    "glb_graph_restrict": (ctypes.c_int, [ctypes.c_void_p, _i64, _i64]),
+    "glb_shard_begin": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(RunParams), _p64, ctypes.c_int,
+                                       ctypes.c_int]),
+    "glb_shard_local": (ctypes.c_int, [ctypes.c_void_p, _p64, ctypes.c_void_p, _i64, _p64]),
+    "glb_shard_apply": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, _i64]),
+    "glb_shard_advance": (ctypes.c_int, [ctypes.c_void_p, _p64]),
+    "glb_shard_finish": (ctypes.c_int, [ctypes.c_void_p, _p64, ctypes.POINTER(RunStats)]),
     "glb_graph_info": (ctypes.c_int, [ctypes.c_void_p, _p64, _p64,
                                       ctypes.POINTER(ctypes.c_int),
                                       ctypes.POINTER(ctypes.c_int)]),

@@ -14,6 +14,15 @@
 
 namespace glb {
 
+// Sharded runs stop at the iteration boundary (before the worklist swap) so
+// the host can exchange remote updates; k_shard_advance resumes.
+__device__ __forceinline__ bool ctl_pause(DevCtrl* c) {
+  if (!c->shard_mode) return false;
+  c->paused = 1;
+  c->done = 1;
+  return true;
+}
+
 __device__ __forceinline__ void ctl_simple_advance(DevCtrl* c) {
   // wl_in.clear(); swap(wl_in, wl_out)  (node_based.py:75-79)
   const unsigned produced = c->qcount[c->out];
@@ -47,6 +56,7 @@ __device__ __forceinline__ void hp_begin_super(DevCtrl* c) {
 }
 
 __device__ __forceinline__ void hp_end_super(DevCtrl* c) {
+  if (ctl_pause(c)) return;
   // super_in.clear(); swap(super_in, super_out)  (hierarchical.py:134-137)
   const unsigned produced = c->qcount[c->sup_out];
   c->qcount[c->sup_in] = 0;
@@ -132,6 +142,7 @@ __global__ void k_control_init(DevCtrl* c, cudaGraphConditionalHandle h_loop,
       c->tag = strategy;
       break;
   }
+  if (c->shard_mode) c->done = 0;  // every shard steps, even with an empty frontier
   if (c->done) c->mode = kModeDone;
   ctl_set_conditionals(c, h_loop, h_mode, graph_mode);
 }
@@ -181,6 +192,7 @@ __global__ void k_control(DevCtrl* c, cudaGraphConditionalHandle h_loop,
   ctl_reset_timers(c);
   switch (c->strategy) {
     case GLB_WD:
+      if (ctl_pause(c)) break;
       if (wd_empty) {  // active nodes have no out-edges (workload.py:181-183)
         c->done = 1;
       } else {
@@ -200,11 +212,35 @@ __global__ void k_control(DevCtrl* c, cudaGraphConditionalHandle h_loop,
       }
       break;
     default:
-      ctl_simple_advance(c);
+      if (!ctl_pause(c)) ctl_simple_advance(c);
       break;
   }
-  if (c->done) c->mode = kModeDone;
+  if (c->done && !c->paused) c->mode = kModeDone;
   ctl_set_conditionals(c, h_loop, h_mode, graph_mode);
+}
+
+// Resume a paused sharded run: the deferred worklist swap / super-iteration
+// switch.  Global termination is the host's all-reduce, not `produced`.
+__global__ void k_shard_advance(DevCtrl* c) {
+  if (threadIdx.x != 0) return;
+  c->paused = 0;
+  c->done = 0;
+  if (c->strategy == GLB_HP) {
+    c->qcount[c->sup_in] = 0;
+    const int t = c->sup_in;
+    c->sup_in = c->sup_out;
+    c->sup_out = t;
+    c->gen += 1;
+    c->iteration += 1;
+    hp_begin_super(c);
+  } else {
+    ctl_simple_advance(c);
+    c->done = 0;
+    c->mode = c->strategy == GLB_WD ? kModeWD : kModeRelax;
+    c->tag = c->strategy;
+    c->sub = -1;
+    c->window = 0;
+  }
 }
 
 }  // namespace glb

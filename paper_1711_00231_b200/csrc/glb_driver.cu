@@ -61,6 +61,17 @@ class Runner {
       : g_(g), p_(p), recs_(recs), s_(g->stream) {}
 
   void run(int64_t* dist_out, glb_run_stats* st) {
+    prepare(st);
+    if (p_.loop_mode == GLB_LOOP_GRAPH)
+      loop_graph();
+    else
+      loop_host();
+    finish_run(dist_out, st, 0, g_->n);
+  }
+
+ protected:
+  // per-run preprocessing + state (the reference's "setup overhead")
+  void prepare(glb_run_stats* st) {
     const double t0 = now_ms();
     GLB_CUDA_TRY(cudaEventRecord(g_->ev[0], s_));
     n_out_ = g_->n;
@@ -97,20 +108,21 @@ class Runner {
     }
     alloc_state();
     setup_ms_ = now_ms() - t0;
+  }
 
-    if (p_.loop_mode == GLB_LOOP_GRAPH)
-      loop_graph();
-    else
-      loop_host();
-
-    long long* out = (long long*)ensure(g_->ws.out64, (size_t)std::max<long long>(n_out_, 1) * 8);
-    k_dist_out<D><<<grid_for(n_out_, kBlock, g_->num_sms * 8), kBlock, 0, s_>>>(cells_, n_out_,
-                                                                                  out);
-    GLB_CHECK_LAUNCH();
+  // distances of ids [lo, hi) to the host, counters into records / stats
+  void finish_run(int64_t* dist_out, glb_run_stats* st, long long lo, long long hi) {
+    const long long cnt = std::max<long long>(hi - lo, 0);
+    long long* out = (long long*)ensure(g_->ws.out64, (size_t)std::max<long long>(cnt, 1) * 8);
+    if (cnt) {
+      k_dist_out<D><<<grid_for(cnt, kBlock, g_->num_sms * 8), kBlock, 0, s_>>>(cells_ + lo, cnt,
+                                                                                out);
+      GLB_CHECK_LAUNCH();
+    }
     GLB_CUDA_TRY(cudaEventRecord(g_->ev[1], s_));
     GLB_CUDA_TRY(cudaMemcpyAsync(&h_->ctrl, ctrl_, sizeof(DevCtrl), cudaMemcpyDeviceToHost, s_));
-    if (n_out_ > 0 && dist_out)
-      GLB_CUDA_TRY(cudaMemcpyAsync(dist_out, out, (size_t)n_out_ * 8, cudaMemcpyDeviceToHost, s_));
+    if (cnt > 0 && dist_out)
+      GLB_CUDA_TRY(cudaMemcpyAsync(dist_out, out, (size_t)cnt * 8, cudaMemcpyDeviceToHost, s_));
     GLB_CUDA_TRY(cudaStreamSynchronize(s_));
     if (h_->ctrl.overflow) throw OverflowRestart{};
     g_->stamp_epoch = h_->ctrl.gen;
@@ -121,7 +133,6 @@ class Runner {
     finish(st, dev_ms);
   }
 
- private:
   glb_graph* g_;
   const glb_run_params& p_;
   std::vector<glb_record>& recs_;
@@ -149,6 +160,7 @@ class Runner {
   int cap_relax_ = 0, cap_scan_ = 0, cap_wd_ = 0, cap_hp_ = 0;
   double setup_ms_ = 0;
   long long seed_count_ = 0;
+  bool shard_mode_ = false;
   // host-loop per-record event timing
   struct EvPair {
     cudaEvent_t k0, k1, o0, o1;
@@ -232,6 +244,7 @@ class Runner {
     c.gen = g_->stamp_epoch;
     c.scan_epoch = g_->scan_epoch + 1;
     c.rec_cap = kMaxRecords;
+    c.shard_mode = shard_mode_ ? 1 : 0;
     c.recs = drecs_;
     c.ls = ls_;
     h_->ctrl = c;
@@ -343,6 +356,11 @@ class Runner {
     k_control_init<<<1, 32, 0, s_>>>(ctrl_, 0, 0, 0);
     GLB_CHECK_LAUNCH();
     read_ctrl();
+    step_host();
+  }
+
+  // launch steps until the control block reports done (or paused)
+  void step_host() {
     const bool timing = p_.record_timing != 0;
     while (!h_->ctrl.done) {
       const DevCtrl& c = h_->ctrl;
@@ -567,6 +585,174 @@ class Runner {
   }
 };
 
+// =========================================================== sharded run ===
+// 1-D vertex partition: the shard is a graph over the GLOBAL id
+// space whose rows outside [lo, hi) are empty, so every strategy kernel runs
+// unchanged on the owned frontier.  Cells of remote vertices act as
+// sender-side shadows: a candidate for remote v is atomically min-combined
+// into cells[v], and v is pushed once per generation like any improvement.
+// At the iteration boundary the out list is split by owner; remote entries
+// (v, best candidate) go to per-owner send buckets that the host exchanges
+// (NCCL all-to-all), and received updates are relaxed into the owner's cells
+// with the same generation, so local and remote pushes deduplicate together.
+
+__device__ __forceinline__ int owner_of(const long long* __restrict__ bounds, int parts,
+                                        uint32_t v) {
+  int lo = 0, hi = parts;  // bounds[0] = 0 <= v < bounds[parts]
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if ((long long)v >= bounds[mid])
+      lo = mid;
+    else
+      hi = mid;
+  }
+  return lo;
+}
+
+struct ShardBounds {
+  long long b[65];
+};
+
+__global__ void k_shard_count(const DevCtrl* __restrict__ c, ShardBounds sb, int parts,
+                              unsigned long long* __restrict__ counts) {
+  __shared__ unsigned int s_cnt[64];
+  if (threadIdx.x < 64) s_cnt[threadIdx.x] = 0;
+  __syncthreads();
+  const int ol = c->strategy == GLB_HP ? c->sup_out : c->out;
+  const uint32_t* q = c->qptr[ol];
+  const unsigned n = c->qcount[ol];
+  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    atomicAdd(&s_cnt[owner_of(sb.b, parts, q[i])], 1u);
+  __syncthreads();
+  if (threadIdx.x < parts && s_cnt[threadIdx.x])
+    atomicAdd(counts + threadIdx.x, (unsigned long long)s_cnt[threadIdx.x]);
+}
+
+// cursors[o] start at the owner's offset in `send`; the local owner's cursor
+// indexes `local_tmp`.
+__global__ void k_shard_scatter(const DevCtrl* __restrict__ c, ShardBounds sb, int parts, int me,
+                                const unsigned long long* __restrict__ cells,
+                                unsigned long long* __restrict__ cursors,
+                                unsigned long long* __restrict__ send,
+                                uint32_t* __restrict__ local_tmp) {
+  const int ol = c->strategy == GLB_HP ? c->sup_out : c->out;
+  const uint32_t* q = c->qptr[ol];
+  const unsigned n = c->qcount[ol];
+  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const uint32_t v = q[i];
+    const int o = owner_of(sb.b, parts, v);
+    const unsigned long long slot = atomicAdd(cursors + o, 1ull);
+    if (o == me)
+      local_tmp[slot] = v;
+    else
+      send[slot] = ((unsigned long long)Cell<uint32_t>::dist(cells[v]) << 32) | v;
+  }
+}
+
+// received (dist << 32 | v) updates: relax with this iteration's generation
+__global__ void k_shard_apply(DevCtrl* __restrict__ c, unsigned long long* __restrict__ cells,
+                              const unsigned long long* __restrict__ recv, long long nrecv) {
+  const int ol = c->strategy == GLB_HP ? c->sup_out : c->out;
+  uint32_t* q = c->qptr[ol];
+  unsigned int* nq = &c->qcount[ol];
+  const uint32_t gen = c->gen;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nrecv;
+       i += (long long)gridDim.x * blockDim.x) {
+    const unsigned long long e = recv[i];
+    const uint32_t v = (uint32_t)e, d = (uint32_t)(e >> 32);
+    bool first = false;
+    if (relax_cell<uint32_t>(cells, v, d, gen, &first) && first) q_append(q, nq, v);
+  }
+}
+
+template <bool W>
+class ShardSession : public ShardSessionBase, public Runner<uint32_t, W> {
+  using R = Runner<uint32_t, W>;
+
+ public:
+  ShardSession(glb_graph* g, const glb_run_params& p, const long long* bounds, int parts, int rank)
+      : R(g, params_, recs_), params_(p), parts_(parts), me_(rank) {
+    for (int i = 0; i <= parts; ++i) sb_.b[i] = bounds[i];
+    lo_ = bounds[rank];
+    hi_ = bounds[rank + 1];
+    this->shard_mode_ = true;
+    std::memset(&stats_, 0, sizeof(stats_));
+    stats_.split_fraction = -1.0;
+    R::prepare(&stats_);
+    if (p.source < lo_ || p.source >= hi_)  // not ours: start with an empty frontier
+      GLB_CUDA_TRY(cudaMemsetAsync(&this->ctrl_->qcount[0], 0, 4, this->s_));
+    k_control_init<<<1, 32, 0, this->s_>>>(this->ctrl_, 0, 0, 0);
+    GLB_CHECK_LAUNCH();
+    this->read_ctrl();
+    counts_ = (unsigned long long*)ensure(g->ws.misc_small, 64 * 8 * 2);
+    tmp_ = (uint32_t*)ensure(g->ws.shard_tmp, (size_t)std::max<long long>(g->n, 1) * 4);
+  }
+
+  void local(int64_t* send_counts, unsigned long long* send, long long cap,
+             int64_t* local_next) override {
+    this->step_host();  // until the control block pauses at the iteration boundary
+    const DevCtrl& hc = this->h_->ctrl;
+    const int ol = hc.strategy == GLB_HP ? hc.sup_out : hc.out;
+    const long long n = hc.qcount[ol];
+    cudaStream_t s = this->s_;
+    GLB_CUDA_TRY(cudaMemsetAsync(counts_, 0, 64 * 8, s));
+    const unsigned grid = grid_for(std::max<long long>(n, 1), kBlock, this->g_->num_sms * 4);
+    k_shard_count<<<grid, kBlock, 0, s>>>(this->ctrl_, sb_, parts_, counts_);
+    GLB_CHECK_LAUNCH();
+    unsigned long long h[64];
+    GLB_CUDA_TRY(cudaMemcpyAsync(h, counts_, 8 * parts_, cudaMemcpyDeviceToHost, s));
+    GLB_CUDA_TRY(cudaStreamSynchronize(s));
+    unsigned long long off[64], run = 0;
+    for (int o = 0; o < parts_; ++o) {
+      off[o] = o == me_ ? 0 : run;
+      if (o != me_) run += h[o];
+      send_counts[o] = o == me_ ? 0 : (int64_t)h[o];
+    }
+    if ((long long)run > cap) throw Error{GLB_ENOMEM, "shard send buffer too small"};
+    GLB_CUDA_TRY(cudaMemcpyAsync(counts_ + 64, off, 8 * parts_, cudaMemcpyHostToDevice, s));
+    k_shard_scatter<<<grid, kBlock, 0, s>>>(this->ctrl_, sb_, parts_, me_, this->cells_,
+                                            counts_ + 64, send, tmp_);
+    GLB_CHECK_LAUNCH();
+    // the out list keeps only owned vertices
+    const unsigned nlocal = (unsigned)h[me_];
+    GLB_CUDA_TRY(cudaMemcpyAsync(this->q_[ol], tmp_, (size_t)nlocal * 4, cudaMemcpyDeviceToDevice, s));
+    GLB_CUDA_TRY(cudaMemcpyAsync(&this->ctrl_->qcount[ol], &nlocal, 4, cudaMemcpyHostToDevice, s));
+    GLB_CUDA_TRY(cudaStreamSynchronize(s));
+    *local_next = nlocal;
+  }
+
+  void apply(const unsigned long long* recv, long long n) override {
+    if (n > 0) {
+      k_shard_apply<<<grid_for(n, kBlock, this->g_->num_sms * 4), kBlock, 0, this->s_>>>(
+          this->ctrl_, this->cells_, recv, n);
+      GLB_CHECK_LAUNCH();
+    }
+  }
+
+  long long advance() override {
+    k_shard_advance<<<1, 32, 0, this->s_>>>(this->ctrl_);
+    GLB_CHECK_LAUNCH();
+    this->read_ctrl();
+    const DevCtrl& hc = this->h_->ctrl;
+    return hc.strategy == GLB_HP ? hc.qcount[hc.sup_in] : hc.qcount[hc.in];
+  }
+
+  void finish(int64_t* dist_owned, glb_run_stats* st) override {
+    R::finish_run(dist_owned, &stats_, lo_, hi_);
+    *st = stats_;
+  }
+
+ private:
+  glb_run_params params_;
+  std::vector<glb_record> recs_;
+  glb_run_stats stats_;
+  ShardBounds sb_;
+  int parts_, me_;
+  long long lo_, hi_;
+  unsigned long long* counts_ = nullptr;
+  uint32_t* tmp_ = nullptr;
+};
+
 template <typename D>
 void run_typed(glb_graph* g, const glb_run_params& p, int64_t* dist_out, glb_run_stats* st,
                std::vector<glb_record>& recs) {
@@ -604,6 +790,8 @@ void run_guarded(glb_graph* g, const glb_run_params& p, int64_t* dist_out, glb_r
 }
 
 }  // namespace
+
+void reset_epochs_public(glb_graph* g) { reset_epochs(g); }
 
 void run(glb_graph* g, const glb_run_params& p, int64_t* dist_out, glb_run_stats* st,
          std::vector<glb_record>& recs) {
@@ -706,4 +894,105 @@ extern "C" int glb_run_records(glb_graph* g, int64_t offset, glb_record* records
   if (k > 0) std::memcpy(records, g->last_records.data() + offset, (size_t)k * sizeof(glb_record));
   *written = k;
   return GLB_OK;
+}
+
+// ============================================================ shard C-ABI ===
+namespace {
+template <typename F>
+int shard_guard(glb_graph* g, F&& f) {
+  try {
+    if (!g) throw glb::Error{GLB_EINVAL, "graph is NULL"};
+    std::lock_guard<std::mutex> lk(g->mu);
+    int prev = -1;
+    cudaGetDevice(&prev);
+    GLB_CUDA_TRY(cudaSetDevice(g->device));
+    try {
+      f();
+    } catch (...) {
+      if (prev >= 0) cudaSetDevice(prev);
+      throw;
+    }
+    if (prev >= 0) cudaSetDevice(prev);
+    return GLB_OK;
+  } catch (const glb::Error& e) {
+    glb::set_error(e.msg);
+    return e.code;
+  } catch (const std::exception& e) {
+    glb::set_error(e.what());
+    return GLB_ECUDA;
+  }
+}
+}  // namespace
+
+extern "C" int glb_shard_begin(glb_graph* g, const glb_run_params* p, const int64_t* bounds,
+                               int parts, int rank) {
+  return shard_guard(g, [&] {
+    if (!p || !bounds) throw glb::Error{GLB_EINVAL, "params/bounds is NULL"};
+    if (parts < 1 || parts > 64 || rank < 0 || rank >= parts)
+      throw glb::Error{GLB_EINVAL, "parts must be in [1, 64] and 0 <= rank < parts"};
+    if (bounds[0] != 0 || bounds[parts] != g->n)
+      throw glb::Error{GLB_EINVAL, "bounds must start at 0 and end at num_nodes"};
+    for (int i = 0; i < parts; ++i)
+      if (bounds[i + 1] < bounds[i]) throw glb::Error{GLB_EINVAL, "bounds must be nondecreasing"};
+    if (p->strategy != GLB_BS && p->strategy != GLB_WD && p->strategy != GLB_HP)
+      throw glb::Error{GLB_EINVAL, "sharded runs support the BS, WD and HP strategies"};
+    if (p->algo != GLB_BFS && p->algo != GLB_SSSP) throw glb::Error{GLB_EINVAL, "unknown algo"};
+    if (p->source < 0 || p->source >= g->n)
+      throw glb::Error{GLB_EINVAL, "source out of range"};
+    if (p->block_size < 1) throw glb::Error{GLB_EINVAL, "block_size must be >= 1"};
+    if (p->dist_bits == 64) throw glb::Error{GLB_EINVAL, "sharded runs use 32-bit distances"};
+    delete g->shard;
+    g->shard = nullptr;
+    const bool weighted = p->algo == GLB_SSSP && g->wt != nullptr;
+    long long bb[65];
+    for (int i = 0; i <= parts; ++i) bb[i] = bounds[i];
+    if (weighted)
+      g->shard = new glb::ShardSession<true>(g, *p, bb, parts, rank);
+    else
+      g->shard = new glb::ShardSession<false>(g, *p, bb, parts, rank);
+  });
+}
+
+extern "C" int glb_shard_local(glb_graph* g, int64_t* send_counts, void* send_buf,
+                               int64_t send_capacity, int64_t* local_next) {
+  return shard_guard(g, [&] {
+    if (!g->shard) throw glb::Error{GLB_EINVAL, "no sharded run in progress"};
+    if (!send_counts || !local_next || (!send_buf && send_capacity > 0))
+      throw glb::Error{GLB_EINVAL, "NULL argument"};
+    g->shard->local(send_counts, (unsigned long long*)send_buf, send_capacity, local_next);
+  });
+}
+
+extern "C" int glb_shard_apply(glb_graph* g, const void* recv_buf, int64_t nrecv) {
+  return shard_guard(g, [&] {
+    if (!g->shard) throw glb::Error{GLB_EINVAL, "no sharded run in progress"};
+    if (nrecv < 0 || (nrecv > 0 && !recv_buf)) throw glb::Error{GLB_EINVAL, "bad receive buffer"};
+    g->shard->apply((const unsigned long long*)recv_buf, nrecv);
+  });
+}
+
+extern "C" int glb_shard_advance(glb_graph* g, int64_t* frontier) {
+  return shard_guard(g, [&] {
+    if (!g->shard) throw glb::Error{GLB_EINVAL, "no sharded run in progress"};
+    const long long f = g->shard->advance();
+    if (frontier) *frontier = f;
+  });
+}
+
+extern "C" int glb_shard_finish(glb_graph* g, int64_t* dist_owned, glb_run_stats* stats) {
+  return shard_guard(g, [&] {
+    if (!g->shard) throw glb::Error{GLB_EINVAL, "no sharded run in progress"};
+    glb_run_stats st;
+    try {
+      g->shard->finish(dist_owned, &st);
+    } catch (...) {
+      delete g->shard;
+      g->shard = nullptr;
+      glb::reset_epochs_public(g);
+      throw;
+    }
+    if (stats) *stats = st;
+    delete g->shard;
+    g->shard = nullptr;
+  });
 }

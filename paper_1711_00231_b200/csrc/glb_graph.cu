@@ -605,6 +605,7 @@ __global__ void k_find_offsets(const long long* __restrict__ prefix, long long s
 
 // ================================================================ C-ABI ===
 using glb::Error;
+using namespace glb;
 
 namespace {
 struct DeviceGuard {
@@ -782,6 +783,83 @@ int glb_graph_download(glb_graph* g, int64_t* row_offsets, int64_t* col, int64_t
   });
 }
 
+int glb_graph_partition(glb_graph* g, int parts, int64_t* bounds) {
+  return guarded([&] {
+    if (!g || !bounds) throw Error{GLB_EINVAL, "NULL argument"};
+    if (parts < 1 || parts > 64) throw Error{GLB_EINVAL, "parts must be in [1, 64]"};
+    std::lock_guard<std::mutex> lk(g->mu);
+    DeviceGuard dg(g->device);
+    // edge-balanced contiguous ranges: bounds[r] = first v with row[v] >= r*m/parts
+    std::vector<long long> h((size_t)g->n + 1);
+    GLB_CUDA_TRY(cudaMemcpy(h.data(), g->row, ((size_t)g->n + 1) * 8, cudaMemcpyDeviceToHost));
+    bounds[0] = 0;
+    for (int r = 1; r < parts; ++r) {
+      const long long target = (long long)((__int128)g->m * r / parts);
+      bounds[r] = std::lower_bound(h.begin(), h.end() - 1, target) - h.begin();
+      if (bounds[r] < bounds[r - 1]) bounds[r] = bounds[r - 1];
+    }
+    bounds[parts] = g->n;
+  });
+}
+
+__global__ void k_restrict_rows(const long long* __restrict__ row, long long n, long long lo,
+                                long long hi, long long e_lo, long long e_hi,
+                                long long* __restrict__ out) {
+  for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; v <= n;
+       v += (long long)gridDim.x * blockDim.x) {
+    long long r = row[v];
+    r = r < e_lo ? e_lo : (r > e_hi ? e_hi : r);
+    out[v] = (v <= lo ? e_lo : (v >= hi ? e_hi : r)) - e_lo;
+  }
+}
+
+int glb_graph_restrict(glb_graph* g, int64_t v_lo, int64_t v_hi) {
+  return guarded([&] {
+    if (!g) throw Error{GLB_EINVAL, "graph is NULL"};
+    if (v_lo < 0 || v_hi < v_lo || v_hi > g->n) throw Error{GLB_EINVAL, "bad vertex range"};
+    std::lock_guard<std::mutex> lk(g->mu);
+    DeviceGuard dg(g->device);
+    long long e[2];
+    GLB_CUDA_TRY(cudaMemcpy(&e[0], g->row + v_lo, 8, cudaMemcpyDeviceToHost));
+    GLB_CUDA_TRY(cudaMemcpy(&e[1], g->row + v_hi, 8, cudaMemcpyDeviceToHost));
+    const long long m2 = e[1] - e[0];
+    long long* row2 = nullptr;
+    uint32_t *col2 = nullptr, *w2 = nullptr;
+    GLB_CUDA_TRY(cudaMalloc(&row2, (size_t)(g->n + 1) * 8));
+    GLB_CUDA_TRY(cudaMalloc(&col2, (size_t)std::max<long long>(m2, 1) * 4));
+    if (g->wt) GLB_CUDA_TRY(cudaMalloc(&w2, (size_t)std::max<long long>(m2, 1) * 4));
+    k_restrict_rows<<<grid_for(g->n + 1, kBlock, g->num_sms * 8), kBlock, 0, g->stream>>>(
+        g->row, g->n, v_lo, v_hi, e[0], e[1], row2);
+    GLB_CHECK_LAUNCH();
+    if (m2) {
+      GLB_CUDA_TRY(cudaMemcpyAsync(col2, g->col + e[0], (size_t)m2 * 4, cudaMemcpyDeviceToDevice,
+                                   g->stream));
+      if (g->wt)
+        GLB_CUDA_TRY(cudaMemcpyAsync(w2, g->wt + e[0], (size_t)m2 * 4, cudaMemcpyDeviceToDevice,
+                                     g->stream));
+    }
+    GLB_CUDA_TRY(cudaStreamSynchronize(g->stream));
+    cudaFree(g->row);
+    cudaFree(g->col);
+    cudaFree(g->wt);
+    g->row = row2;
+    g->col = col2;
+    g->wt = w2;
+    g->m = m2;
+    for (auto& kv : g->gexec) cudaGraphExecDestroy(kv.second);
+    g->gexec.clear();
+    DevCtrl* ctrl = (DevCtrl*)ensure(g->ws.ctrl, sizeof(DevCtrl));
+    GLB_CUDA_TRY(cudaMemsetAsync(ctrl, 0, sizeof(DevCtrl), g->stream));
+    k_check_rows<<<grid_for(g->n, kBlock, g->num_sms * 8), kBlock, 0, g->stream>>>(
+        g->row, g->n, g->m, &ctrl->bad_input, (unsigned long long*)&ctrl->aux[0]);
+    GLB_CHECK_LAUNCH();
+    long long mx = 0;
+    GLB_CUDA_TRY(cudaMemcpyAsync(&mx, &ctrl->aux[0], 8, cudaMemcpyDeviceToHost, g->stream));
+    GLB_CUDA_TRY(cudaStreamSynchronize(g->stream));
+    g->max_degree = mx;
+  });
+}
+
 int glb_graph_destroy(glb_graph* g) {
   if (!g) return GLB_OK;
   int prev = -1;
@@ -798,6 +876,8 @@ int glb_graph_destroy(glb_graph* g) {
                          &ws.ns_col, &ws.ns_w,   &ws.ns_parent, &ws.ns_cs,  &ws.ns_tmp,
                          &ws.ep_src, &ws.eq[0],  &ws.eq[1],    &ws.out64,   &ws.misc,
                          &ws.recs,   &ws.hist,   &ws.tile_node};
+  delete g->shard;
+  g->shard = nullptr;
   for (auto& kv : g->gexec) cudaGraphExecDestroy(kv.second);
   g->gexec.clear();
   for (auto* b : bufs) glb::free_buf(*b);

@@ -142,6 +142,8 @@ struct DevCtrl {
   unsigned int scan_epoch;      // look-back epoch of the next WD scan
   int done;
   unsigned long long scan_ticket, relax_ticket;  // dynamic tile tickets of the WD step
+  int shard_mode;   // sharded run: pause at every iteration boundary for the exchange
+  int paused;
   // ---- HP super-iteration state (hierarchical.py:54-136)
   int sup_in, sup_out, cur, spare;
   long long s;
@@ -173,8 +175,21 @@ struct Workspace {
   DevBuf misc;
   DevBuf hist;                               // histogram counts
   DevBuf tile_node;                          // first node of every edge tile
+  DevBuf misc_small, shard_tmp;              // sharded-run counters / local split
 };
 
+}  // namespace glb
+
+namespace glb {
+// One rank's part of a sharded run (glb_shard_* C-ABI, glb_driver.cu).
+struct ShardSessionBase {
+  virtual ~ShardSessionBase() {}
+  virtual void local(int64_t* send_counts, unsigned long long* send, long long cap,
+                     int64_t* local_next) = 0;
+  virtual void apply(const unsigned long long* recv, long long n) = 0;
+  virtual long long advance() = 0;
+  virtual void finish(int64_t* dist_owned, glb_run_stats* st) = 0;
+};
 }  // namespace glb
 
 struct glb_graph {
@@ -197,6 +212,7 @@ struct glb_graph {
   std::vector<cudaEvent_t> ev_pool;
   std::vector<glb_record> last_records;  // records of the most recent glb_run
   std::vector<std::pair<std::string, cudaGraphExec_t>> gexec;  // instantiated loops
+  glb::ShardSessionBase* shard = nullptr;                       // sharded run in progress
   std::mutex mu;              // drivers are not re-entrant (common.py:5-6)
 };
 

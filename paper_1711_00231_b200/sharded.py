@@ -1,0 +1,249 @@
+"""Multi-GPU BFS/SSSP: 1-D vertex partition with a per-iteration exchange.
+
+Each rank owns a contiguous, edge-balanced vertex range [lo, hi) and holds the
+graph over the GLOBAL id space with only its own rows (``glb_graph_restrict``),
+so the single-GPU strategy kernels (BS, WD, HP) run unchanged on the owned
+frontier.  Per iteration (bulk-synchronous, as the reference's host loop):
+
+1. ``local``   -- the rank relaxes its frontier to the iteration boundary;
+                  candidates for remote vertices are min-combined on the
+                  sender (shadow cells) and bucketed by owner;
+2. ``exchange``-- the (dist << 32 | v) buckets go to their owners: NCCL
+                  all-to-all over NVLink (one process per GPU), or device
+                  slices when several virtual ranks share one GPU;
+3. ``apply``   -- received entries are relaxed with the same generation, so
+                  local and remote improvements deduplicate together;
+4. ``advance`` -- worklists swap; the run ends when the all-reduced frontier
+                  is empty.
+
+Relaxation is confluent (engine.py:7-9), so any partition and exchange order
+reaches the reference's fixpoint: distances are bit-identical to a
+single-device run.  This module is orchestration only; the kernels, the
+split into buckets and the relaxation of received updates are CUDA
+(glb_shard_* in libgraphlb_b200.so).
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .graph import DeviceCsrGraph, generate_rmat
+from .runtime import KernelConfig
+from .strategies import RelaxOp, _ID_OF
+
+SHARD_TAGS = ("BS", "WD", "HP")
+
+
+@dataclass
+class ShardGraph:
+    """One rank's part of a partitioned graph (resident on `device`)."""
+
+    graph: DeviceCsrGraph
+    bounds: np.ndarray  # int64[parts + 1], edge-balanced vertex ranges
+    rank: int
+    device: int
+
+    @property
+    def parts(self) -> int:
+        return int(self.bounds.shape[0] - 1)
+
+    @property
+    def lo(self) -> int:
+        return int(self.bounds[self.rank])
+
+    @property
+    def hi(self) -> int:
+        return int(self.bounds[self.rank + 1])
+
+    @property
+    def num_nodes(self) -> int:
+        return self.graph.num_nodes
+
+
+def partition_bounds(g, parts: int) -> np.ndarray:
+    """Edge-balanced contiguous vertex ranges of a device graph."""
+    b = np.empty(parts + 1, dtype=np.int64)
+    _lib.check(_lib.lib().glb_graph_partition(g.device_graph(), parts, _lib.ptr64(b)),
+               "glb_graph_partition")
+    return b
+
+
+def shard_rmat(scale: int, edge_factor: int, parts: int, rank: int, device: int, *,
+               params=(0.45, 0.15, 0.15, 0.25), seed: int = 1, weighted: bool = True,
+               max_weight: int = 255) -> ShardGraph:
+    """Generate the R-MAT graph on `device` (bit-identical to generate_rmat),
+    cut the edge-balanced partition and keep this rank's rows."""
+    g = generate_rmat(scale, edge_factor, params=params, seed=seed, weighted=weighted,
+                      max_weight=max_weight, device=device, download=False)
+    bounds = partition_bounds(g, parts)
+    _lib.check(_lib.lib().glb_graph_restrict(g.device_graph(), int(bounds[rank]),
+                                             int(bounds[rank + 1])), "glb_graph_restrict")
+    m = ctypes.c_int64()
+    _lib.check(_lib.lib().glb_graph_info(g.device_graph(), None, ctypes.byref(m), None, None))
+    g.num_edges = int(m.value)
+    return ShardGraph(g, bounds, rank, device)
+
+
+def shard_graph(g, parts: int, rank: int, device: int) -> ShardGraph:
+    """This rank's part of a host CsrGraph (uploaded, then restricted)."""
+    h = ctypes.c_void_p()
+    _lib.check(_lib.lib().glb_graph_create(_lib.ptr64(g.row_offsets), _lib.ptr64(g.col_indices),
+                                           _lib.ptr64(g.weights), g.num_nodes, g.num_edges,
+                                           device, ctypes.byref(h)), "glb_graph_create")
+    dg = DeviceCsrGraph(h.value, g.num_nodes, g.num_edges, g.weights is not None, device)
+    bounds = partition_bounds(dg, parts)
+    _lib.check(_lib.lib().glb_graph_restrict(h.value, int(bounds[rank]), int(bounds[rank + 1])),
+               "glb_graph_restrict")
+    return ShardGraph(dg, bounds, rank, device)
+
+
+# ----------------------------------------------------------------- backends
+class CudaShard:
+    """glb_shard_* calls for one rank; buffers are torch tensors on its device."""
+
+    def __init__(self, sg: ShardGraph, tag: str, source: int, op: RelaxOp, cfg: KernelConfig,
+                 torch):
+        if tag.upper() not in SHARD_TAGS:
+            raise ValueError(f"sharded runs support {SHARD_TAGS}, not {tag!r}")
+        self.sg = sg
+        self.torch = torch
+        self.h = sg.graph.device_graph()
+        p = _lib.RunParams()
+        p.strategy = _ID_OF[tag.upper()]
+        p.algo = _lib.GLB_BFS if op.kind == "bfs" else _lib.GLB_SSSP
+        p.source = source
+        p.bins = 10
+        p.chunked = 1
+        p.max_cells = 1 << 62
+        p.block_size = cfg.block_size
+        p.hp_fallback = 1
+        p.record_timing = 1 if cfg.record_timing else 0
+        self.dev = torch.device("cuda", sg.device)
+        self.send = torch.empty(sg.num_nodes, dtype=torch.int64, device=self.dev)
+        _lib.check(_lib.lib().glb_shard_begin(self.h, ctypes.byref(p), _lib.ptr64(sg.bounds),
+                                              sg.parts, sg.rank), "glb_shard_begin")
+
+    def local(self):
+        counts = np.zeros(self.sg.parts, dtype=np.int64)
+        nxt = ctypes.c_int64()
+        _lib.check(_lib.lib().glb_shard_local(self.h, _lib.ptr64(counts),
+                                              ctypes.c_void_p(self.send.data_ptr()),
+                                              self.send.numel(), ctypes.byref(nxt)),
+                   "glb_shard_local")
+        return counts, self.send
+
+    def apply(self, recv, n: int):
+        if n:
+            _lib.check(_lib.lib().glb_shard_apply(self.h, ctypes.c_void_p(recv.data_ptr()), n),
+                       "glb_shard_apply")
+
+    def advance(self) -> int:
+        f = ctypes.c_int64()
+        _lib.check(_lib.lib().glb_shard_advance(self.h, ctypes.byref(f)), "glb_shard_advance")
+        return int(f.value)
+
+    def finish(self):
+        out = np.empty(self.sg.hi - self.sg.lo, dtype=np.int64)
+        st = _lib.RunStats()
+        _lib.check(_lib.lib().glb_shard_finish(self.h, _lib.ptr64(out), ctypes.byref(st)),
+                   "glb_shard_finish")
+        return out, {f: getattr(st, f) for f, _ in _lib.RunStats._fields_}
+
+
+# --------------------------------------------------------------- transports
+class DistTransport:
+    """All-to-all of the owner buckets + all-reduce of frontiers through
+    torch.distributed (NCCL over NVLink between GPUs; gloo works on CPU)."""
+
+    def __init__(self, torch, group=None):
+        import torch.distributed as dist
+
+        self.torch = torch
+        self.dist = dist
+        self.group = group
+
+    def exchange(self, counts: np.ndarray, send):
+        torch, dist = self.torch, self.dist
+        c_send = torch.as_tensor(counts, dtype=torch.int64).to(send.device)
+        c_recv = torch.empty_like(c_send)
+        dist.all_to_all_single(c_recv, c_send, group=self.group)
+        in_split = [int(x) for x in counts]
+        out_split = [int(x) for x in c_recv.cpu()]
+        total_out = sum(out_split)
+        recv = torch.empty(max(total_out, 1), dtype=torch.int64, device=send.device)
+        dist.all_to_all_single(recv[:total_out], send[:sum(in_split)], out_split, in_split,
+                               group=self.group)
+        return recv, total_out
+
+    def allreduce_sum(self, x: int, device) -> int:
+        t = self.torch.tensor([x], dtype=self.torch.int64, device=device)
+        self.dist.all_reduce(t, group=self.group)
+        return int(t.item())
+
+
+def bsp_loop(shard, transport, device, max_iterations: int | None = None) -> int:
+    """One rank of the bulk-synchronous loop; returns the iteration count."""
+    it = 0
+    while True:
+        counts, send = shard.local()
+        recv, n = transport.exchange(counts, send)
+        shard.apply(recv, n)
+        front = shard.advance()
+        it += 1
+        if transport.allreduce_sum(front, device) == 0:
+            return it
+        if max_iterations is not None and it >= max_iterations:
+            raise RuntimeError("sharded run did not converge")
+
+
+def run_sharded(tag: str, sg: ShardGraph, source: int, op: RelaxOp,
+                cfg: KernelConfig | None = None, transport=None):
+    """This rank's part of a sharded run (one process per GPU).  Returns the
+    int64 distances of the owned range [sg.lo, sg.hi) and device stats."""
+    import torch
+
+    cfg = cfg or KernelConfig()
+    transport = transport or DistTransport(torch)
+    shard = CudaShard(sg, tag, source, op, cfg, torch)
+    it = bsp_loop(shard, transport, shard.dev)
+    dist, info = shard.finish()
+    info["bsp_iterations"] = it
+    return dist, info
+
+
+def run_virtual(tag: str, shards: list[ShardGraph], source: int, op: RelaxOp,
+                cfg: KernelConfig | None = None):
+    """All ranks in one process (e.g. several virtual ranks on one GPU): the
+    exchange is device-side slicing.  Returns the full int64 distance array."""
+    import torch
+
+    cfg = cfg or KernelConfig()
+    ranks = [CudaShard(sg, tag, source, op, cfg, torch) for sg in shards]
+    parts = len(shards)
+    iters = 0
+    while True:
+        outs = [r.local() for r in ranks]
+        offs = []
+        for me, (counts, _) in enumerate(outs):
+            o, run = np.zeros(parts, dtype=np.int64), 0
+            for d in range(parts):
+                o[d] = run
+                if d != me:
+                    run += counts[d]
+            offs.append(o)
+        for d, r in enumerate(ranks):
+            pieces = [outs[s][1][offs[s][d]: offs[s][d] + outs[s][0][d]]
+                      for s in range(parts) if s != d and outs[s][0][d] > 0]
+            if pieces:
+                recv = torch.cat([p.to(r.dev) for p in pieces])
+                r.apply(recv, int(recv.numel()))
+        fronts = [r.advance() for r in ranks]
+        iters += 1
+        if sum(fronts) == 0:
+            break
+    dist = np.concatenate([r.finish()[0] for r in ranks])
+    return dist, iters

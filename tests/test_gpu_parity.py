@@ -274,3 +274,25 @@ def test_device_rmat_generator_matches_numpy(golden):
     r = pkg.run_wd(dg, 0, pkg.RelaxOp("sssp"), pkg.KernelConfig())
     h = pkg.generate_rmat(12, 8, seed=3)
     assert np.array_equal(r.dist.array, pkg.run_wd(h, 0, pkg.RelaxOp("sssp"), pkg.KernelConfig()).dist.array)
+
+
+def test_sharded_virtual_ranks_match_reference(golden):
+    from paper_1711_00231_b200 import sharded
+
+    for gid in ("rmat10_s1", "rmat10_skew", "grid24", "quirks", "rmat12_s4", "degrees"):
+        g = gs.build(pkg, gs.CORPUS[gid])
+        for parts in (2, 3, 4):
+            shards = [sharded.shard_graph(g, parts, r, 0) for r in range(parts)]
+            for algo in ("bfs", "sssp"):
+                exp = golden["corpus"][f"{gid}|0|{algo}"]
+                for tag in sharded.SHARD_TAGS:
+                    d, it = sharded.run_virtual(tag, shards, 0, pkg.RelaxOp(algo))
+                    assert np.array_equal(d, exp), (gid, parts, algo, tag)
+    # device-generated shards of an R-MAT vs the single-device run
+    shards = [sharded.shard_rmat(14, 8, 4, r, 0, seed=3) for r in range(4)]
+    h = pkg.generate_rmat(14, 8, seed=3, max_weight=255)
+    for algo in ("bfs", "sssp"):
+        exp = pkg.run_wd(h, 0, pkg.RelaxOp(algo), pkg.KernelConfig()).dist.array
+        for tag in sharded.SHARD_TAGS:
+            d, _ = sharded.run_virtual(tag, shards, 0, pkg.RelaxOp(algo))
+            assert np.array_equal(d, exp), (algo, tag)
