@@ -258,10 +258,18 @@ def ours(args):
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
     peak = peaks.get("hbm_gbs", 6650.0)
     achieved = k_bytes / (k_ms / 1e3) / 1e9 if k_ms > 0 else None
-    traffic = None
+    # ncu DRAM traffic of the same kernel (one --set full capture, committed
+    # under profiles/): traffic / algorithmic bytes measured on the captured
+    # launches, applied to this run's mean algorithmic bytes per launch
+    traffic = traffic_note = None
     prof = ROOT / "profiles" / "ncu_summary.json"
     if prof.exists():
-        traffic = json.loads(prof.read_text()).get(f"{args.strategy}_{args.algo}_dram_bytes_per_launch")
+        ps = json.loads(prof.read_text())
+        ratio = ps.get(f"{args.strategy}_{args.algo}_traffic_over_algorithmic")
+        if ratio and recs:
+            traffic = int(ratio * k_bytes / len(recs))
+            traffic_note = (f"ncu dram read+write / algorithmic bytes = {ratio} on the captured "
+                            f"launches ({ps.get('source', '')})")
     roofline = {
         "bound": "hbm",
         "achieved": round(achieved, 1) if achieved else None,
@@ -269,6 +277,7 @@ def ours(args):
         "unit": "GB/s",
         "frac": round(achieved / peak, 4) if achieved else None,
         "traffic": traffic,
+        "traffic_source": traffic_note,
         "kernel": {"WD": "k_wd_relax", "HP": "k_hp_window", "BS": "k_bs_relax",
                    "NS": "k_ns_relax", "EP": "k_ep_relax"}[args.strategy],
         "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if peaks else "fallback",
