@@ -50,7 +50,7 @@ def parse():
     ap.add_argument("--algo", default="sssp", choices=("bfs", "sssp"))
     ap.add_argument("--scale", type=int, default=22)
     ap.add_argument("--edge-factor", type=int, default=16)
-    ap.add_argument("--loop", default=os.environ.get("GLB_BENCH_LOOP", "host"),
+    ap.add_argument("--loop", default=os.environ.get("GLB_BENCH_LOOP", "graph"),
                     choices=("host", "graph"))
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-extras", action="store_true", help="skip the per-strategy table")

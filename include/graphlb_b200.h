@@ -127,6 +127,10 @@ const char* glb_version(void);
 int glb_device_count(int* count);
 /* number of CUDA kernels this library has launched in the process */
 uint64_t glb_kernel_launches(void);
+/* Return the device memory cached by the library's allocator (graph arrays and
+ * workspaces of destroyed graphs are kept for reuse) to the driver.
+ * device < 0: every device.  *bytes_released may be NULL. */
+int glb_release_cached_memory(int device, int64_t* bytes_released);
 
 /* ---- graph (csr.py:42-118) ---- */
 /* Copies the host CSR (int64 row_offsets[n+1], col[m], weights[m] or NULL) into

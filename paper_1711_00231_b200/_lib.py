@@ -69,6 +69,7 @@ SIGNATURES = {
     "glb_version": (ctypes.c_char_p, []),
     "glb_device_count": (ctypes.c_int, [ctypes.POINTER(ctypes.c_int)]),
     "glb_kernel_launches": (ctypes.c_uint64, []),
+    "glb_release_cached_memory": (ctypes.c_int, [ctypes.c_int, _p64]),
     "glb_graph_create": (ctypes.c_int, [_p64, _p64, _p64, _i64, _i64, ctypes.c_int,
                                         ctypes.POINTER(ctypes.c_void_p)]),
     "glb_graph_destroy": (ctypes.c_int, [ctypes.c_void_p]),

@@ -113,18 +113,29 @@ class Runner {
   // distances of ids [lo, hi) to the host, counters into records / stats
   void finish_run(int64_t* dist_out, glb_run_stats* st, long long lo, long long hi) {
     const long long cnt = std::max<long long>(hi - lo, 0);
-    long long* out = (long long*)ensure(g_->ws.out64, (size_t)std::max<long long>(cnt, 1) * 8);
-    if (cnt) {
-      k_dist_out<D><<<grid_for(cnt, kBlock, g_->num_sms * 8), kBlock, 0, s_>>>(cells_ + lo, cnt,
-                                                                                out);
+    // 32-bit distances travel as u32 and are widened by the host workers;
+    // 64-bit ones are widened to the int64 layout on the device
+    constexpr bool kNarrow = sizeof(D) == 4;
+    void* out = ensure(g_->ws.out64, (size_t)std::max<long long>(cnt, 1) * (kNarrow ? 4 : 8));
+    if (cnt && dist_out) {
+      if (kNarrow)
+        k_dist_u32<<<grid_for(cnt, kBlock, g_->num_sms * 8), kBlock, 0, s_>>>(cells_ + lo, cnt,
+                                                                              (uint32_t*)out);
+      else
+        k_dist_out<D><<<grid_for(cnt, kBlock, g_->num_sms * 8), kBlock, 0, s_>>>(
+            cells_ + lo, cnt, (long long*)out);
       GLB_CHECK_LAUNCH();
     }
     GLB_CUDA_TRY(cudaEventRecord(g_->ev[1], s_));
     GLB_CUDA_TRY(cudaMemcpyAsync(&h_->ctrl, ctrl_, sizeof(DevCtrl), cudaMemcpyDeviceToHost, s_));
-    if (cnt > 0 && dist_out)
-      GLB_CUDA_TRY(cudaMemcpyAsync(dist_out, out, (size_t)cnt * 8, cudaMemcpyDeviceToHost, s_));
     GLB_CUDA_TRY(cudaStreamSynchronize(s_));
     if (h_->ctrl.overflow) throw OverflowRestart{};
+    if (cnt > 0 && dist_out) {
+      if (kNarrow)
+        download_dist_u32(s_, (const uint32_t*)out, cnt, dist_out);
+      else
+        GLB_CUDA_TRY(cudaMemcpy(dist_out, out, (size_t)cnt * 8, cudaMemcpyDeviceToHost));
+    }
     g_->stamp_epoch = h_->ctrl.gen;
     g_->scan_epoch = h_->ctrl.scan_epoch;
     float dev_ms = 0;
@@ -151,9 +162,7 @@ class Runner {
   DevRecord* drecs_ = nullptr;
   HostMirror* h_ = nullptr;
   // WD workspace
-  long long* c_pre_ = nullptr;
-  long long* c_base_ = nullptr;
-  D* c_dn_ = nullptr;
+  WdItem* items_ = nullptr;
   unsigned* tile_first_ = nullptr;
   LookbackState<2> lb_{};
   // grids
@@ -209,9 +218,7 @@ class Runner {
         q_[i] = (i < 2 || p_.strategy == GLB_HP) ? (uint32_t*)ensure(ws.q[i], nb * 4) : q_[1];
     }
     if (p_.strategy == GLB_WD || p_.strategy == GLB_HP) {
-      c_pre_ = (long long*)ensure(ws.c_pre, nb * 8);
-      c_base_ = (long long*)ensure(ws.c_base, nb * 8);
-      c_dn_ = (D*)ensure(ws.c_node, nb * sizeof(D));
+      items_ = (WdItem*)ensure(ws.c_pre, nb * sizeof(WdItem));
       const long long max_tiles = (g_->m + kWdTile - 1) / kWdTile + 2;
       tile_first_ = (unsigned*)ensure(ws.tile_first, (size_t)max_tiles * 4);
       const long long stiles = ((long long)nb + kWdScanTile - 1) / kWdScanTile + 1;
@@ -327,12 +334,12 @@ class Runner {
     GLB_CHECK_LAUNCH();
   }
   void launch_wd_scan(unsigned grid) {
-    k_wd_scan<D><<<grid, kBlock, 0, s_>>>(row_, cells_, lb_, c_pre_, c_base_, c_dn_, tile_first_,
+    k_wd_scan<D><<<grid, kBlock, 0, s_>>>(row_, lb_, items_, tile_first_,
                                           ctrl_);
     GLB_CHECK_LAUNCH();
   }
   void launch_wd_relax(unsigned grid) {
-    k_wd_relax<D, W><<<grid, kBlock, 0, s_>>>(relaxer(), c_pre_, c_base_, c_dn_, tile_first_,
+    k_wd_relax<D, W><<<grid, kBlock, 0, s_>>>(relaxer(), items_, tile_first_,
                                                ctrl_);
     GLB_CHECK_LAUNCH();
   }
@@ -419,8 +426,7 @@ class Runner {
       << '|' << cap_scan_ << '|' << cap_wd_ << '|' << cap_hp_ << '|' << (const void*)row_ << '|'
       << (const void*)col_ << '|' << (const void*)wt_ << '|' << (const void*)cs_ << '|'
       << (const void*)src_ << '|' << (const void*)cells_ << '|' << (const void*)stamp_ << '|'
-      << (const void*)ctrl_ << '|' << (const void*)c_pre_ << '|' << (const void*)c_base_ << '|'
-      << (const void*)c_dn_ << '|' << (const void*)tile_first_ << '|'
+      << (const void*)ctrl_ << '|' << (const void*)items_ << '|' << (const void*)tile_first_ << '|'
       << (const void*)lb_.flags << '|' << (const void*)lb_.aggs << '|' << g_->n;
     return k.str();
   }

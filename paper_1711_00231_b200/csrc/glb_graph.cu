@@ -28,16 +28,24 @@ const char* last_error() { return g_last_error.c_str(); }
 void* ensure(DevBuf& b, size_t bytes) {
   if (bytes == 0) bytes = 16;
   if (b.bytes >= bytes) return b.p;
-  if (b.p) GLB_CUDA_TRY(cudaFree(b.p));
+  if (b.p) {  // queued work may still read the old block: drain before recycling it
+    GLB_CUDA_TRY(cudaDeviceSynchronize());
+    dfree(b.p);
+  }
   b.p = nullptr;
   b.bytes = 0;
-  GLB_CUDA_TRY(cudaMalloc(&b.p, bytes));
+  b.p = dmalloc(bytes);
   b.bytes = bytes;
+  // Workspaces start zeroed, as fresh driver allocations do in practice: the
+  // look-back flags and counters rely on it, and a recycled block holds
+  // another graph's epochs.
+  GLB_CUDA_TRY(cudaMemset(b.p, 0, bytes));
+  GLB_CUDA_TRY(cudaDeviceSynchronize());
   return b.p;
 }
 
 void free_buf(DevBuf& b) {
-  if (b.p) cudaFree(b.p);
+  if (b.p) dfree(b.p);
   b.p = nullptr;
   b.bytes = 0;
 }
@@ -94,120 +102,24 @@ __global__ void k_check_rows(const long long* __restrict__ row, long long n, lon
   if (err) atomicOr(bad, 1u);
 }
 
-namespace {
-// Process-wide pinned staging ring for pageable -> HBM uploads.
-struct Staging {
-  std::mutex mu;
-  static constexpr size_t kChunk = size_t(8) << 20;  // int64 elements per chunk (64 MB)
-  void* pinned[2] = {nullptr, nullptr};
-  bool ok = false;
-  bool init() {
-    if (ok) return true;
-    for (int i = 0; i < 2; ++i)
-      if (cudaHostAlloc(&pinned[i], kChunk * 8, cudaHostAllocDefault) != cudaSuccess) return false;
-    ok = true;
-    return true;
-  }
-};
-Staging& staging() {
-  static Staging s;
-  return s;
-}
-
-void parallel_copy(void* dst, const void* src, size_t bytes) {
-  unsigned hw = std::max(1u, std::thread::hardware_concurrency());
-  unsigned nt = (unsigned)std::min<size_t>(std::min(16u, hw), bytes / (size_t(4) << 20) + 1);
-  if (nt <= 1) {
-    std::memcpy(dst, src, bytes);
-    return;
-  }
-  std::vector<std::thread> th;
-  size_t per = (bytes + nt - 1) / nt;
-  per = (per + 63) & ~size_t(63);
-  for (unsigned t = 0; t < nt; ++t) {
-    size_t off = t * per;
-    if (off >= bytes) break;
-    size_t len = std::min(per, bytes - off);
-    th.emplace_back([=] { std::memcpy((char*)dst + off, (const char*)src + off, len); });
-  }
-  for (auto& t : th) t.join();
-}
-}  // namespace
-
-// Upload `count` int64 host values: either verbatim into an int64 device
-// array (narrow == false) or narrowed into uint32 with a range check.
-static void upload_int64(glb_graph* g, const int64_t* host, long long count, void* dst,
-                         bool narrow, unsigned long long limit, unsigned bad_code,
-                         unsigned int* d_bad) {
-  if (count <= 0) return;
-  Staging& st = staging();
-  std::lock_guard<std::mutex> lk(st.mu);
-  if (!st.init()) throw Error{GLB_ENOMEM, "cudaHostAlloc of the upload staging ring failed"};
-  DevBuf& stage = g->ws.misc;
-  long long* dstage[2];
-  if (narrow) {
-    ensure(stage, Staging::kChunk * 8 * 2);
-    dstage[0] = (long long*)stage.p;
-    dstage[1] = dstage[0] + Staging::kChunk;
-  }
-  cudaEvent_t done[2];
-  GLB_CUDA_TRY(cudaEventCreateWithFlags(&done[0], cudaEventDisableTiming));
-  GLB_CUDA_TRY(cudaEventCreateWithFlags(&done[1], cudaEventDisableTiming));
-  bool used[2] = {false, false};
-  long long chunks = (count + (long long)Staging::kChunk - 1) / (long long)Staging::kChunk;
-  for (long long c = 0; c < chunks; ++c) {
-    int b = (int)(c & 1);
-    long long off = c * (long long)Staging::kChunk;
-    long long len = std::min<long long>((long long)Staging::kChunk, count - off);
-    if (used[b]) GLB_CUDA_TRY(cudaEventSynchronize(done[b]));
-    parallel_copy(st.pinned[b], host + off, (size_t)len * 8);
-    if (narrow) {
-      GLB_CUDA_TRY(cudaMemcpyAsync(dstage[b], st.pinned[b], (size_t)len * 8,
-                                   cudaMemcpyHostToDevice, g->stream));
-      unsigned grid = grid_for((len + 1) / 2, kBlock, g->num_sms * 8);
-      k_narrow_u32<<<grid, kBlock, 0, g->stream>>>(dstage[b], (uint32_t*)dst + off, len, limit,
-                                                   d_bad, bad_code);
-      GLB_CHECK_LAUNCH();
-    } else {
-      GLB_CUDA_TRY(cudaMemcpyAsync((long long*)dst + off, st.pinned[b], (size_t)len * 8,
-                                   cudaMemcpyHostToDevice, g->stream));
-    }
-    GLB_CUDA_TRY(cudaEventRecord(done[b], g->stream));
-    used[b] = true;
-  }
-  GLB_CUDA_TRY(cudaStreamSynchronize(g->stream));
-  cudaEventDestroy(done[0]);
-  cudaEventDestroy(done[1]);
-}
-
 void rmat_device(glb_graph* g, int scale, long long edge_factor, double t_a, double t_ab,
                  double t_abc, const unsigned long long state[2], const unsigned long long inc[2],
                  bool weighted, long long max_weight);
 
 void graph_upload(glb_graph* g, const int64_t* row, const int64_t* col, const int64_t* w) {
-  GLB_CUDA_TRY(cudaMalloc(&g->row, (size_t)(g->n + 1) * 8));
-  GLB_CUDA_TRY(cudaMalloc(&g->col, (size_t)std::max<long long>(g->m, 1) * 4));
-  if (w) GLB_CUDA_TRY(cudaMalloc(&g->wt, (size_t)std::max<long long>(g->m, 1) * 4));
-  DevCtrl* ctrl = (DevCtrl*)ensure(g->ws.ctrl, sizeof(DevCtrl));
-  GLB_CUDA_TRY(cudaMemsetAsync(ctrl, 0, sizeof(DevCtrl), g->stream));
-  unsigned long long* d_max = (unsigned long long*)&ctrl->aux[0];
-  upload_int64(g, row, g->n + 1, g->row, false, 0, 0, &ctrl->bad_input);
-  upload_int64(g, col, g->m, g->col, true, (unsigned long long)g->n, 2u, &ctrl->bad_input);
-  if (w) upload_int64(g, w, g->m, g->wt, true, 0x100000000ull, 4u, &ctrl->bad_input);
-  {
-    unsigned grid = grid_for(g->n, kBlock, g->num_sms * 8);
-    k_check_rows<<<grid, kBlock, 0, g->stream>>>(g->row, g->n, g->m, &ctrl->bad_input, d_max);
-    GLB_CHECK_LAUNCH();
+  g->row = (long long*)dmalloc((size_t)(g->n + 1) * 8);
+  g->col = (uint32_t*)dmalloc((size_t)std::max<long long>(g->m, 1) * 4);
+  if (w) g->wt = (uint32_t*)dmalloc((size_t)std::max<long long>(g->m, 1) * 4);
+  long long mx = 0;
+  upload_rows(g, row, g->n, g->m, g->row, &mx);
+  upload_narrow(g, col, g->m, g->col, (unsigned long long)g->n, false, nullptr,
+                "col_indices contains a node id out of range");
+  if (w) {
+    void* scratch = ensure(g->ws.misc, kUploadScratchBytes);
+    upload_narrow(g, w, g->m, g->wt, 0x100000000ull, true, scratch,
+                  "edge weights must be nonnegative and below 2^32 on the device");
   }
-  DevCtrl h;
-  GLB_CUDA_TRY(cudaMemcpyAsync(&h, ctrl, sizeof(DevCtrl), cudaMemcpyDeviceToHost, g->stream));
-  GLB_CUDA_TRY(cudaStreamSynchronize(g->stream));
-  if (h.bad_input & 1u)
-    throw Error{GLB_EINVAL, "row_offsets must start at 0, end at num_edges and be nondecreasing"};
-  if (h.bad_input & 2u) throw Error{GLB_EINVAL, "col_indices contains a node id out of range"};
-  if (h.bad_input & 4u)
-    throw Error{GLB_EINVAL, "edge weights must be nonnegative and below 2^32 on the device"};
-  g->max_degree = (int64_t)h.aux[0];
+  g->max_degree = mx;
 }
 
 // ======================================================= degree analysis ===
@@ -673,6 +585,7 @@ int glb_graph_create(const int64_t* row_offsets, const int64_t* col, const int64
     if (n < 0 || m < 0) throw Error{GLB_EINVAL, "node and edge counts must be nonnegative"};
     if (!row_offsets || (m > 0 && !col)) throw Error{GLB_EINVAL, "row_offsets/col_indices is NULL"};
     if (n >= (int64_t)0xFFFFFFFFll) throw Error{GLB_EINVAL, "num_nodes must be below 2^32-1 on the device"};
+    if (m >= (int64_t)0xFFFFFFFFll) throw Error{GLB_EINVAL, "num_edges must be below 2^32-1 on the device"};
     require_device(device);
     DeviceGuard dg(device);
     glb_graph* g = new glb_graph();
@@ -699,7 +612,7 @@ int glb_graph_create(const int64_t* row_offsets, const int64_t* col, const int64
       }
       GLB_CUDA_TRY(cudaEventCreate(&g->ev[0]));
       GLB_CUDA_TRY(cudaEventCreate(&g->ev[1]));
-      GLB_CUDA_TRY(cudaHostAlloc(&g->host_ctrl, 1 << 16, cudaHostAllocDefault));
+      g->host_ctrl = glb::pinned_small_get();
       glb::graph_upload(g, row_offsets, col, weights_or_null);
     } catch (...) {
       glb_graph_destroy(g);
@@ -733,7 +646,7 @@ int glb_graph_create_rmat(int scale, int64_t edge_factor, double t_a, double t_a
       GLB_CUDA_TRY(cudaDeviceGetAttribute(&g->num_sms, cudaDevAttrMultiProcessorCount, device));
       GLB_CUDA_TRY(cudaEventCreate(&g->ev[0]));
       GLB_CUDA_TRY(cudaEventCreate(&g->ev[1]));
-      GLB_CUDA_TRY(cudaHostAlloc(&g->host_ctrl, 1 << 16, cudaHostAllocDefault));
+      g->host_ctrl = glb::pinned_small_get();
       const unsigned long long st[2] = {state_hi_lo[0], state_hi_lo[1]};
       const unsigned long long ic[2] = {inc_hi_lo[0], inc_hi_lo[1]};
       glb::rmat_device(g, scale, edge_factor, t_a, t_ab, t_abc, st, ic, weighted != 0, max_weight);
@@ -825,9 +738,9 @@ int glb_graph_restrict(glb_graph* g, int64_t v_lo, int64_t v_hi) {
     const long long m2 = e[1] - e[0];
     long long* row2 = nullptr;
     uint32_t *col2 = nullptr, *w2 = nullptr;
-    GLB_CUDA_TRY(cudaMalloc(&row2, (size_t)(g->n + 1) * 8));
-    GLB_CUDA_TRY(cudaMalloc(&col2, (size_t)std::max<long long>(m2, 1) * 4));
-    if (g->wt) GLB_CUDA_TRY(cudaMalloc(&w2, (size_t)std::max<long long>(m2, 1) * 4));
+    row2 = (long long*)dmalloc((size_t)(g->n + 1) * 8);
+    col2 = (uint32_t*)dmalloc((size_t)std::max<long long>(m2, 1) * 4);
+    if (g->wt) w2 = (uint32_t*)dmalloc((size_t)std::max<long long>(m2, 1) * 4);
     k_restrict_rows<<<grid_for(g->n + 1, kBlock, g->num_sms * 8), kBlock, 0, g->stream>>>(
         g->row, g->n, v_lo, v_hi, e[0], e[1], row2);
     GLB_CHECK_LAUNCH();
@@ -839,9 +752,9 @@ int glb_graph_restrict(glb_graph* g, int64_t v_lo, int64_t v_hi) {
                                      g->stream));
     }
     GLB_CUDA_TRY(cudaStreamSynchronize(g->stream));
-    cudaFree(g->row);
-    cudaFree(g->col);
-    cudaFree(g->wt);
+    dfree(g->row);
+    dfree(g->col);
+    dfree(g->wt);
     g->row = row2;
     g->col = col2;
     g->wt = w2;
@@ -866,9 +779,9 @@ int glb_graph_destroy(glb_graph* g) {
   cudaGetDevice(&prev);
   cudaSetDevice(g->device);
   if (g->stream) cudaStreamSynchronize(g->stream);
-  cudaFree(g->row);
-  cudaFree(g->col);
-  cudaFree(g->wt);
+  glb::dfree(g->row);
+  glb::dfree(g->col);
+  glb::dfree(g->wt);
   glb::Workspace& ws = g->ws;
   glb::DevBuf* bufs[] = {&ws.dist,   &ws.stamp,  &ws.q[0],     &ws.q[1],    &ws.q[2],
                          &ws.q[3],   &ws.c_pre,  &ws.c_base,   &ws.c_node,  &ws.tile_first,
@@ -884,7 +797,7 @@ int glb_graph_destroy(glb_graph* g) {
   for (auto e : g->ev_pool) cudaEventDestroy(e);
   if (g->ev[0]) cudaEventDestroy(g->ev[0]);
   if (g->ev[1]) cudaEventDestroy(g->ev[1]);
-  if (g->host_ctrl) cudaFreeHost(g->host_ctrl);
+  glb::pinned_small_put(g->host_ctrl);
   if (g->stream) cudaStreamDestroy(g->stream);
   if (prev >= 0) cudaSetDevice(prev);
   delete g;

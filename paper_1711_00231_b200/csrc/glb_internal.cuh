@@ -219,8 +219,24 @@ struct glb_graph {
 namespace glb {
 
 // -------------------------------------------------------- host helpers ---
+// Device memory goes through the process-wide cache of glb_memory.cu; dfree
+// requires that no queued work still uses the block.
+void* dmalloc(size_t bytes);
+void dfree(void* p);
+size_t release_cached(int device);  // device < 0: every device
 void* ensure(DevBuf& b, size_t bytes);  // grow-only device allocation
 void free_buf(DevBuf& b);
+constexpr size_t kPinnedSmallBytes = size_t(1) << 16;
+void* pinned_small_get();  // pooled pinned block of kPinnedSmallBytes
+void pinned_small_put(void* p);
+unsigned host_workers();
+// staged transfers (glb_memory.cu)
+void upload_rows(glb_graph* g, const int64_t* row, long long n, long long m, long long* d_row,
+                 long long* max_degree);
+void upload_narrow(glb_graph* g, const int64_t* src, long long count, uint32_t* d_dst,
+                   unsigned long long limit, bool allow_u8, void* d_scratch, const char* what);
+void download_dist_u32(cudaStream_t s, const uint32_t* d_src, long long count, int64_t* out);
+constexpr size_t kUploadScratchBytes = size_t(32) << 20;  // u8 weight chunks on the device
 int max_resident_blocks(const void* kernel, int block, size_t smem, int num_sms);
 
 inline unsigned int grid_for(long long items, int per_block, int cap) {

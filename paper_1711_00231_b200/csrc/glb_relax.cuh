@@ -90,6 +90,14 @@ __device__ __forceinline__ void bq_flush(BlockQ& q, uint32_t* qout, unsigned int
   __syncthreads();
 }
 
+// warp shuffle of a distance value (32- or 64-bit)
+__device__ __forceinline__ uint32_t shfl_dist(uint32_t d, int src) {
+  return __shfl_sync(0xffffffffu, d, src);
+}
+__device__ __forceinline__ unsigned long long shfl_dist(unsigned long long d, int src) {
+  return __shfl_sync(0xffffffffu, d, src);
+}
+
 // --------------------------------------------------------- relax helper ---
 template <typename D, bool W>
 struct Relaxer {
@@ -450,23 +458,28 @@ __global__ void __launch_bounds__(kBlock) k_ep_relax(const long long* __restrict
 }
 
 // ====================================================== WD (K4 + K5/K6) ===
-constexpr int kWdIPT = 8;                    // frontier items per thread in the scan
+constexpr int kWdIPT = 8;                     // frontier items per thread in the scan
 constexpr int kWdScanTile = kBlock * kWdIPT;  // 2048 items per scan tile
-constexpr int kWdEPT = 8;                    // edges per thread per relax tile
-constexpr int kWdTile = kBlock * kWdEPT;     // 2048 edges per relax tile
+constexpr int kWdEPL = 8;                     // edges per lane of a warp tile
+constexpr int kWdTile = 32 * kWdEPL;          // 256 edges per warp tile
+constexpr int kWdWarpQ = 256;                 // per-warp push buffer (smem entries)
+
+// One compacted frontier item of a WD invocation (16 B, one 128-bit load):
+// its first active edge `pre` in the invocation's edge space, `base` = CSR
+// index of that edge minus `pre` (mod 2^32: edge ids are < 2^32), and the node.
+struct __align__(16) WdItem {
+  uint32_t pre, base, node, pad;
+};
 
 // Remaining degree of every frontier item (minus the HP base offset
 // min(window, deg), hierarchical.py:69-72), scanned as {edges, non-empty}.
-// Non-empty items are compacted to j = exclusive count: c_pre[j] = first
-// active edge, c_base[j] = CSR index of that edge minus c_pre[j], c_dn[j] =
-// the node's distance when the invocation starts (a later decrease re-pushes
-// the node, so reading it here instead of per edge is confluent).
-// tile_first[b] = item holding active edge b*kWdTile.
+// Non-empty items are compacted to j = exclusive count (items[j]), and
+// tile_first[b] = the item holding active edge b*kWdTile -- the per-thread
+// start of find_offsets (workload.py:45-72) at warp-tile granularity.
 template <typename D>
 __global__ void __launch_bounds__(kBlock) k_wd_scan(
-    const long long* __restrict__ row, const unsigned long long* __restrict__ cells,
-    LookbackState<2> lb, long long* __restrict__ c_pre, long long* __restrict__ c_base,
-    D* __restrict__ c_dn, unsigned int* __restrict__ tile_first, DevCtrl* ctrl) {
+    const long long* __restrict__ row, LookbackState<2> lb, WdItem* __restrict__ items,
+    unsigned int* __restrict__ tile_first, DevCtrl* ctrl) {
   using TS = TileScan<2, kBlock>;
   __shared__ typename TS::Storage st;
   __shared__ long long s_tile;
@@ -523,9 +536,12 @@ __global__ void __launch_bounds__(kBlock) k_wd_scan(
     for (int k = 0; k < kWdIPT; ++k) {
       if (rem[k] > 0) {
         const long long j = ex.w[1], pre = ex.w[0];
-        c_pre[j] = pre;
-        c_base[j] = beg[k] - pre;
-        c_dn[j] = Cell<D>::dist(cells[v[k]]);  // dn of the node (workload.py:131,140)
+        WdItem it;
+        it.pre = (uint32_t)pre;
+        it.base = (uint32_t)beg[k] - (uint32_t)pre;
+        it.node = v[k];
+        it.pad = 0;
+        items[j] = it;
         for (long long b = (pre + kWdTile - 1) / kWdTile; b * kWdTile < pre + rem[k]; ++b)
           tile_first[b] = (unsigned)j;
         ex.w[0] += rem[k];
@@ -540,117 +556,145 @@ __global__ void __launch_bounds__(kBlock) k_wd_scan(
   timer_end(ctrl->t_scan);
 }
 
-struct MaxOp {
-  __device__ __forceinline__ int operator()(int a, int b) const { return a > b ? a : b; }
-};
+// Warp-private push buffer in shared memory, flushed to the global worklist
+// with one reservation per kWdWarpQ entries (no CTA barriers anywhere).
+__device__ __forceinline__ void wq_flush(uint32_t* buf, unsigned& cnt, uint32_t* qout,
+                                         unsigned int* nout) {
+  __syncwarp();
+  unsigned base = 0;
+  if (lane_id() == 0 && cnt) base = atomicAdd(nout, cnt);
+  base = __shfl_sync(0xffffffffu, base, 0);
+  for (unsigned i = lane_id(); i < cnt; i += 32) qout[base + i] = buf[i];
+  __syncwarp();
+  cnt = 0;
+}
+
+// Equal-work warp tiles: warp tile t owns active edges [t*256, t*256+256) and
+// lane l relaxes edges t*256 + k*32 + l (k < 8), so every lane gets the same
+// edge count (workload.py:104-108) and each group of 32 lanes
+// walks consecutive CSR edges.  The owner item of an edge is found by a
+// shuffle binary search over the (<= 32 per window) item starts the warp
+// holds in registers; the item's distance is read fresh from its cell at
+// that point (the reference re-reads dn at every node entry,
+// workload.py:131,140).  No CTA-wide barriers: warps advance independently,
+// each keeping 8 independent col/weight loads, then 8 dist loads, then the
+// atomics in flight.
+constexpr int kWdWarps = kBlock / 32;
 
 template <typename D, bool W>
-__global__ void __launch_bounds__(kBlock, GLB_RELAX_MINB) k_wd_relax(Relaxer<D, W> rx0,
-                                                     const long long* __restrict__ c_pre,
-                                                     const long long* __restrict__ c_base,
-                                                     const D* __restrict__ c_dn,
-                                                     const unsigned int* __restrict__ tile_first,
-                                                     DevCtrl* ctrl) {
-  using BScan = cub::BlockScan<int, kBlock, cub::BLOCK_SCAN_WARP_SCANS>;
-  static_assert(kQCap == kWdTile, "the CTA queue reuses the owner array");
-  __shared__ __align__(16) int s_own[kWdTile];  // owners, then the push queue
-  __shared__ long long s_base[kWdTile + 1];
-  __shared__ D s_dn[kWdTile + 1];
-  __shared__ typename BScan::TempStorage s_scan;
-  __shared__ BlockQ bq;
-  __shared__ long long s_tile;
+__global__ void __launch_bounds__(kBlock, GLB_RELAX_MINB) k_wd_relax(
+    Relaxer<D, W> rx0, const WdItem* __restrict__ items,
+    const unsigned int* __restrict__ tile_first, DevCtrl* ctrl) {
+  __shared__ uint32_t s_q[kWdWarps][kWdWarpQ];
   const long long total = ctrl->wd_total;
   const long long nitems = ctrl->wd_items;
   const long long ntiles = (total + kWdTile - 1) / kWdTile;
-  if (blockIdx.x >= ntiles) return;  // idle CTA
+  if ((long long)blockIdx.x * kWdWarps >= ntiles) return;  // idle CTA
   timer_begin(ctrl->t_relax);
-  bq_init(bq, reinterpret_cast<uint32_t*>(s_own));
   const Relaxer<D, W> rx = bind(rx0, ctrl);
+  const unsigned lane = lane_id();
+  const unsigned warp = threadIdx.x >> 5;
+  uint32_t* wq = s_q[warp];
+  unsigned qn = 0;
   ThreadCounters c;
-  while (true) {  // edge tiles in ticket order: the last wave self-balances
-    if (threadIdx.x == 0) s_tile = (long long)atomicAdd(&ctrl->relax_ticket, 1ull);
-    __syncthreads();
-    const long long b = s_tile;
-    if (b >= ntiles) break;
-    const long long e0 = b * kWdTile;
-    const long long e1 = e0 + kWdTile < total ? e0 + kWdTile : total;
-    const long long j0 = tile_first[b];
-    const long long j1 = b + 1 < ntiles ? (long long)tile_first[b + 1] : nitems - 1;
-    const int cnt = (int)(j1 - j0 + 1);
-    int4* own4 = reinterpret_cast<int4*>(s_own);
-    for (int k = threadIdx.x; k < kWdTile / 4; k += kBlock) own4[k] = make_int4(0, 0, 0, 0);
-    __syncthreads();
-    for (int k = threadIdx.x; k < cnt; k += kBlock) {
-      const long long j = j0 + k;
-      const long long pre = c_pre[j];
-      s_base[k] = c_base[j];
-      s_dn[k] = c_dn[j];
-      long long h = pre - e0;
-      if (h < 0) h = 0;
-      if (h < kWdTile) s_own[h] = k;
-    }
-    __syncthreads();
-    // carry each item head forward: inclusive max-scan over the tile
-    int loc[kWdEPT];
-    {
-      const int4* p = reinterpret_cast<const int4*>(s_own + threadIdx.x * kWdEPT);
-      const int4 a = p[0], bb = p[1];
-      loc[0] = a.x; loc[1] = a.y; loc[2] = a.z; loc[3] = a.w;
-      loc[4] = bb.x; loc[5] = bb.y; loc[6] = bb.z; loc[7] = bb.w;
-    }
-    int tmax = 0;
-#pragma unroll
-    for (int k = 0; k < kWdEPT; ++k) {
-      tmax = loc[k] > tmax ? loc[k] : tmax;
-      loc[k] = tmax;
-    }
-    int carry;
-    BScan(s_scan).ExclusiveScan(tmax, carry, 0, MaxOp());
-    __syncthreads();
-    {
-      int4* p = reinterpret_cast<int4*>(s_own + threadIdx.x * kWdEPT);
-#pragma unroll
-      for (int k = 0; k < kWdEPT; ++k) loc[k] = loc[k] > carry ? loc[k] : carry;
-      p[0] = make_int4(loc[0], loc[1], loc[2], loc[3]);
-      p[1] = make_int4(loc[4], loc[5], loc[6], loc[7]);
-    }
-    __syncthreads();
-    // this thread's edges: e0 + k*kBlock + tid (lanes on consecutive edges)
-    long long e[kWdEPT];
-    D dn[kWdEPT];
+  constexpr unsigned FULL = 0xffffffffu;
+  for (long long t = (long long)blockIdx.x * kWdWarps + warp; t < ntiles;
+       t += (long long)gridDim.x * kWdWarps) {
+    const uint32_t e0 = (uint32_t)(t * kWdTile);
+    const uint32_t ecount = (uint32_t)(total - (long long)e0 < kWdTile ? total - e0 : kWdTile);
+    const uint32_t j0 = tile_first[t];
+    const uint32_t j1 = t + 1 < ntiles ? tile_first[t + 1] : (uint32_t)(nitems - 1);
+    uint32_t e[kWdEPL];
+    D dn[kWdEPL];
     unsigned valid = 0;
+    for (uint32_t wb = j0; wb <= j1; wb += 32) {  // windows of 32 items
+      const uint32_t j = wb + lane;
+      uint32_t st = 0xFFFFFFFFu, base = 0;
+      D du = DistTraits<D>::kInf;
+      if (j <= j1) {
+        const WdItem it = items[j];
+        st = it.pre > e0 ? it.pre - e0 : 0u;
+        base = it.base;
+        du = rx.dist(it.node);
+      }
+      const uint32_t wlo = __shfl_sync(FULL, st, 0);
+      uint32_t whi = kWdTile;
+      if (wb + 32 <= j1) whi = items[wb + 32].pre - e0;
 #pragma unroll
-    for (int k = 0; k < kWdEPT; ++k) {
-      const int local = k * kBlock + threadIdx.x;
-      const long long ee = e0 + local;
-      if (ee < e1) {
-        const int o = s_own[local];
-        dn[k] = s_dn[o];
-        e[k] = s_base[o] + ee;
-        if (dn[k] != DistTraits<D>::kInf)
-          valid |= 1u << k;
-        else
-          ++c.work;
+      for (int k = 0; k < kWdEPL; ++k) {
+        const uint32_t f = (uint32_t)k * 32u + lane;
+        int o = 0;
+#pragma unroll
+        for (int step = 16; step > 0; step >>= 1) {
+          const uint32_t s = __shfl_sync(FULL, st, o + step);
+          if (s <= f) o += step;
+        }
+        const uint32_t ob = __shfl_sync(FULL, base, o);
+        const D od = shfl_dist(du, o);
+        if (f < ecount && f >= wlo && f < whi) {
+          e[k] = ob + e0 + f;
+          dn[k] = od;
+          if (od != DistTraits<D>::kInf)
+            valid |= 1u << k;
+          else
+            ++c.work;
+        }
       }
     }
-    __syncthreads();  // owners consumed: s_own becomes the push queue
-    // two half-batches keep the register footprint at 4 CTAs / SM
+    // gather col / weights, then dist[dst], then the atomics (atomic_relax_min)
+    uint32_t v[kWdEPL], w[kWdEPL];
 #pragma unroll
-    for (int half = 0; half < 2; ++half) {
-      constexpr int H = kWdEPT / 2;
-      long long eh[H];
-      D dh[H];
-#pragma unroll
-      for (int k = 0; k < H; ++k) {
-        eh[k] = e[half * H + k];
-        dh[k] = dn[half * H + k];
+    for (int k = 0; k < kWdEPL; ++k)
+      if (valid >> k & 1u) {
+        v[k] = __ldcs(rx.col + e[k]);
+        w[k] = W ? __ldcs(rx.wt + e[k]) : 1u;
       }
-      uint32_t v[H];
-      D cand[H];
-      relax_batch<H>(rx, bq, eh, dh, (valid >> (half * H)) & ((1u << H) - 1u), c, v, cand);
+    D cur[kWdEPL];
+#pragma unroll
+    for (int k = 0; k < kWdEPL; ++k)
+      if (valid >> k & 1u) cur[k] = rx.dist(v[k]);
+    unsigned want = 0;
+    D cand[kWdEPL];
+#pragma unroll
+    for (int k = 0; k < kWdEPL; ++k)
+      if (valid >> k & 1u) {
+        ++c.work;
+        ++c.relax;
+        if (make_cand<D>(dn[k], w[k], cand[k], rx.ovf) && cand[k] < cur[k]) want |= 1u << k;
+      }
+    unsigned first = 0;
+#pragma unroll
+    for (int k = 0; k < kWdEPL; ++k)
+      if (want >> k & 1u) {
+        const unsigned long long old = atomicMin(rx.cells + v[k], Cell<D>::make(cand[k], rx.gen));
+        if (cand[k] < Cell<D>::dist(old)) {
+          if (Cell<D>::kPacked) {
+            if (Cell<D>::gen(old) != rx.gen) first |= 1u << k;
+          } else if (claim(rx.stamp, v[k], rx.gen)) {
+            first |= 1u << k;
+          }
+        }
+      }
+    // warp-aggregated append of the improved destinations
+    const unsigned mine = __popc(first);
+    unsigned incl = mine;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const unsigned y = __shfl_up_sync(FULL, incl, off);
+      if (lane >= (unsigned)off) incl += y;
     }
-    bq_flush(bq, rx.qout, rx.nout);
+    const unsigned wtotal = __shfl_sync(FULL, incl, 31);
+    if (wtotal) {
+      if (qn + wtotal > (unsigned)kWdWarpQ) wq_flush(wq, qn, rx.qout, rx.nout);
+      unsigned pos = qn + incl - mine;
+#pragma unroll
+      for (int k = 0; k < kWdEPL; ++k)
+        if (first >> k & 1u) wq[pos++] = v[k];
+      qn += wtotal;
+      c.push += mine;
+    }
   }
+  wq_flush(wq, qn, rx.qout, rx.nout);
   flush_counters(ctrl->ls, c);
   timer_end(ctrl->t_relax);
 }
@@ -791,6 +835,14 @@ __global__ void k_seed(unsigned long long* cells, uint32_t* q, unsigned int* nq,
     }
     if (tid == 0) *nq = (unsigned)(1 + kid_hi - kid_lo);
   }
+}
+
+// packed u32 cells -> u32 distances (INF stays 0xFFFFFFFF; widened on the host)
+__global__ void k_dist_u32(const unsigned long long* __restrict__ cells, long long n,
+                           uint32_t* __restrict__ out) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    out[i] = Cell<uint32_t>::dist(cells[i]);
 }
 
 template <typename D>
