@@ -94,12 +94,35 @@ __device__ __forceinline__ void hp_decide_sub(DevCtrl* c) {
   }
 }
 
+__device__ __forceinline__ int ctl_step_kind(const DevCtrl* c) {
+  return c->use_small ? (int)kModeSmall : c->mode;
+}
+
 __device__ __forceinline__ void ctl_set_conditionals(DevCtrl* c, cudaGraphConditionalHandle h_loop,
                                                      cudaGraphConditionalHandle h_mode,
                                                      int graph_mode) {
   if (graph_mode) {
     cudaGraphSetConditional(h_loop, c->done ? 0u : 1u);
-    if (h_mode) cudaGraphSetConditional(h_mode, (unsigned)c->mode);
+    if (h_mode) cudaGraphSetConditional(h_mode, (unsigned)ctl_step_kind(c));
+  }
+}
+
+// Small-frontier steps that k_small_loop (glb_small.cuh) can run: BS / NS
+// node steps, WD steps, and HP's super-list WD-fallback.
+constexpr int kSmallItemsCtl = 8192;
+__device__ __forceinline__ bool small_eligible(const DevCtrl* c) {
+  if (!c->small_ok || c->done || c->shard_mode) return false;
+  if (c->qcount[c->in] > (unsigned)kSmallItemsCtl) return false;
+  switch (c->strategy) {
+    case GLB_BS:
+    case GLB_NS:
+      return c->mode == kModeRelax;
+    case GLB_WD:
+      return c->mode == kModeWD;
+    case GLB_HP:
+      return c->mode == kModeWD && c->sub < 0 && c->window == 0;
+    default:
+      return false;
   }
 }
 
@@ -144,6 +167,9 @@ __global__ void k_control_init(DevCtrl* c, cudaGraphConditionalHandle h_loop,
   }
   if (c->shard_mode) c->done = 0;  // every shard steps, even with an empty frontier
   if (c->done) c->mode = kModeDone;
+  c->small_exit = 0;
+  c->kernels = 1;
+  c->use_small = small_eligible(c);
   ctl_set_conditionals(c, h_loop, h_mode, graph_mode);
 }
 
@@ -165,6 +191,14 @@ __global__ void k_control(DevCtrl* c, cudaGraphConditionalHandle h_loop,
     mx = o > mx ? o : mx;
   }
   if (lane != 0) return;
+  // this control kernel + the step's kernels (WD: scan + relax)
+  c->kernels += c->small_exit || c->done ? 2 : (c->mode == kModeWD ? 3 : 2);
+  if (c->small_exit) {  // k_small_loop recorded and advanced its own iterations
+    c->small_exit = 0;
+    c->use_small = 0;
+    ctl_set_conditionals(c, h_loop, h_mode, graph_mode);
+    return;
+  }
   if (c->done) {  // nothing ran (already finished)
     ctl_set_conditionals(c, h_loop, h_mode, graph_mode);
     return;
@@ -216,6 +250,7 @@ __global__ void k_control(DevCtrl* c, cudaGraphConditionalHandle h_loop,
       break;
   }
   if (c->done && !c->paused) c->mode = kModeDone;
+  c->use_small = small_eligible(c);
   ctl_set_conditionals(c, h_loop, h_mode, graph_mode);
 }
 

@@ -23,6 +23,7 @@
 #include "glb_internal.cuh"
 #include "glb_relax.cuh"
 #include "glb_scan.cuh"
+#include "glb_small.cuh"
 
 namespace glb {
 
@@ -129,6 +130,7 @@ class Runner {
     GLB_CUDA_TRY(cudaEventRecord(g_->ev[1], s_));
     GLB_CUDA_TRY(cudaMemcpyAsync(&h_->ctrl, ctrl_, sizeof(DevCtrl), cudaMemcpyDeviceToHost, s_));
     GLB_CUDA_TRY(cudaStreamSynchronize(s_));
+    if (p_.loop_mode == GLB_LOOP_GRAPH) count_launches(h_->ctrl.kernels);
     if (h_->ctrl.overflow) throw OverflowRestart{};
     if (cnt > 0 && dist_out) {
       if (kNarrow)
@@ -230,6 +232,10 @@ class Runner {
       cap_wd_ = cap((const void*)k_wd_relax<D, W>);
     }
     if (p_.strategy == GLB_HP) cap_hp_ = std::max(cap((const void*)k_hp_window<D, W>), g_->num_sms);
+    if (p_.strategy != GLB_EP)
+      GLB_CUDA_TRY(cudaFuncSetAttribute((const void*)k_small_loop<D, W>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)small_smem_bytes<D>()));
     if (relax_kernel()) cap_relax_ = std::max(cap(relax_kernel()), g_->num_sms);
     pin_cells_in_l2(nb * 8);
     ctrl_ = (DevCtrl*)ensure(ws.ctrl, sizeof(DevCtrl));
@@ -252,6 +258,7 @@ class Runner {
     c.scan_epoch = g_->scan_epoch + 1;
     c.rec_cap = kMaxRecords;
     c.shard_mode = shard_mode_ ? 1 : 0;
+    c.small_ok = !shard_mode_ && p_.strategy != GLB_EP && !getenv("GLB_NO_SMALL") ? 1 : 0;
     c.recs = drecs_;
     c.ls = ls_;
     h_->ctrl = c;
@@ -347,6 +354,11 @@ class Runner {
     k_hp_window<D, W><<<grid, kBlock, 0, s_>>>(row_, relaxer(), ctrl_);
     GLB_CHECK_LAUNCH();
   }
+  void launch_small() {
+    k_small_loop<D, W><<<kSmallCtas, kSmallThreads, small_smem_bytes<D>(), s_>>>(
+        row_, p_.strategy == GLB_NS ? cs_ : nullptr, g_->n, relaxer(), ctrl_);
+    GLB_CHECK_LAUNCH();
+  }
   void launch_control(cudaGraphConditionalHandle hl, cudaGraphConditionalHandle hm, int gm) {
     k_control<<<1, 32, 0, s_>>>(ctrl_, hl, hm, gm);
     GLB_CHECK_LAUNCH();
@@ -379,7 +391,14 @@ class Runner {
         ev.k0 = event();
         ev.k1 = event();
       }
-      switch (c.mode) {
+      switch (c.use_small ? (int)kModeSmall : c.mode) {
+        case kModeSmall: {
+          ev.threads = kSmallAll;
+          if (timing) GLB_CUDA_TRY(cudaEventRecord(ev.k0, s_));
+          launch_small();
+          if (timing) GLB_CUDA_TRY(cudaEventRecord(ev.k1, s_));
+          break;
+        }
         case kModeRelax: {
           const long long per = p_.strategy == GLB_EP ? 4LL * kBlock : kBlock;
           const unsigned grid = grid_for(n_in, (int)per, cap_relax_);
@@ -413,9 +432,15 @@ class Runner {
         }
         default: throw Error{GLB_ECUDA, "control block in an unknown mode"};
       }
+      const bool small = c.use_small != 0;
       launch_control(0, 0, 0);
       read_ctrl();
-      if (h_->ctrl.nrec > nrec0) ev_of_rec_.push_back(ev);
+      if (small) {  // several iterations in one launch: per-record device timers
+        for (unsigned r = nrec0; r < h_->ctrl.nrec; ++r)
+          ev_of_rec_.push_back(EvPair{nullptr, nullptr, nullptr, nullptr, kSmallAll});
+      } else if (h_->ctrl.nrec > nrec0) {
+        ev_of_rec_.push_back(ev);
+      }
     }
   }
 
@@ -454,8 +479,7 @@ class Runner {
     try {
       cudaGraphConditionalHandle h_loop = 0, h_mode = 0;
       GLB_CUDA_TRY(cudaGraphConditionalHandleCreate(&h_loop, graph, 0, 0));
-      if (p_.strategy == GLB_HP)
-        GLB_CUDA_TRY(cudaGraphConditionalHandleCreate(&h_mode, graph, 0, 0));
+      GLB_CUDA_TRY(cudaGraphConditionalHandleCreate(&h_mode, graph, 0, 0));
       capture_into(graph, nullptr, 0);
       k_control_init<<<1, 32, 0, s_>>>(ctrl_, h_loop, h_mode, 1);
       GLB_CHECK_LAUNCH();
@@ -472,34 +496,38 @@ class Runner {
       GLB_CUDA_TRY(cudaGraphAddNode(&wnode, graph, &init, 1, &wp));
       cudaGraph_t body = wp.conditional.phGraph_out[0];
 
-      if (p_.strategy == GLB_HP) {
-        alignas(cudaGraphNodeParams) unsigned char sbuf[sizeof(cudaGraphNodeParams)] = {};
-        cudaGraphNodeParams& sp = *reinterpret_cast<cudaGraphNodeParams*>(sbuf);
-        sp.type = cudaGraphNodeTypeConditional;
-        sp.conditional.handle = h_mode;
-        sp.conditional.type = cudaGraphCondTypeSwitch;
-        sp.conditional.size = 4;  // StepMode: done, relax, WD, HP
-        cudaGraphNode_t snode;
-        GLB_CUDA_TRY(cudaGraphAddNode(&snode, body, nullptr, 0, &sp));
-        cudaGraph_t b_wd = sp.conditional.phGraph_out[kModeWD];
-        cudaGraph_t b_hp = sp.conditional.phGraph_out[kModeHP];
-        capture_into(b_wd, nullptr, 0);
+      // SWITCH on the step kind (StepMode): the strategy's grid kernels or
+      // the CTA-resident small-frontier loop
+      alignas(cudaGraphNodeParams) unsigned char sbuf[sizeof(cudaGraphNodeParams)] = {};
+      cudaGraphNodeParams& sp = *reinterpret_cast<cudaGraphNodeParams*>(sbuf);
+      sp.type = cudaGraphNodeTypeConditional;
+      sp.conditional.handle = h_mode;
+      sp.conditional.type = cudaGraphCondTypeSwitch;
+      sp.conditional.size = kNumModes;
+      cudaGraphNode_t snode;
+      GLB_CUDA_TRY(cudaGraphAddNode(&snode, body, nullptr, 0, &sp));
+      if (p_.strategy == GLB_WD || p_.strategy == GLB_HP) {
+        capture_into(sp.conditional.phGraph_out[kModeWD], nullptr, 0);
         launch_wd_scan(cap_scan_);
         launch_wd_relax(cap_wd_);
         end_capture();
-        capture_into(b_hp, nullptr, 0);
+      }
+      if (p_.strategy == GLB_HP) {
+        capture_into(sp.conditional.phGraph_out[kModeHP], nullptr, 0);
         launch_hp(cap_hp_);
         end_capture();
-        capture_into(body, &snode, 1);
-      } else {
-        capture_into(body, nullptr, 0);
-        if (p_.strategy == GLB_WD) {
-          launch_wd_scan(cap_scan_);
-          launch_wd_relax(cap_wd_);
-        } else {
-          launch_relax(cap_relax_);
-        }
       }
+      if (relax_kernel()) {
+        capture_into(sp.conditional.phGraph_out[kModeRelax], nullptr, 0);
+        launch_relax(cap_relax_);
+        end_capture();
+      }
+      if (p_.strategy != GLB_EP) {
+        capture_into(sp.conditional.phGraph_out[kModeSmall], nullptr, 0);
+        launch_small();
+        end_capture();
+      }
+      capture_into(body, &snode, 1);
       launch_control(h_loop, h_mode, 1);
       end_capture();
       cudaGraphExec_t exec;

@@ -43,6 +43,7 @@ struct Error {
 // Every kernel launch site ends with GLB_CHECK_LAUNCH(): it surfaces launch
 // errors and counts the launch (glb_kernel_launches()).
 void count_launch();
+void count_launches(unsigned long long n);  // kernels executed inside a CUDA graph
 #define GLB_CHECK_LAUNCH()             \
   do {                                 \
     ::glb::count_launch();             \
@@ -105,7 +106,10 @@ struct LaunchStats {
 };
 
 // Step modes of the device-side strategy state machine (k_control).
-enum StepMode : int { kModeDone = 0, kModeRelax = 1, kModeWD = 2, kModeHP = 3 };
+// kModeSmall is the CTA-resident loop of glb_small.cuh running the strategy's
+// own step (the underlying mode stays in DevCtrl::mode, `use_small` selects it).
+enum StepMode : int { kModeDone = 0, kModeRelax = 1, kModeWD = 2, kModeHP = 3, kModeSmall = 4 };
+constexpr int kNumModes = 5;
 
 struct StepTimer {  // %globaltimer ns, min over CTA starts / max over CTA ends
   unsigned long long start;
@@ -144,6 +148,10 @@ struct DevCtrl {
   unsigned long long scan_ticket, relax_ticket;  // dynamic tile tickets of the WD step
   int shard_mode;   // sharded run: pause at every iteration boundary for the exchange
   int paused;
+  int small_ok;     // small-frontier iterations may run in k_small_loop
+  int use_small;    // the next step runs in k_small_loop
+  int small_exit;   // k_small_loop ran (and already recorded / advanced) this step
+  unsigned long long kernels;  // kernels the device loop has executed (graph mode launch count)
   // ---- HP super-iteration state (hierarchical.py:54-136)
   int sup_in, sup_out, cur, spare;
   long long s;

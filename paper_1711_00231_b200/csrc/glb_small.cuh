@@ -1,0 +1,341 @@
+// glb_small.cuh -- small-frontier iterations without a kernel launch each.
+//
+// High-diameter graphs (config C3: 8,191 BFS levels on the 4096^2 grid) and
+// the tails of low-diameter traversals run long sequences of iterations whose
+// worklists hold a few thousand nodes.  There, a step costs its launch and
+// memory-latency chain (scan -> relax -> control, ~30 us), not its work.
+// k_small_loop runs such iterations back to back inside ONE thread-block
+// cluster (8 CTAs x 1024 threads, one per SM): every CTA keeps an identical
+// copy of the control block in shared memory and applies the same
+// transitions; iterations are separated by cluster barriers; the
+// per-iteration counters meet in CTA 0 through distributed shared memory.
+// Each iteration is the strategy's own decomposition at cluster scale,
+//   * BS: thread per worklist node, all out-edges (node_based.py:43-67)
+//   * NS: BS over the split graph + child mirroring (splitting.py:141-162)
+//   * WD (and HP's super-list WD-fallback, hierarchical.py:55-61): frontier
+//     scan into shared memory, then equal edge counts per thread with a
+//     binary search for the owner (workload.py:75-159)
+// and the iteration bookkeeping is the same k_control logic (records, stamp
+// generation, worklist swap).  It returns to the grid-wide kernels as soon as
+// a worklist outgrows the cluster (kSmallItems nodes, kSmallEdges WD edges).
+//
+// Distances and worklists are re-read with ld.global.cg inside the loop: L1
+// is not coherent with the L2 atomics, and a node's distance must be fresh
+// when it is expanded again in a later iteration of the same launch.
+#pragma once
+
+#include <cooperative_groups.h>
+#include <cub/block/block_scan.cuh>
+
+#include "glb_control.cuh"
+#include "glb_internal.cuh"
+#include "glb_relax.cuh"
+
+namespace glb {
+
+namespace cg = cooperative_groups;
+
+constexpr int kSmallCtas = 8;                     // cluster size (portable maximum)
+constexpr int kSmallThreads = 1024;               // threads per CTA
+constexpr int kSmallAll = kSmallCtas * kSmallThreads;
+constexpr int kSmallItems = kSmallItemsCtl;       // worklist nodes one iteration may hold
+constexpr long long kSmallEdges = 65536;          // WD: active edges one iteration may hold
+
+// dynamic shared memory of k_small_loop (the WD item table, replicated per CTA)
+template <typename D>
+constexpr size_t small_smem_bytes() {
+  return (size_t)(kSmallItems + 1) * 4 + (size_t)kSmallItems * 4 + (size_t)kSmallItems * sizeof(D);
+}
+
+template <typename D>
+__device__ __forceinline__ D dist_cg(const unsigned long long* cells, uint32_t v) {
+  return Cell<D>::dist(__ldcg(cells + v));
+}
+
+// Warp-aggregated append to a global worklist cursor.
+__device__ __forceinline__ void g_append(uint32_t* q, unsigned int* cursor, uint32_t item) {
+  q_append(q, cursor, item);
+}
+
+// Relax one batch of K edges; improved destinations are appended to the
+// global out-list (its cursor lives in the global control block).
+template <int K, typename D, bool W>
+__device__ __forceinline__ unsigned small_relax(const Relaxer<D, W>& rx, unsigned* cursor,
+                                                uint32_t* qout, const uint32_t (&e)[K],
+                                                const D (&dn)[K], unsigned valid,
+                                                ThreadCounters& c, uint32_t (&v)[K],
+                                                D (&cand)[K]) {
+  uint32_t w[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k)
+    if (valid >> k & 1u) {
+      v[k] = __ldg(rx.col + e[k]);
+      w[k] = W ? __ldg(rx.wt + e[k]) : 1u;
+    }
+  D cur[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k)
+    if (valid >> k & 1u) cur[k] = dist_cg<D>(rx.cells, v[k]);
+  unsigned want = 0;
+#pragma unroll
+  for (int k = 0; k < K; ++k)
+    if (valid >> k & 1u) {
+      ++c.work;
+      ++c.relax;
+      if (make_cand<D>(dn[k], w[k], cand[k], rx.ovf) && cand[k] < cur[k]) want |= 1u << k;
+    }
+  unsigned won = 0, first = 0;
+#pragma unroll
+  for (int k = 0; k < K; ++k)
+    if (want >> k & 1u) {
+      const unsigned long long old = atomicMin(rx.cells + v[k], Cell<D>::make(cand[k], rx.gen));
+      if (cand[k] < Cell<D>::dist(old)) {
+        won |= 1u << k;
+        if (Cell<D>::kPacked ? Cell<D>::gen(old) != rx.gen
+                             : atomicExch(rx.stamp + v[k], rx.gen) != rx.gen)
+          first |= 1u << k;
+      }
+    }
+#pragma unroll
+  for (int k = 0; k < K; ++k)
+    if (first >> k & 1u) {
+      g_append(qout, cursor, v[k]);
+      ++c.push;
+    }
+  return won;
+}
+
+template <typename D, bool W>
+__global__ void __cluster_dims__(kSmallCtas, 1, 1) __launch_bounds__(kSmallThreads, 1)
+    k_small_loop(const long long* __restrict__ row, const long long* __restrict__ cs,
+                 long long n_orig, Relaxer<D, W> rx0, DevCtrl* gctrl) {
+  extern __shared__ __align__(16) unsigned char s_dyn[];
+  D* s_dn = reinterpret_cast<D*>(s_dyn);                                   // [kSmallItems]
+  uint32_t* s_pre = reinterpret_cast<uint32_t*>(s_dyn + kSmallItems * sizeof(D));  // [+1]
+  uint32_t* s_base = s_pre + kSmallItems + 1;                              // [kSmallItems]
+  using LScan = cub::BlockScan<long long, kSmallThreads, cub::BLOCK_SCAN_WARP_SCANS>;
+  using IScan = cub::BlockScan<int, kSmallThreads, cub::BLOCK_SCAN_WARP_SCANS>;
+  __shared__ union {
+    typename LScan::TempStorage l;
+    typename IScan::TempStorage i;
+  } s_scan;
+  __shared__ DevCtrl sc;                 // this CTA's copy of the control block
+  __shared__ unsigned long long s_acc[5];  // CTA 0: the cluster's iteration counters
+  __shared__ long long s_total;
+  __shared__ int s_go;
+  __shared__ unsigned long long s_t0;
+
+  cg::cluster_group cluster = cg::this_cluster();
+  const unsigned rank = cluster.block_rank();
+  const unsigned tid = threadIdx.x;
+  const unsigned gt = rank * kSmallThreads + tid;
+  unsigned long long* acc0 = cluster.map_shared_rank(s_acc, 0);
+
+  if (tid == 0) {
+    sc = *gctrl;
+    s_go = small_eligible(&sc);
+    s_t0 = gtime();
+  }
+  if (tid < 5) s_acc[tid] = 0;
+  cluster.sync();
+  while (s_go) {
+    const unsigned n = sc.qcount[sc.in];
+    const uint32_t* qin = sc.qptr[sc.in];
+    uint32_t* qout = sc.qptr[sc.out];
+    unsigned* cursor = &gctrl->qcount[sc.out];  // zero at iteration start (see below)
+    Relaxer<D, W> rx = rx0;
+    rx.gen = sc.gen;
+    ThreadCounters c;
+    bool ran = true;
+    if (sc.mode == kModeWD) {
+      // ---- scan of remaining degrees, replicated in every CTA (items
+      //      contiguous per thread), so each holds the whole item table
+      const long long window = sc.window;
+      const unsigned ipt = (n + kSmallThreads - 1) / kSmallThreads;
+      const unsigned i0 = tid * ipt;
+      long long rem_sum = 0;
+      int cnt = 0;
+      for (unsigned k = 0; k < ipt; ++k) {
+        const unsigned i = i0 + k;
+        if (i < n) {
+          const uint32_t u = __ldcg(qin + i);
+          const long long lo = row[u], hi = row[u + 1];
+          const long long b = hi - lo < window ? hi - lo : window;
+          rem_sum += hi - lo - b;
+          cnt += hi - lo - b > 0;
+        }
+      }
+      long long ex_e, tot_e;
+      int ex_i, tot_i;
+      LScan(s_scan.l).ExclusiveSum(rem_sum, ex_e, tot_e);
+      __syncthreads();
+      IScan(s_scan.i).ExclusiveSum(cnt, ex_i, tot_i);
+      if (tid == 0) s_total = tot_e;
+      if (tot_e > kSmallEdges) {  // too big for the cluster: the grid kernels take this step
+        ran = false;
+      } else if (tot_e > 0) {
+        for (unsigned k = 0; k < ipt; ++k) {
+          const unsigned i = i0 + k;
+          if (i < n) {
+            const uint32_t u = __ldcg(qin + i);
+            const long long lo = row[u], hi = row[u + 1];
+            const long long b = hi - lo < window ? hi - lo : window;
+            const long long r = hi - lo - b;
+            if (r > 0) {
+              s_pre[ex_i] = (uint32_t)ex_e;
+              s_base[ex_i] = (uint32_t)(lo + b) - (uint32_t)ex_e;
+              s_dn[ex_i] = dist_cg<D>(rx.cells, u);  // dn at node entry (workload.py:131,140)
+              ++ex_i;
+              ex_e += r;
+            }
+          }
+        }
+        if (tid == 0) s_pre[tot_i] = (uint32_t)tot_e;
+        __syncthreads();
+        // ---- equal edges per thread across the cluster: f = gt + r * 8192
+        constexpr int K = 4;
+        const uint32_t total = (uint32_t)tot_e;
+        for (uint32_t f0 = gt; f0 < total; f0 += (uint32_t)K * kSmallAll) {
+          uint32_t e[K];
+          D d[K];
+          unsigned valid = 0;
+#pragma unroll
+          for (int k = 0; k < K; ++k) {
+            const uint32_t f = f0 + (uint32_t)k * kSmallAll;
+            if (f < total) {
+              int lo = 0, hi = tot_i;  // last item with s_pre <= f
+              while (hi - lo > 1) {
+                const int mid = (lo + hi) >> 1;
+                if (s_pre[mid] <= f)
+                  lo = mid;
+                else
+                  hi = mid;
+              }
+              e[k] = s_base[lo] + f;
+              d[k] = s_dn[lo];
+              if (d[k] != DistTraits<D>::kInf)
+                valid |= 1u << k;
+              else
+                ++c.work;
+            }
+          }
+          uint32_t v[K];
+          D cand[K];
+          small_relax<K>(rx, cursor, qout, e, d, valid, c, v, cand);
+        }
+      }
+    } else {
+      // ---- BS / NS: thread per worklist node (node i -> cluster thread i mod 8192)
+      for (unsigned i = gt; i < n; i += kSmallAll) {
+        const uint32_t u = __ldcg(qin + i);
+        const D du = dist_cg<D>(rx.cells, u);
+        if (du == DistTraits<D>::kInf) continue;
+        const uint32_t lo = (uint32_t)row[u], hi = (uint32_t)row[u + 1];
+        constexpr int K = 4;
+        for (uint32_t b = lo; b < hi; b += K) {
+          uint32_t e[K];
+          D d[K];
+          unsigned valid = 0;
+#pragma unroll
+          for (int k = 0; k < K; ++k) {
+            e[k] = b + k;
+            d[k] = du;
+            if (b + k < hi) valid |= 1u << k;
+          }
+          uint32_t v[K];
+          D cand[K];
+          const unsigned won = small_relax<K>(rx, cursor, qout, e, d, valid, c, v, cand);
+          if (cs) {  // NS: mirror improved parents onto their children (splitting.py:154-160)
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+              if (!(won >> k & 1u) || v[k] >= n_orig) continue;
+              const long long k1 = cs[v[k] + 1];
+              for (long long ch = cs[v[k]]; ch < k1; ++ch) {
+                const uint32_t child = (uint32_t)(n_orig + ch);
+                ++c.relax;
+                bool first = false;
+                if (relax_cell<D>(rx.cells, child, cand[k], rx.gen, &first) &&
+                    rx.claim_push(child, first)) {
+                  g_append(qout, cursor, child);
+                  ++c.push;
+                }
+              }
+            }
+          }
+        }
+      }
+    }
+    // ---- counters of the iteration meet in CTA 0 (distributed shared memory)
+    if (ran) {
+      unsigned long long w = c.work, r = c.relax, p = c.push, sq = c.work * c.work, mx = c.work;
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        w += __shfl_xor_sync(0xffffffffu, w, off);
+        r += __shfl_xor_sync(0xffffffffu, r, off);
+        p += __shfl_xor_sync(0xffffffffu, p, off);
+        sq += __shfl_xor_sync(0xffffffffu, sq, off);
+        const unsigned long long o = __shfl_xor_sync(0xffffffffu, mx, off);
+        mx = o > mx ? o : mx;
+      }
+      if (lane_id() == 0) {
+        if (w) atomicAdd(&acc0[0], w);
+        if (r) atomicAdd(&acc0[1], r);
+        if (p) atomicAdd(&acc0[2], p);
+        if (sq) atomicAdd(&acc0[3], sq);
+        if (mx) atomicMax(&acc0[4], mx);
+      }
+    }
+    cluster.sync();  // every push and counter of the iteration has landed
+    if (tid == 0) {
+      DevCtrl* cc = &sc;
+      if (!ran) {
+        s_go = 0;
+      } else {
+        const unsigned produced = __ldcg(cursor);
+        cc->qcount[cc->out] = produced;
+        const bool wd_empty = cc->mode == kModeWD && s_total == 0;
+        if (rank == 0 && !wd_empty && cc->nrec < cc->rec_cap) {
+          DevRecord& rec = cc->recs[cc->nrec];
+          rec.iteration = cc->iteration;
+          rec.sub = cc->sub;
+          rec.tag = cc->tag;
+          rec.active = n;
+          rec.threads = kSmallAll;
+          rec.work = (long long)s_acc[0];
+          rec.relax = (long long)s_acc[1];
+          rec.push = (long long)s_acc[2];
+          rec.work_max = (long long)s_acc[4];
+          rec.work_sumsq = (double)s_acc[3];
+          rec.k0 = s_t0;
+          rec.k1 = gtime();
+          rec.o0 = rec.o1 = 0;
+        }
+        if (!wd_empty) cc->nrec += 1;
+        if (cc->strategy == GLB_HP) {  // super-list fallback done (hierarchical.py:134-137)
+          hp_end_super(cc);
+        } else if (wd_empty) {
+          cc->done = 1;
+        } else {
+          ctl_simple_advance(cc);
+        }
+        if (cc->done) cc->mode = kModeDone;
+        s_go = small_eligible(cc);
+        if (rank == 0) {
+          if (s_go) __stcg(&gctrl->qcount[cc->out], 0u);  // the next iteration's out cursor
+          for (int k = 0; k < 5; ++k) s_acc[k] = 0;
+          s_t0 = gtime();
+        }
+      }
+    }
+    cluster.sync();  // transitions agree; the next out cursor is zero
+  }
+  if (rank == 0 && tid == 0) {
+    sc.overflow |= __ldcg(&gctrl->overflow);  // make_cand's flag lives in the global block
+    sc.small_exit = 1;
+    sc.use_small = 0;
+    ctl_reset_timers(&sc);
+    *gctrl = sc;
+  }
+}
+
+}  // namespace glb

@@ -1,0 +1,6 @@
+#!/bin/bash
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+timeout 900 python tools/suite.py --configs C3 --reps 1 --algos bfs > gpurun_out/suite_c3.log 2>&1
+timeout 600 python bench.py --no-extras > gpurun_out/bench.log 2>&1
+true
