@@ -270,6 +270,20 @@ def ours(args):
             traffic = int(ratio * k_bytes / len(recs))
             traffic_note = (f"ncu dram read+write / algorithmic bytes = {ratio} on the captured "
                             f"launches ({ps.get('source', '')})")
+    # measured ceiling of this path's real bottleneck on the same graph: one
+    # random 8 B cell gather per edge (dist[col[e]]) through L1TEX
+    gp = (ctypes.c_double * 4)()
+    _lib.check(_lib.lib().glb_measure_gather(runner.h, gp), "glb_measure_gather")
+    k_edges = sum(r.work_total for r in recs)
+    edge_rate = k_edges / (k_ms / 1e3) if k_ms > 0 else None
+    gather = {
+        "what": "dist[col[e]] gather rate on this graph's col array at full occupancy "
+                "(glb_measure_gather), vs the dominant kernel's examined-edge rate",
+        "gathers_per_s": round(gp[1] * 1e9, 0), "atomic_min_per_s": round(gp[2] * 1e9, 0),
+        "col_stream_GBs": round(gp[0], 1), "cells_MB": round(gp[3], 1),
+        "kernel_edges_per_s": round(edge_rate, 0) if edge_rate else None,
+        "frac": round(edge_rate / (gp[1] * 1e9), 4) if edge_rate and gp[1] > 0 else None,
+    }
     roofline = {
         "bound": "hbm",
         "achieved": round(achieved, 1) if achieved else None,
@@ -286,6 +300,7 @@ def ours(args):
         "kernel_share_of_step": round(k_ms / ms, 4) if ms else None,
         "relax_per_traversed_edge": round(stats[-1].relax_ops / max(e_r, 1), 3),
         "whole_step_frac": round(algorithmic_bytes(args.algo, e_r, n_r) / (ms_step / 1e3) / 1e9 / peak, 5),
+        "gather_ceiling": gather,
     }
 
     # ---- e2e through the C-ABI with host buffers

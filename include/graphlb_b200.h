@@ -190,6 +190,14 @@ int glb_shard_apply(glb_graph* g, const void* recv_buf, int64_t nrecv);
 int glb_shard_advance(glb_graph* g, int64_t* frontier);
 int glb_shard_finish(glb_graph* g, int64_t* dist_owned, glb_run_stats* stats);
 
+/* ---- measurement ---- */
+/* Ceilings of the relaxation's memory pattern measured on this graph's own
+ * col array (no reference counterpart; used by bench.py's roofline):
+ * out4[0] col stream GB/s, out4[1] gathers/s of dist[col[e]] (G/s, 8-byte
+ * cells, full occupancy), out4[2] atomicMin(dist[col[e]]) G/s, out4[3] MB of
+ * the gathered cell array. */
+int glb_measure_gather(glb_graph* g, double* out4);
+
 /* ---- degree analysis (degrees.py) ---- */
 int glb_degree_stats(glb_graph* g, int64_t* max_degree, int64_t* sum_degree,
                      double* sum_sq_degree);

@@ -94,6 +94,7 @@ SIGNATURES = {
                                ctypes.POINTER(RunStats), ctypes.POINTER(Record), _i64]),
     "glb_run_records": (ctypes.c_int, [ctypes.c_void_p, _i64, ctypes.POINTER(Record), _i64,
                                        _p64]),
+    "glb_measure_gather": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_double)]),
     "glb_degree_stats": (ctypes.c_int, [ctypes.c_void_p, _p64, _p64,
                                         ctypes.POINTER(ctypes.c_double)]),
     "glb_histogram": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, _p64, _p64,

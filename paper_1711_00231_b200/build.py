@@ -20,7 +20,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
          "-Xptxas", "-warn-spills", "-diag-suppress", "20054"]
-SOURCES = ["glb_memory.cu", "glb_graph.cu", "glb_driver.cu", "glb_gen.cu"]
+SOURCES = ["glb_memory.cu", "glb_graph.cu", "glb_driver.cu", "glb_gen.cu", "glb_peak.cu"]
 EXTRA = os.environ.get("GLB_EXTRA_FLAGS", "").split()
 
 

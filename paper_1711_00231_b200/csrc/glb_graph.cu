@@ -107,6 +107,8 @@ void rmat_device(glb_graph* g, int scale, long long edge_factor, double t_a, dou
                  double t_abc, const unsigned long long state[2], const unsigned long long inc[2],
                  bool weighted, long long max_weight);
 
+void measure_gather(glb_graph* g, double out[4]);
+
 void graph_upload(glb_graph* g, const int64_t* row, const int64_t* col, const int64_t* w) {
   g->row = (long long*)dmalloc((size_t)(g->n + 1) * 8);
   g->col = (uint32_t*)dmalloc((size_t)std::max<long long>(g->m, 1) * 4);
@@ -803,6 +805,15 @@ int glb_graph_destroy(glb_graph* g) {
   if (prev >= 0) cudaSetDevice(prev);
   delete g;
   return GLB_OK;
+}
+
+int glb_measure_gather(glb_graph* g, double* out4) {
+  return guarded([&] {
+    if (!g || !out4) throw Error{GLB_EINVAL, "NULL argument"};
+    std::lock_guard<std::mutex> lk(g->mu);
+    DeviceGuard dg(g->device);
+    glb::measure_gather(g, out4);
+  });
 }
 
 int glb_graph_info(const glb_graph* g, int64_t* n, int64_t* m, int* weighted, int* device) {

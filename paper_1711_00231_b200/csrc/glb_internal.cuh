@@ -257,6 +257,41 @@ inline unsigned int grid_for(long long items, int per_block, int cap) {
 // ------------------------------------------------------ device helpers ---
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
 
+// L2 eviction-priority hints (sm_80+ createpolicy): the distance cells are the
+// randomly re-read working set and should outlive the single-use col/weight
+// stream in the 126 MB L2.
+#ifndef GLB_L2_HINTS
+#define GLB_L2_HINTS 0  // measured slower on C2 (evict_last cells / evict_first streams)
+#endif
+__device__ __forceinline__ unsigned long long ld_cell(const unsigned long long* p) {
+#if GLB_L2_HINTS
+  unsigned long long r;
+  asm volatile(
+      "{\n\t.reg .b64 pol;\n\t"
+      "createpolicy.fractional.L2::evict_last.b64 pol, 1.0;\n\t"
+      "ld.global.L2::cache_hint.u64 %0, [%1], pol;\n\t}"
+      : "=l"(r)
+      : "l"(p));
+  return r;
+#else
+  return *p;
+#endif
+}
+__device__ __forceinline__ uint32_t ld_stream(const uint32_t* p) {
+#if GLB_L2_HINTS
+  uint32_t r;
+  asm volatile(
+      "{\n\t.reg .b64 pol;\n\t"
+      "createpolicy.fractional.L2::evict_first.b64 pol, 1.0;\n\t"
+      "ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], pol;\n\t}"
+      : "=r"(r)
+      : "l"(p));
+  return r;
+#else
+  return __ldcs(p);
+#endif
+}
+
 // Warp-aggregated append (one atomicAdd per converged group) -- the device
 // form of wl_push_node's cursor bump (worklist.py:107-130).
 __device__ __forceinline__ void q_append(uint32_t* q, unsigned int* cursor,

@@ -39,7 +39,10 @@
 #define GLB_PRECHECK 1  // plain-load filter before the relaxation atomic
 #endif
 #ifndef GLB_RELAX_MINB
-#define GLB_RELAX_MINB 3  // CTAs per SM the WD / HP relax kernels are register-capped for
+#define GLB_RELAX_MINB 3  // CTAs per SM the HP window kernel is register-capped for
+#endif
+#ifndef GLB_WD_MINB
+#define GLB_WD_MINB 2  // the pipelined WD relax: 2 CTAs/SM without spills beat 3 with (C2 A/B)
 #endif
 
 namespace glb {
@@ -110,7 +113,7 @@ struct Relaxer {
   unsigned int* nout;
   unsigned int* ovf;
 
-  __device__ __forceinline__ D dist(uint32_t u) const { return Cell<D>::dist(cells[u]); }
+  __device__ __forceinline__ D dist(uint32_t u) const { return Cell<D>::dist(ld_cell(cells + u)); }
   // push claim after a strict decrease (first = packed-cell verdict)
   __device__ __forceinline__ bool claim_push(uint32_t v, bool first) const {
     if (Cell<D>::kPacked) return first;
@@ -154,8 +157,8 @@ __device__ __forceinline__ unsigned relax_batch(const Relaxer<D, W>& rx, BlockQ&
 #pragma unroll
   for (int k = 0; k < K; ++k)
     if (valid >> k & 1u) {
-      v[k] = __ldcs(rx.col + e[k]);
-      w[k] = W ? __ldcs(rx.wt + e[k]) : 1u;
+      v[k] = ld_stream(rx.col + e[k]);
+      w[k] = W ? ld_stream(rx.wt + e[k]) : 1u;
     }
   unsigned want = 0;
 #if GLB_PRECHECK
@@ -384,8 +387,8 @@ __global__ void __launch_bounds__(kBlock) k_ep_relax(const long long* __restrict
     for (int k = 0; k < K; ++k)
       if (valid >> k & 1u) {
         u[k] = __ldcs(src + e[k]);
-        v[k] = __ldcs(rx.col + e[k]);
-        w[k] = W ? __ldcs(rx.wt + e[k]) : 1u;
+        v[k] = ld_stream(rx.col + e[k]);
+        w[k] = W ? ld_stream(rx.wt + e[k]) : 1u;
       }
 #pragma unroll
     for (int k = 0; k < K; ++k)
@@ -571,21 +574,38 @@ __device__ __forceinline__ void wq_flush(uint32_t* buf, unsigned& cnt, uint32_t*
 
 // Equal-work warp tiles: warp tile t owns active edges [t*256, t*256+256) and
 // lane l relaxes edges t*256 + k*32 + l (k < 8), so every lane gets the same
-// edge count (workload.py:104-108) and each group of 32 lanes
-// walks consecutive CSR edges.  The owner item of an edge is found by a
-// shuffle binary search over the (<= 32 per window) item starts the warp
-// holds in registers; the item's distance is read fresh from its cell at
-// that point (the reference re-reads dn at every node entry,
-// workload.py:131,140).  No CTA-wide barriers: warps advance independently,
-// each keeping 8 independent col/weight loads, then 8 dist loads, then the
-// atomics in flight.
+// edge count (workload.py:104-108) and every col / weight load
+// instruction covers 32 consecutive edges.  Owners come from a head-flag
+// array in the warp's shared memory: every item of the tile writes its index
+// at its first edge, and a thread-local + warp max-scan carries it forward.
+// The kernel is bound by random 32 B sector gathers through L1TEX (one per
+// cycle per SM, measured by tools/gather_peak.cu), so the layout spends
+// about one L1 wavefront per edge on the dist[dst] gather and ~1/8 on the
+// streams.  The item's distance is read fresh from its cell when the
+// tile starts (the reference re-reads dn at every node entry,
+// workload.py:131,140).  No CTA-wide barriers: warps advance independently.
+//
+// Software pipeline: while tile t's col/weight -> dist -> atomic chain is in
+// flight, the warp fetches tile t+stride's tile_first -> item -> item
+// distance chain, so each tile costs about three memory round trips.
 constexpr int kWdWarps = kBlock / 32;
 
+template <typename D>
+struct WdMeta {
+  uint32_t j0, j1;  // first / last item of the tile
+  uint32_t st;      // lane's item (of the first 32): first edge relative to the tile
+  uint32_t base;    // lane's item: CSR index - pre
+  D du;             // lane's item distance
+};
+
 template <typename D, bool W>
-__global__ void __launch_bounds__(kBlock, GLB_RELAX_MINB) k_wd_relax(
+__global__ void __launch_bounds__(kBlock, GLB_WD_MINB) k_wd_relax(
     Relaxer<D, W> rx0, const WdItem* __restrict__ items,
     const unsigned int* __restrict__ tile_first, DevCtrl* ctrl) {
   __shared__ uint32_t s_q[kWdWarps][kWdWarpQ];
+  __shared__ __align__(16) int s_own[kWdWarps][kWdTile];
+  __shared__ uint32_t s_base[kWdWarps][kWdTile + 1];
+  __shared__ D s_dn[kWdWarps][kWdTile + 1];
   const long long total = ctrl->wd_total;
   const long long nitems = ctrl->wd_items;
   const long long ntiles = (total + kWdTile - 1) / kWdTile;
@@ -595,87 +615,158 @@ __global__ void __launch_bounds__(kBlock, GLB_RELAX_MINB) k_wd_relax(
   const unsigned lane = lane_id();
   const unsigned warp = threadIdx.x >> 5;
   uint32_t* wq = s_q[warp];
+  int* own = s_own[warp];
+  uint32_t* sbase = s_base[warp];
+  D* sdn = s_dn[warp];
   unsigned qn = 0;
-  ThreadCounters c;
+  unsigned long long n_work = 0, n_relax = 0, n_push = 0;
   constexpr unsigned FULL = 0xffffffffu;
-  for (long long t = (long long)blockIdx.x * kWdWarps + warp; t < ntiles;
-       t += (long long)gridDim.x * kWdWarps) {
+  const long long stride = (long long)gridDim.x * kWdWarps;
+  const uint32_t last_item = (uint32_t)(nitems - 1);
+
+  auto load_items = [&](long long tt, WdMeta<D>& mm, uint32_t& node) {
+    const uint32_t te0 = (uint32_t)(tt * kWdTile);
+    mm.st = 0xFFFFFFFFu;
+    mm.base = 0;
+    node = 0;
+    if (mm.j0 + lane <= mm.j1) {
+      const WdItem it = items[mm.j0 + lane];
+      mm.st = it.pre > te0 ? it.pre - te0 : 0u;
+      mm.base = it.base;
+      node = it.node;
+    }
+  };
+
+  // ---- prologue: metadata of the warp's first tile
+  long long t = (long long)blockIdx.x * kWdWarps + warp;
+  WdMeta<D> m;
+  {
+    m.j0 = tile_first[t];
+    m.j1 = t + 1 < ntiles ? tile_first[t + 1] : last_item;
+    uint32_t node;
+    load_items(t, m, node);
+    m.du = m.st != 0xFFFFFFFFu ? rx.dist(node) : DistTraits<D>::kInf;
+  }
+
+  while (t < ntiles) {
+    const long long tn = t + stride;
+    const bool has_next = tn < ntiles;  // warp-uniform
     const uint32_t e0 = (uint32_t)(t * kWdTile);
     const uint32_t ecount = (uint32_t)(total - (long long)e0 < kWdTile ? total - e0 : kWdTile);
-    const uint32_t j0 = tile_first[t];
-    const uint32_t j1 = t + 1 < ntiles ? tile_first[t + 1] : (uint32_t)(nitems - 1);
-    uint32_t e[kWdEPL];
-    D dn[kWdEPL];
-    unsigned valid = 0;
-    for (uint32_t wb = j0; wb <= j1; wb += 32) {  // windows of 32 items
-      const uint32_t j = wb + lane;
-      uint32_t st = 0xFFFFFFFFu, base = 0;
-      D du = DistTraits<D>::kInf;
-      if (j <= j1) {
-        const WdItem it = items[j];
-        st = it.pre > e0 ? it.pre - e0 : 0u;
-        base = it.base;
-        du = rx.dist(it.node);
-      }
-      const uint32_t wlo = __shfl_sync(FULL, st, 0);
-      uint32_t whi = kWdTile;
-      if (wb + 32 <= j1) whi = items[wb + 32].pre - e0;
-#pragma unroll
-      for (int k = 0; k < kWdEPL; ++k) {
-        const uint32_t f = (uint32_t)k * 32u + lane;
-        int o = 0;
-#pragma unroll
-        for (int step = 16; step > 0; step >>= 1) {
-          const uint32_t s = __shfl_sync(FULL, st, o + step);
-          if (s <= f) o += step;
-        }
-        const uint32_t ob = __shfl_sync(FULL, base, o);
-        const D od = shfl_dist(du, o);
-        if (f < ecount && f >= wlo && f < whi) {
-          e[k] = ob + e0 + f;
-          dn[k] = od;
-          if (od != DistTraits<D>::kInf)
-            valid |= 1u << k;
-          else
-            ++c.work;
-        }
+    // ---- head flags: item i of the tile writes i at its first edge
+    {
+      int4* o4 = reinterpret_cast<int4*>(own + lane * kWdEPL);
+      o4[0] = make_int4(0, 0, 0, 0);
+      o4[1] = make_int4(0, 0, 0, 0);
+    }
+    __syncwarp();
+    // (the tile's last item may start exactly at the next tile: st == 256)
+    if (m.st < (uint32_t)kWdTile) {
+      own[m.st] = (int)lane;
+      sbase[lane] = m.base;
+      sdn[lane] = m.du;
+    }
+    for (uint32_t c0 = m.j0 + 32; c0 <= m.j1; c0 += 32) {  // rare: > 32 items in the tile
+      const uint32_t j = c0 + lane;
+      const WdItem it = items[j <= m.j1 ? j : m.j1];
+      if (j <= m.j1 && it.pre - e0 < (uint32_t)kWdTile) {
+        const uint32_t idx = j - m.j0;
+        own[it.pre - e0] = (int)idx;
+        sbase[idx] = it.base;
+        sdn[idx] = rx.dist(it.node);
       }
     }
-    // gather col / weights, then dist[dst], then the atomics (atomic_relax_min)
+    __syncwarp();
+    // ---- owners: local max over the lane's 8 consecutive head slots, warp
+    //      max-scan for the carry, scanned owners back to shared memory ...
+    {
+      int4* o4 = reinterpret_cast<int4*>(own + lane * kWdEPL);
+      const int4 a = o4[0], b = o4[1];
+      int o[kWdEPL] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+      for (int k = 1; k < kWdEPL; ++k) o[k] = o[k] > o[k - 1] ? o[k] : o[k - 1];
+      int carry = o[kWdEPL - 1];
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const int y = __shfl_up_sync(FULL, carry, off);
+        if (lane >= (unsigned)off) carry = y > carry ? y : carry;
+      }
+      int prev = __shfl_up_sync(FULL, carry, 1);
+      if (lane == 0) prev = 0;
+#pragma unroll
+      for (int k = 0; k < kWdEPL; ++k) o[k] = o[k] > prev ? o[k] : prev;
+      o4[0] = make_int4(o[0], o[1], o[2], o[3]);
+      o4[1] = make_int4(o[4], o[5], o[6], o[7]);
+    }
+    __syncwarp();
+    // ... and read back so that lane l takes edges k*32 + l: each load
+    //     instruction of the col / weight streams covers 32 consecutive edges
+    uint32_t e[kWdEPL];
+    D dn[kWdEPL];
+    unsigned valid = 0, inf_edges = 0;
+#pragma unroll
+    for (int k = 0; k < kWdEPL; ++k) {
+      const uint32_t f = (uint32_t)k * 32u + lane;
+      const int ok = own[f];
+      e[k] = sbase[ok] + e0 + f;
+      dn[k] = sdn[ok];
+      if (f < ecount) {
+        if (dn[k] != DistTraits<D>::kInf)
+          valid |= 1u << k;
+        else
+          ++inf_edges;
+      }
+    }
+    // ---- stage 1: this tile's col / weights  ||  next tile's tile_first
     uint32_t v[kWdEPL], w[kWdEPL];
 #pragma unroll
     for (int k = 0; k < kWdEPL; ++k)
       if (valid >> k & 1u) {
-        v[k] = __ldcs(rx.col + e[k]);
-        w[k] = W ? __ldcs(rx.wt + e[k]) : 1u;
+        v[k] = __ldg(rx.col + e[k]);
+        w[k] = W ? __ldg(rx.wt + e[k]) : 1u;
       }
+    WdMeta<D> nm;
+    nm.j0 = nm.j1 = 0;
+    if (has_next) {
+      nm.j0 = tile_first[tn];
+      nm.j1 = tn + 1 < ntiles ? tile_first[tn + 1] : last_item;
+    }
+    // ---- stage 2: this tile's dist[dst]  ||  next tile's items
     D cur[kWdEPL];
 #pragma unroll
     for (int k = 0; k < kWdEPL; ++k)
       if (valid >> k & 1u) cur[k] = rx.dist(v[k]);
+    uint32_t nnode = 0;
+    nm.st = 0xFFFFFFFFu;
+    if (has_next) load_items(tn, nm, nnode);
+    // ---- stage 3: this tile's atomics  ||  next tile's item distances
     unsigned want = 0;
     D cand[kWdEPL];
 #pragma unroll
     for (int k = 0; k < kWdEPL; ++k)
       if (valid >> k & 1u) {
-        ++c.work;
-        ++c.relax;
         if (make_cand<D>(dn[k], w[k], cand[k], rx.ovf) && cand[k] < cur[k]) want |= 1u << k;
       }
+    unsigned long long old[kWdEPL];
+#pragma unroll
+    for (int k = 0; k < kWdEPL; ++k)
+      if (want >> k & 1u) old[k] = atomicMin(rx.cells + v[k], Cell<D>::make(cand[k], rx.gen));
+    nm.du = DistTraits<D>::kInf;
+    if (nm.st != 0xFFFFFFFFu) nm.du = rx.dist(nnode);
     unsigned first = 0;
 #pragma unroll
     for (int k = 0; k < kWdEPL; ++k)
-      if (want >> k & 1u) {
-        const unsigned long long old = atomicMin(rx.cells + v[k], Cell<D>::make(cand[k], rx.gen));
-        if (cand[k] < Cell<D>::dist(old)) {
-          if (Cell<D>::kPacked) {
-            if (Cell<D>::gen(old) != rx.gen) first |= 1u << k;
-          } else if (claim(rx.stamp, v[k], rx.gen)) {
-            first |= 1u << k;
-          }
+      if ((want >> k & 1u) && cand[k] < Cell<D>::dist(old[k])) {
+        if (Cell<D>::kPacked) {
+          if (Cell<D>::gen(old[k]) != rx.gen) first |= 1u << k;
+        } else if (claim(rx.stamp, v[k], rx.gen)) {
+          first |= 1u << k;
         }
       }
-    // warp-aggregated append of the improved destinations
+    const unsigned nv = __popc(valid);
+    n_work += nv + inf_edges;
+    n_relax += nv;
+    // ---- warp-aggregated append of the improved destinations
     const unsigned mine = __popc(first);
     unsigned incl = mine;
 #pragma unroll
@@ -691,10 +782,17 @@ __global__ void __launch_bounds__(kBlock, GLB_RELAX_MINB) k_wd_relax(
       for (int k = 0; k < kWdEPL; ++k)
         if (first >> k & 1u) wq[pos++] = v[k];
       qn += wtotal;
-      c.push += mine;
+      n_push += mine;
     }
+    __syncwarp();  // the head-flag array is rewritten by the next tile
+    m = nm;
+    t = tn;
   }
   wq_flush(wq, qn, rx.qout, rx.nout);
+  ThreadCounters c;
+  c.work = n_work;
+  c.relax = n_relax;
+  c.push = n_push;
   flush_counters(ctrl->ls, c);
   timer_end(ctrl->t_relax);
 }

@@ -2,7 +2,7 @@
 # build a variant of libgraphlb_b200.so with extra nvcc flags into _exp/<name>.so
 name=$1; shift
 out=_exp/$name; mkdir -p $out
-for f in glb_memory glb_graph glb_driver glb_gen; do
+for f in glb_memory glb_graph glb_driver glb_gen glb_peak; do
   /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -lineinfo -Xcompiler -fPIC --expt-relaxed-constexpr -diag-suppress 20054 "$@" -c paper_1711_00231_b200/csrc/$f.cu -o $out/$f.o &
 done
 wait
