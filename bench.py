@@ -55,6 +55,7 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-extras", action="store_true", help="skip the per-strategy table")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-check", action="store_true", help="N>1: skip the single-GPU self-check")
     return ap.parse_args()
 
 
@@ -371,6 +372,154 @@ def ours(args):
         dist.destroy_process_group()
 
 
+# ------------------------------------------------------- sharded (N > 1)
+def ours_sharded(args, world, rank, local):
+    """N ranks, one GPU each: RMAT scale args.scale + log2(N) (weak scaling:
+    the same 2^(scale+4) edges per GPU as the 1-GPU C2 step), 1-D edge-balanced
+    vertex partition, one NCCL all-to-all exchange of (dist << 32 | v)
+    updates per BSP iteration plus an all-reduce of frontier sizes
+    (paper_1711_00231_b200.sharded).  Each step is one full traversal from
+    vertex 0; time = max over ranks of CUDA-event time, value = E_r of the
+    whole graph / that time."""
+    import math
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_1711_00231_b200 as pkg
+    from paper_1711_00231_b200 import _lib, sharded
+
+    backend = os.environ.get("GLB_BENCH_BACKEND", "nccl")
+    ndev = torch.cuda.device_count()
+    dev = local % max(ndev, 1)
+    torch.cuda.set_device(dev)
+    if backend == "nccl":
+        dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+    else:
+        dist.init_process_group(backend)
+    scale = args.scale + int(round(math.log2(world)))
+    tag = args.strategy if args.strategy in sharded.SHARD_TAGS else "WD"
+    t0 = time.time()
+    g = pkg.generate_rmat(scale, args.edge_factor, seed=1, max_weight=255, device=dev,
+                          download=False)
+    bounds = sharded.partition_bounds(g, world)
+    lo, hi = int(bounds[rank]), int(bounds[rank + 1])
+    row = np.empty(g.num_nodes + 1, dtype=np.int64)
+    _lib.check(_lib.lib().glb_graph_download(g.device_graph(), _lib.ptr64(row), None, None))
+    deg_own = np.diff(row[lo:hi + 1])
+    # self-check on rank 0: the single-GPU run on the full graph
+    ref = None
+    if rank == 0 and not args.no_check:
+        ref = pkg.run_strategy(tag, g, 0, pkg.RelaxOp(args.algo),
+                               pkg.KernelConfig(loop="graph")).dist.array
+    _lib.check(_lib.lib().glb_graph_restrict(g.device_graph(), lo, hi), "glb_graph_restrict")
+    sg = sharded.ShardGraph(g, bounds, rank, dev)
+    gen_s = time.time() - t0
+    transport = sharded.DistTransport(torch)
+    cfg = pkg.KernelConfig(record_timing=False)
+    op = pkg.RelaxOp(args.algo)
+
+    def step():
+        return sharded.run_sharded(tag, sg, 0, op, cfg, transport)
+
+    d_own, info = step()
+    reached = d_own != (1 << 63) - 1
+    t = torch.tensor([int(deg_own[reached].sum()), int(reached.sum())], dtype=torch.int64,
+                     device="cuda" if backend == "nccl" else "cpu")
+    dist.all_reduce(t)
+    e_r, n_r = int(t[0]), int(t[1])
+    parity = None
+    if not args.no_check:  # gather the owned ranges on rank 0 and compare
+        full = [None] * world if rank == 0 else None
+        dist.gather_object(d_own, full, dst=0)
+        if rank == 0:
+            parity = bool(np.array_equal(np.concatenate(full), ref))
+    for _ in range(args.warmup):
+        step()
+    launches0 = _lib.lib().glb_kernel_launches()
+    clocks = ClockSampler(dev)
+    clocks.start()
+    dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    iters = 0
+    for _ in range(args.steps):
+        _, inf = step()
+        iters = inf["bsp_iterations"]
+    e1.record()
+    torch.cuda.synchronize()
+    dist.barrier()
+    clk = clocks.stop()
+    launches = _lib.lib().glb_kernel_launches() - launches0
+    ms_step = e0.elapsed_time(e1) / args.steps
+    tt = torch.tensor([ms_step], dtype=torch.float64, device="cuda" if backend == "nccl" else "cpu")
+    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    ms_step = float(tt.item())
+    value = e_r / (ms_step / 1e3) / 1e9
+
+    # e2e: each rank uploads only its own rows from host int64 arrays, runs,
+    # and reads its owned int64 distances back (max over ranks)
+    e2e = None
+    if args.e2e_steps > 0:
+        # the device graph is already restricted: its download is the host shard
+        hrow = np.empty(g.num_nodes + 1, dtype=np.int64)
+        m_own = int(row[hi] - row[lo])
+        hcol = np.empty(m_own, dtype=np.int64)
+        hw = np.empty(m_own, dtype=np.int64)
+        _lib.check(_lib.lib().glb_graph_download(g.device_graph(), _lib.ptr64(hrow),
+                                                 _lib.ptr64(hcol), _lib.ptr64(hw)))
+        times = []
+        for i in range(args.e2e_steps + 1):
+            dist.barrier()
+            torch.cuda.synchronize()
+            t1 = time.perf_counter()
+            h = ctypes.c_void_p()
+            _lib.check(_lib.lib().glb_graph_create(_lib.ptr64(hrow), _lib.ptr64(hcol), _lib.ptr64(hw),
+                                                   g.num_nodes, m_own, dev, ctypes.byref(h)))
+            dg = pkg.DeviceCsrGraph(h.value, g.num_nodes, m_own, True, dev)
+            d2, _ = sharded.run_sharded(tag, sharded.ShardGraph(dg, bounds, rank, dev), 0, op, cfg,
+                                        transport)
+            dg.release_device()
+            torch.cuda.synchronize()
+            if i:
+                times.append(time.perf_counter() - t1)
+        assert np.array_equal(d2, d_own)
+        te = torch.tensor([statistics.median(times)], dtype=torch.float64,
+                          device="cuda" if backend == "nccl" else "cpu")
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        t_e2e = float(te.item())
+        e2e = {"value": round(e_r / t_e2e / 1e9, 4), "unit": UNIT,
+               "h2d_bytes_per_step": int(hrow.nbytes + hcol.nbytes + hw.nbytes),
+               "d2h_bytes_per_step": int(d_own.nbytes), "ms_per_step": round(t_e2e * 1e3, 2),
+               "path": "per rank: glb_graph_create(own rows, host int64) + sharded run + "
+                       "owned int64 dist to host (bytes are rank 0's)"}
+    cpu = None
+    if rank == 0 and not args.no_cpu:
+        cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count() or 1, "kind": "port",
+               "sample": "not run at N>1 (the CPU reference is timed on the 1-GPU workload)"}
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+            "data": "synthetic (RMAT generated on each GPU, bit-identical to graphlb.generate_rmat)",
+            "config": {
+                "workload": (f"{args.algo.upper()} on RMAT scale-{scale} edge-factor "
+                             f"{args.edge_factor} (0.45,0.15,0.15,0.25) seed 1, weights 1..255, "
+                             f"source 0, 1-D edge-balanced vertex partition over {world} GPUs, "
+                             f"{backend} all-to-all exchange per BSP iteration"),
+                "strategy": tag, "nodes": g.num_nodes, "edges": int(row[-1]),
+                "parallelism": f"shard{world}", "E_r": e_r, "N_r": n_r,
+                "bsp_iterations": iters, "gen_s": round(gen_s, 1),
+                "l2": "inputs larger than L2; no flush"},
+            "roofline": None, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
+            "gpu_launches": int(launches), "parity_vs_single_gpu": parity,
+        }
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
+
+
 def cpu_baseline(g, args, e_r):
     from oracle import oracle
 
@@ -445,5 +594,8 @@ if __name__ == "__main__":
     a = parse()
     if a.impl == "reference":
         reference(a)
+    elif int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        ours_sharded(a, int(os.environ["WORLD_SIZE"]), int(os.environ.get("RANK", "0")),
+                     int(os.environ.get("LOCAL_RANK", "0")))
     else:
         ours(a)

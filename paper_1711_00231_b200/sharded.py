@@ -101,6 +101,33 @@ def shard_graph(g, parts: int, rank: int, device: int) -> ShardGraph:
     return ShardGraph(dg, bounds, rank, device)
 
 
+def restrict_host(g, bounds: np.ndarray, rank: int):
+    """Host CSR arrays of rank `rank`'s shard over the global id space: the
+    owned rows keep their edges, every other row is empty (what
+    glb_graph_restrict leaves on the device)."""
+    lo, hi = int(bounds[rank]), int(bounds[rank + 1])
+    row = np.asarray(g.row_offsets)
+    e_lo, e_hi = int(row[lo]), int(row[hi])
+    r = np.clip(row, e_lo, e_hi) - e_lo
+    r[: lo + 1] = 0
+    r[hi:] = e_hi - e_lo
+    col = np.ascontiguousarray(g.col_indices[e_lo:e_hi])
+    w = None if g.weights is None else np.ascontiguousarray(g.weights[e_lo:e_hi])
+    return np.ascontiguousarray(r, dtype=np.int64), col, w
+
+
+def shard_host_graph(g, bounds: np.ndarray, rank: int, device: int) -> ShardGraph:
+    """Upload only this rank's rows of a host CsrGraph (the sharded form of
+    glb_graph_create): 1/P of the edges cross PCIe on every rank."""
+    row, col, w = restrict_host(g, bounds, rank)
+    h = ctypes.c_void_p()
+    _lib.check(_lib.lib().glb_graph_create(_lib.ptr64(row), _lib.ptr64(col), _lib.ptr64(w),
+                                           g.num_nodes, int(col.shape[0]), device, ctypes.byref(h)),
+               "glb_graph_create")
+    dg = DeviceCsrGraph(h.value, g.num_nodes, int(col.shape[0]), w is not None, device)
+    return ShardGraph(dg, np.asarray(bounds, dtype=np.int64), rank, device)
+
+
 # ----------------------------------------------------------------- backends
 class CudaShard:
     """glb_shard_* calls for one rank; buffers are torch tensors on its device."""
@@ -165,22 +192,26 @@ class DistTransport:
         self.torch = torch
         self.dist = dist
         self.group = group
+        # gloo moves host tensors only: stage device buffers through the host
+        self.host = dist.get_backend(group) == "gloo"
 
     def exchange(self, counts: np.ndarray, send):
         torch, dist = self.torch, self.dist
-        c_send = torch.as_tensor(counts, dtype=torch.int64).to(send.device)
+        dev = torch.device("cpu") if self.host else send.device
+        c_send = torch.as_tensor(counts, dtype=torch.int64).to(dev)
         c_recv = torch.empty_like(c_send)
         dist.all_to_all_single(c_recv, c_send, group=self.group)
         in_split = [int(x) for x in counts]
         out_split = [int(x) for x in c_recv.cpu()]
         total_out = sum(out_split)
-        recv = torch.empty(max(total_out, 1), dtype=torch.int64, device=send.device)
-        dist.all_to_all_single(recv[:total_out], send[:sum(in_split)], out_split, in_split,
-                               group=self.group)
-        return recv, total_out
+        recv = torch.empty(max(total_out, 1), dtype=torch.int64, device=dev)
+        dist.all_to_all_single(recv[:total_out], send[:sum(in_split)].to(dev), out_split,
+                               in_split, group=self.group)
+        return recv.to(send.device), total_out
 
     def allreduce_sum(self, x: int, device) -> int:
-        t = self.torch.tensor([x], dtype=self.torch.int64, device=device)
+        dev = "cpu" if self.host else device
+        t = self.torch.tensor([x], dtype=self.torch.int64, device=dev)
         self.dist.all_reduce(t, group=self.group)
         return int(t.item())
 
