@@ -35,6 +35,23 @@ __device__ __forceinline__ void ctl_simple_advance(DevCtrl* c) {
   c->done = produced == 0;
 }
 
+// WD with fused pushes: the next step's item list is the one just appended
+// (run_wd's loop, workload.py:175-189; it ends when the list has no edges,
+// workload.py:181-183).
+__device__ __forceinline__ void ctl_wd_fused_advance(DevCtrl* c, unsigned long long next,
+                                                     unsigned zeros) {
+  const unsigned items = (unsigned)(next >> 32);
+  c->qcount[c->out] = items + zeros;  // the worklist length the record reports
+  ctl_simple_advance(c);
+  c->wd_total = (long long)(next & 0xFFFFFFFFull);
+  c->wd_items = items;
+  c->wd_cur ^= 1;
+  c->wd_next = 0;
+  c->wd_zero_next = 0;
+  c->mode = kModeWDF;
+  if (c->wd_total == 0) c->done = 1;
+}
+
 __device__ __forceinline__ void hp_decide_sub(DevCtrl* c);
 
 __device__ __forceinline__ void hp_begin_super(DevCtrl* c) {
@@ -110,6 +127,7 @@ __device__ __forceinline__ void ctl_set_conditionals(DevCtrl* c, cudaGraphCondit
 // Small-frontier steps that k_small_loop (glb_small.cuh) can run: BS / NS
 // node steps, WD steps, and HP's super-list WD-fallback.
 constexpr int kSmallItemsCtl = 8192;
+constexpr long long kSmallEdgesCtl = 16384;  // WD: active edges one cluster iteration takes
 __device__ __forceinline__ bool small_eligible(const DevCtrl* c) {
   if (!c->small_ok || c->done || c->shard_mode) return false;
   if (c->qcount[c->in] > (unsigned)kSmallItemsCtl) return false;
@@ -118,7 +136,7 @@ __device__ __forceinline__ bool small_eligible(const DevCtrl* c) {
     case GLB_NS:
       return c->mode == kModeRelax;
     case GLB_WD:
-      return c->mode == kModeWD;
+      return c->mode == kModeWD || (c->mode == kModeWDF && c->wd_total <= kSmallEdgesCtl);
     case GLB_HP:
       return c->mode == kModeWD && c->sub < 0 && c->window == 0;
     default:
@@ -193,6 +211,8 @@ __global__ void k_control(DevCtrl* c, cudaGraphConditionalHandle h_loop,
   if (lane != 0) return;
   // this control kernel + the step's kernels (WD: scan + relax)
   c->kernels += c->small_exit || c->done ? 2 : (c->mode == kModeWD ? 3 : 2);
+  const unsigned long long wd_next = c->wd_next;
+  const unsigned wd_zero = c->wd_zero_next;
   if (c->small_exit) {  // k_small_loop recorded and advanced its own iterations
     c->small_exit = 0;
     c->use_small = 0;
@@ -203,7 +223,7 @@ __global__ void k_control(DevCtrl* c, cudaGraphConditionalHandle h_loop,
     ctl_set_conditionals(c, h_loop, h_mode, graph_mode);
     return;
   }
-  const bool wd_empty = c->mode == kModeWD && c->wd_total == 0;
+  const bool wd_empty = (c->mode == kModeWD || c->mode == kModeWDF) && c->wd_total == 0;
   if (!wd_empty && c->nrec < c->rec_cap) {  // decompose_invocation returns None: no record
     DevRecord& rec = c->recs[c->nrec];
     rec.iteration = c->iteration;
@@ -229,6 +249,8 @@ __global__ void k_control(DevCtrl* c, cudaGraphConditionalHandle h_loop,
       if (ctl_pause(c)) break;
       if (wd_empty) {  // active nodes have no out-edges (workload.py:181-183)
         c->done = 1;
+      } else if (c->wd_fused) {
+        ctl_wd_fused_advance(c, wd_next, wd_zero);
       } else {
         ctl_simple_advance(c);
       }

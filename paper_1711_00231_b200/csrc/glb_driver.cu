@@ -164,8 +164,8 @@ class Runner {
   DevRecord* drecs_ = nullptr;
   HostMirror* h_ = nullptr;
   // WD workspace
-  WdItem* items_ = nullptr;
-  unsigned* tile_first_ = nullptr;
+  WdItem* items_[2] = {nullptr, nullptr};
+  unsigned* tile_first_[2] = {nullptr, nullptr};
   LookbackState<2> lb_{};
   // grids
   int cap_relax_ = 0, cap_scan_ = 0, cap_wd_ = 0, cap_hp_ = 0;
@@ -220,9 +220,11 @@ class Runner {
         q_[i] = (i < 2 || p_.strategy == GLB_HP) ? (uint32_t*)ensure(ws.q[i], nb * 4) : q_[1];
     }
     if (p_.strategy == GLB_WD || p_.strategy == GLB_HP) {
-      items_ = (WdItem*)ensure(ws.c_pre, nb * sizeof(WdItem));
+      items_[0] = (WdItem*)ensure(ws.c_pre, nb * sizeof(WdItem));
+      items_[1] = (WdItem*)ensure(ws.c_base, nb * sizeof(WdItem));
       const long long max_tiles = (g_->m + kWdTile - 1) / kWdTile + 2;
-      tile_first_ = (unsigned*)ensure(ws.tile_first, (size_t)max_tiles * 4);
+      tile_first_[0] = (unsigned*)ensure(ws.tile_first, (size_t)max_tiles * 4);
+      tile_first_[1] = (unsigned*)ensure(ws.tile_node, (size_t)max_tiles * 4);
       const long long stiles = ((long long)nb + kWdScanTile - 1) / kWdScanTile + 1;
       unsigned* flags = (unsigned*)ensure_zero(ws.scan_flags, (size_t)stiles * 4 + 4096, s_);
       const size_t vb = (size_t)stiles * sizeof(Vec<2>);
@@ -259,6 +261,14 @@ class Runner {
     c.rec_cap = kMaxRecords;
     c.shard_mode = shard_mode_ ? 1 : 0;
     c.small_ok = !shard_mode_ && p_.strategy != GLB_EP && !getenv("GLB_NO_SMALL") ? 1 : 0;
+    for (int i = 0; i < 2; ++i) {
+      c.wd_items_buf[i] = items_[i];
+      c.wd_tf_buf[i] = tile_first_[i];
+    }
+    // Fused item pushes (no scan between WD steps) measured slower on C2 than
+    // scan + relax (the pushes' row loads sit on the relax kernel's critical
+    // path), so they are opt-in.
+    c.wd_fused = p_.strategy == GLB_WD && !shard_mode_ && getenv("GLB_WD_FUSED") ? 1 : 0;
     c.recs = drecs_;
     c.ls = ls_;
     h_->ctrl = c;
@@ -341,12 +351,12 @@ class Runner {
     GLB_CHECK_LAUNCH();
   }
   void launch_wd_scan(unsigned grid) {
-    k_wd_scan<D><<<grid, kBlock, 0, s_>>>(row_, lb_, items_, tile_first_,
+    k_wd_scan<D><<<grid, kBlock, 0, s_>>>(row_, lb_,
                                           ctrl_);
     GLB_CHECK_LAUNCH();
   }
   void launch_wd_relax(unsigned grid) {
-    k_wd_relax<D, W><<<grid, kBlock, 0, s_>>>(relaxer(), items_, tile_first_,
+    k_wd_relax<D, W><<<grid, kBlock, 0, s_>>>(relaxer(), row_,
                                                ctrl_);
     GLB_CHECK_LAUNCH();
   }
@@ -422,6 +432,13 @@ class Runner {
           ev.threads = (long long)cap_wd_ * kBlock;
           break;
         }
+        case kModeWDF: {  // fused WD: the item list is already built
+          if (timing) GLB_CUDA_TRY(cudaEventRecord(ev.k0, s_));
+          launch_wd_relax(cap_wd_);
+          if (timing) GLB_CUDA_TRY(cudaEventRecord(ev.k1, s_));
+          ev.threads = (long long)cap_wd_ * kBlock;
+          break;
+        }
         case kModeHP: {
           const unsigned grid = grid_for(n_in, kBlock, cap_hp_);
           ev.threads = (long long)grid * kBlock;
@@ -451,7 +468,8 @@ class Runner {
       << '|' << cap_scan_ << '|' << cap_wd_ << '|' << cap_hp_ << '|' << (const void*)row_ << '|'
       << (const void*)col_ << '|' << (const void*)wt_ << '|' << (const void*)cs_ << '|'
       << (const void*)src_ << '|' << (const void*)cells_ << '|' << (const void*)stamp_ << '|'
-      << (const void*)ctrl_ << '|' << (const void*)items_ << '|' << (const void*)tile_first_ << '|'
+      << (const void*)ctrl_ << '|' << (const void*)items_[0] << '|' << (const void*)items_[1] << '|'
+      << (const void*)tile_first_[0] << '|' << (const void*)tile_first_[1] << '|'
       << (const void*)lb_.flags << '|' << (const void*)lb_.aggs << '|' << g_->n;
     return k.str();
   }
@@ -509,6 +527,11 @@ class Runner {
       if (p_.strategy == GLB_WD || p_.strategy == GLB_HP) {
         capture_into(sp.conditional.phGraph_out[kModeWD], nullptr, 0);
         launch_wd_scan(cap_scan_);
+        launch_wd_relax(cap_wd_);
+        end_capture();
+      }
+      if (p_.strategy == GLB_WD) {
+        capture_into(sp.conditional.phGraph_out[kModeWDF], nullptr, 0);
         launch_wd_relax(cap_wd_);
         end_capture();
       }

@@ -108,8 +108,12 @@ struct LaunchStats {
 // Step modes of the device-side strategy state machine (k_control).
 // kModeSmall is the CTA-resident loop of glb_small.cuh running the strategy's
 // own step (the underlying mode stays in DevCtrl::mode, `use_small` selects it).
-enum StepMode : int { kModeDone = 0, kModeRelax = 1, kModeWD = 2, kModeHP = 3, kModeSmall = 4 };
-constexpr int kNumModes = 5;
+// kModeWDF is a WD step whose item list the previous step already appended
+// (fused pushes): relax only, no scan.
+enum StepMode : int {
+  kModeDone = 0, kModeRelax = 1, kModeWD = 2, kModeHP = 3, kModeSmall = 4, kModeWDF = 5
+};
+constexpr int kNumModes = 6;
 
 struct StepTimer {  // %globaltimer ns, min over CTA starts / max over CTA ends
   unsigned long long start;
@@ -152,6 +156,15 @@ struct DevCtrl {
   int use_small;    // the next step runs in k_small_loop
   int small_exit;   // k_small_loop ran (and already recorded / advanced) this step
   unsigned long long kernels;  // kernels the device loop has executed (graph mode launch count)
+  // ---- WD with fused pushes: relax kernels append WdItems (pre, base, node)
+  // for the next step directly, reserving (items, edges) with one 64-bit
+  // atomic per warp batch, so no scan runs between WD steps
+  void* wd_items_buf[2];        // WdItem lists (the step's input is [wd_cur])
+  unsigned int* wd_tf_buf[2];   // tile_first of each list
+  int wd_fused;                 // WD strategy outside sharded runs
+  int wd_cur;
+  unsigned long long wd_next;   // (items << 32) | edges appended to list [wd_cur ^ 1]
+  unsigned int wd_zero_next;    // zero-degree nodes pushed (counted for the record only)
   // ---- HP super-iteration state (hierarchical.py:54-136)
   int sup_in, sup_out, cur, spare;
   long long s;

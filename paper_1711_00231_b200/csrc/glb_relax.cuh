@@ -480,9 +480,10 @@ struct __align__(16) WdItem {
 // tile_first[b] = the item holding active edge b*kWdTile -- the per-thread
 // start of find_offsets (workload.py:45-72) at warp-tile granularity.
 template <typename D>
-__global__ void __launch_bounds__(kBlock) k_wd_scan(
-    const long long* __restrict__ row, LookbackState<2> lb, WdItem* __restrict__ items,
-    unsigned int* __restrict__ tile_first, DevCtrl* ctrl) {
+__global__ void __launch_bounds__(kBlock) k_wd_scan(const long long* __restrict__ row,
+                                                    LookbackState<2> lb, DevCtrl* ctrl) {
+  WdItem* __restrict__ items = reinterpret_cast<WdItem*>(ctrl->wd_items_buf[ctrl->wd_cur]);
+  unsigned int* __restrict__ tile_first = ctrl->wd_tf_buf[ctrl->wd_cur];
   using TS = TileScan<2, kBlock>;
   __shared__ typename TS::Storage st;
   __shared__ long long s_tile;
@@ -572,6 +573,73 @@ __device__ __forceinline__ void wq_flush(uint32_t* buf, unsigned& cnt, uint32_t*
   cnt = 0;
 }
 
+// Fused WD push (all 32 lanes): lane nodes with `has` become WdItems of the
+// next step's list, appended in lane order with ONE 64-bit atomic on the
+// (items << 32 | edges) counter -- the exclusive scan of workload.py:99-103
+// done at push time -- plus the tile_first entry of every 256-edge tile
+// boundary the item covers.  Zero-degree nodes are only counted.
+__device__ __forceinline__ void wd_push_items(bool has, uint32_t v,
+                                              const long long* __restrict__ row,
+                                              WdItem* __restrict__ out,
+                                              unsigned int* __restrict__ tf,
+                                              unsigned long long* next_ctr,
+                                              unsigned int* zero_ctr) {
+  constexpr unsigned FULL = 0xffffffffu;
+  const unsigned lane = lane_id();
+  long long lo = 0, hi = 0;
+  if (has) {
+    lo = row[v];
+    hi = row[v + 1];
+  }
+  const uint32_t deg = (uint32_t)(hi - lo);
+  const bool item = has && deg > 0;
+  unsigned ci = item ? 1u : 0u, ce = item ? deg : 0u;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const unsigned a = __shfl_up_sync(FULL, ci, off), b = __shfl_up_sync(FULL, ce, off);
+    if (lane >= (unsigned)off) {
+      ci += a;
+      ce += b;
+    }
+  }
+  const unsigned ti = __shfl_sync(FULL, ci, 31), te = __shfl_sync(FULL, ce, 31);
+  const unsigned zeros = __popc(__ballot_sync(FULL, has && deg == 0));
+  unsigned long long base = 0;
+  if (lane == 0) {
+    if (ti) base = atomicAdd(next_ctr, ((unsigned long long)ti << 32) | te);
+    if (zeros) atomicAdd(zero_ctr, zeros);
+  }
+  base = __shfl_sync(FULL, base, 0);
+  if (item) {
+    const unsigned slot = (unsigned)(base >> 32) + ci - 1u;
+    const uint32_t pre = (uint32_t)base + ce - deg;
+    WdItem it;
+    it.pre = pre;
+    it.base = (uint32_t)lo - pre;
+    it.node = v;
+    it.pad = 0;
+    out[slot] = it;
+    for (uint32_t b = (pre + kWdTile - 1) / kWdTile; (unsigned long long)b * kWdTile < (unsigned long long)pre + deg; ++b)
+      tf[b] = slot;
+  }
+}
+
+// Flush of a warp push buffer as fused WD items.
+__device__ __forceinline__ void wq_flush_items(uint32_t* buf, unsigned& cnt,
+                                               const long long* __restrict__ row, DevCtrl* ctrl) {
+  __syncwarp();
+  const int nb = ctrl->wd_cur ^ 1;
+  WdItem* out = reinterpret_cast<WdItem*>(ctrl->wd_items_buf[nb]);
+  unsigned int* tf = ctrl->wd_tf_buf[nb];
+  for (unsigned c0 = 0; c0 < cnt; c0 += 32) {
+    const unsigned i = c0 + lane_id();
+    wd_push_items(i < cnt, i < cnt ? buf[i] : 0u, row, out, tf, &ctrl->wd_next,
+                  &ctrl->wd_zero_next);
+  }
+  __syncwarp();
+  cnt = 0;
+}
+
 // Equal-work warp tiles: warp tile t owns active edges [t*256, t*256+256) and
 // lane l relaxes edges t*256 + k*32 + l (k < 8), so every lane gets the same
 // edge count (workload.py:104-108) and every col / weight load
@@ -590,18 +658,22 @@ __device__ __forceinline__ void wq_flush(uint32_t* buf, unsigned& cnt, uint32_t*
 // distance chain, so each tile costs about three memory round trips.
 constexpr int kWdWarps = kBlock / 32;
 
+constexpr int kWdPre = 2;  // items per lane prefetched for the next tile (64: degree >= 4)
+
 template <typename D>
 struct WdMeta {
-  uint32_t j0, j1;  // first / last item of the tile
-  uint32_t st;      // lane's item (of the first 32): first edge relative to the tile
-  uint32_t base;    // lane's item: CSR index - pre
-  D du;             // lane's item distance
+  uint32_t j0, j1;        // first / last item of the tile
+  uint32_t st[kWdPre];    // lane's items j0 + lane + 32 i: first edge relative to the tile
+  uint32_t base[kWdPre];  // CSR index - pre
+  D du[kWdPre];           // item distance
 };
 
 template <typename D, bool W>
 __global__ void __launch_bounds__(kBlock, GLB_WD_MINB) k_wd_relax(
-    Relaxer<D, W> rx0, const WdItem* __restrict__ items,
-    const unsigned int* __restrict__ tile_first, DevCtrl* ctrl) {
+    Relaxer<D, W> rx0, const long long* __restrict__ row, DevCtrl* ctrl) {
+  const WdItem* __restrict__ items = reinterpret_cast<const WdItem*>(ctrl->wd_items_buf[ctrl->wd_cur]);
+  const unsigned int* __restrict__ tile_first = ctrl->wd_tf_buf[ctrl->wd_cur];
+  const bool fused = ctrl->wd_fused != 0;
   __shared__ uint32_t s_q[kWdWarps][kWdWarpQ];
   __shared__ __align__(16) int s_own[kWdWarps][kWdTile];
   __shared__ uint32_t s_base[kWdWarps][kWdTile + 1];
@@ -624,17 +696,26 @@ __global__ void __launch_bounds__(kBlock, GLB_WD_MINB) k_wd_relax(
   const long long stride = (long long)gridDim.x * kWdWarps;
   const uint32_t last_item = (uint32_t)(nitems - 1);
 
-  auto load_items = [&](long long tt, WdMeta<D>& mm, uint32_t& node) {
+  auto load_items = [&](long long tt, WdMeta<D>& mm, uint32_t (&node)[kWdPre]) {
     const uint32_t te0 = (uint32_t)(tt * kWdTile);
-    mm.st = 0xFFFFFFFFu;
-    mm.base = 0;
-    node = 0;
-    if (mm.j0 + lane <= mm.j1) {
-      const WdItem it = items[mm.j0 + lane];
-      mm.st = it.pre > te0 ? it.pre - te0 : 0u;
-      mm.base = it.base;
-      node = it.node;
+#pragma unroll
+    for (int i = 0; i < kWdPre; ++i) {
+      mm.st[i] = 0xFFFFFFFFu;
+      mm.base[i] = 0;
+      node[i] = 0;
+      const uint32_t j = mm.j0 + lane + 32u * i;
+      if (j <= mm.j1) {
+        const WdItem it = items[j];
+        mm.st[i] = it.pre > te0 ? it.pre - te0 : 0u;
+        mm.base[i] = it.base;
+        node[i] = it.node;
+      }
     }
+  };
+  auto load_dist = [&](WdMeta<D>& mm, const uint32_t (&node)[kWdPre]) {
+#pragma unroll
+    for (int i = 0; i < kWdPre; ++i)
+      mm.du[i] = mm.st[i] != 0xFFFFFFFFu ? rx.dist(node[i]) : DistTraits<D>::kInf;
   };
 
   // ---- prologue: metadata of the warp's first tile
@@ -643,9 +724,9 @@ __global__ void __launch_bounds__(kBlock, GLB_WD_MINB) k_wd_relax(
   {
     m.j0 = tile_first[t];
     m.j1 = t + 1 < ntiles ? tile_first[t + 1] : last_item;
-    uint32_t node;
+    uint32_t node[kWdPre];
     load_items(t, m, node);
-    m.du = m.st != 0xFFFFFFFFu ? rx.dist(node) : DistTraits<D>::kInf;
+    load_dist(m, node);
   }
 
   while (t < ntiles) {
@@ -661,12 +742,15 @@ __global__ void __launch_bounds__(kBlock, GLB_WD_MINB) k_wd_relax(
     }
     __syncwarp();
     // (the tile's last item may start exactly at the next tile: st == 256)
-    if (m.st < (uint32_t)kWdTile) {
-      own[m.st] = (int)lane;
-      sbase[lane] = m.base;
-      sdn[lane] = m.du;
-    }
-    for (uint32_t c0 = m.j0 + 32; c0 <= m.j1; c0 += 32) {  // rare: > 32 items in the tile
+#pragma unroll
+    for (int i = 0; i < kWdPre; ++i)
+      if (m.st[i] < (uint32_t)kWdTile) {
+        const unsigned idx = lane + 32u * i;
+        own[m.st[i]] = (int)idx;
+        sbase[idx] = m.base[i];
+        sdn[idx] = m.du[i];
+      }
+    for (uint32_t c0 = m.j0 + 32 * kWdPre; c0 <= m.j1; c0 += 32) {  // rare: > 64 items
       const uint32_t j = c0 + lane;
       const WdItem it = items[j <= m.j1 ? j : m.j1];
       if (j <= m.j1 && it.pre - e0 < (uint32_t)kWdTile) {
@@ -736,8 +820,12 @@ __global__ void __launch_bounds__(kBlock, GLB_WD_MINB) k_wd_relax(
 #pragma unroll
     for (int k = 0; k < kWdEPL; ++k)
       if (valid >> k & 1u) cur[k] = rx.dist(v[k]);
-    uint32_t nnode = 0;
-    nm.st = 0xFFFFFFFFu;
+    uint32_t nnode[kWdPre];
+#pragma unroll
+    for (int i = 0; i < kWdPre; ++i) {
+      nm.st[i] = 0xFFFFFFFFu;
+      nnode[i] = 0;
+    }
     if (has_next) load_items(tn, nm, nnode);
     // ---- stage 3: this tile's atomics  ||  next tile's item distances
     unsigned want = 0;
@@ -751,8 +839,7 @@ __global__ void __launch_bounds__(kBlock, GLB_WD_MINB) k_wd_relax(
 #pragma unroll
     for (int k = 0; k < kWdEPL; ++k)
       if (want >> k & 1u) old[k] = atomicMin(rx.cells + v[k], Cell<D>::make(cand[k], rx.gen));
-    nm.du = DistTraits<D>::kInf;
-    if (nm.st != 0xFFFFFFFFu) nm.du = rx.dist(nnode);
+    load_dist(nm, nnode);
     unsigned first = 0;
 #pragma unroll
     for (int k = 0; k < kWdEPL; ++k)
@@ -776,7 +863,12 @@ __global__ void __launch_bounds__(kBlock, GLB_WD_MINB) k_wd_relax(
     }
     const unsigned wtotal = __shfl_sync(FULL, incl, 31);
     if (wtotal) {
-      if (qn + wtotal > (unsigned)kWdWarpQ) wq_flush(wq, qn, rx.qout, rx.nout);
+      if (qn + wtotal > (unsigned)kWdWarpQ) {
+        if (fused)
+          wq_flush_items(wq, qn, row, ctrl);
+        else
+          wq_flush(wq, qn, rx.qout, rx.nout);
+      }
       unsigned pos = qn + incl - mine;
 #pragma unroll
       for (int k = 0; k < kWdEPL; ++k)
@@ -788,7 +880,10 @@ __global__ void __launch_bounds__(kBlock, GLB_WD_MINB) k_wd_relax(
     m = nm;
     t = tn;
   }
-  wq_flush(wq, qn, rx.qout, rx.nout);
+  if (fused)
+    wq_flush_items(wq, qn, row, ctrl);
+  else
+    wq_flush(wq, qn, rx.qout, rx.nout);
   ThreadCounters c;
   c.work = n_work;
   c.relax = n_relax;

@@ -39,7 +39,7 @@ constexpr int kSmallCtas = 8;                     // cluster size (portable maxi
 constexpr int kSmallThreads = 1024;               // threads per CTA
 constexpr int kSmallAll = kSmallCtas * kSmallThreads;
 constexpr int kSmallItems = kSmallItemsCtl;       // worklist nodes one iteration may hold
-constexpr long long kSmallEdges = 65536;          // WD: active edges one iteration may hold
+constexpr long long kSmallEdges = kSmallEdgesCtl;  // WD: active edges one iteration may hold
 
 // dynamic shared memory of k_small_loop (the WD item table, replicated per CTA)
 template <typename D>
@@ -59,12 +59,22 @@ __device__ __forceinline__ void g_append(uint32_t* q, unsigned int* cursor, uint
 
 // Relax one batch of K edges; improved destinations are appended to the
 // global out-list (its cursor lives in the global control block).
+// Fused WD pushes (WdItems of the next list) instead of node appends; every
+// lane of the warp must call small_relax together when it is set.
+struct SmallPush {
+  const long long* row;
+  WdItem* out;
+  unsigned int* tf;
+  unsigned long long* next_ctr;
+  unsigned int* zero_ctr;
+};
+
 template <int K, typename D, bool W>
 __device__ __forceinline__ unsigned small_relax(const Relaxer<D, W>& rx, unsigned* cursor,
                                                 uint32_t* qout, const uint32_t (&e)[K],
                                                 const D (&dn)[K], unsigned valid,
                                                 ThreadCounters& c, uint32_t (&v)[K],
-                                                D (&cand)[K]) {
+                                                D (&cand)[K], const SmallPush* fused = nullptr) {
   uint32_t w[K];
 #pragma unroll
   for (int k = 0; k < K; ++k)
@@ -96,6 +106,14 @@ __device__ __forceinline__ unsigned small_relax(const Relaxer<D, W>& rx, unsigne
           first |= 1u << k;
       }
     }
+  if (fused) {
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+      wd_push_items((first >> k) & 1u, v[k], fused->row, fused->out, fused->tf, fused->next_ctr,
+                    fused->zero_ctr);
+    c.push += __popc(first);
+    return won;
+  }
 #pragma unroll
   for (int k = 0; k < K; ++k)
     if (first >> k & 1u) {
@@ -103,6 +121,46 @@ __device__ __forceinline__ unsigned small_relax(const Relaxer<D, W>& rx, unsigne
       ++c.push;
     }
   return won;
+}
+
+// Equal edges per thread across the cluster (f = gt + r * 8192) over the item
+// table (s_pre: first edge of every item, s_pre[n_items] = total).  The loop
+// bound is warp-uniform so fused pushes can use warp collectives.
+template <typename D, bool W>
+__device__ __forceinline__ void wd_tiles(const Relaxer<D, W>& rx, unsigned* cursor, uint32_t* qout,
+                                         const uint32_t* s_pre, const uint32_t* s_base,
+                                         const D* s_dn, int n_items, uint32_t total, unsigned gt,
+                                         ThreadCounters& c, const SmallPush* fused) {
+  constexpr int K = 4;
+  const unsigned lane = lane_id();
+  for (uint32_t fb = gt - lane; fb < total; fb += (uint32_t)K * kSmallAll) {
+    uint32_t e[K];
+    D d[K];
+    unsigned valid = 0;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const uint32_t f = fb + lane + (uint32_t)k * kSmallAll;
+      if (f < total) {
+        int lo = 0, hi = n_items;  // last item with s_pre <= f
+        while (hi - lo > 1) {
+          const int mid = (lo + hi) >> 1;
+          if (s_pre[mid] <= f)
+            lo = mid;
+          else
+            hi = mid;
+        }
+        e[k] = s_base[lo] + f;
+        d[k] = s_dn[lo];
+        if (d[k] != DistTraits<D>::kInf)
+          valid |= 1u << k;
+        else
+          ++c.work;
+      }
+    }
+    uint32_t v[K];
+    D cand[K];
+    small_relax<K>(rx, cursor, qout, e, d, valid, c, v, cand, fused);
+  }
 }
 
 template <typename D, bool W>
@@ -147,7 +205,34 @@ __global__ void __cluster_dims__(kSmallCtas, 1, 1) __launch_bounds__(kSmallThrea
     rx.gen = sc.gen;
     ThreadCounters c;
     bool ran = true;
-    if (sc.mode == kModeWD) {
+    SmallPush push;
+    const SmallPush* fused = nullptr;
+    if (sc.wd_fused) {
+      push.row = row;
+      push.out = reinterpret_cast<WdItem*>(sc.wd_items_buf[sc.wd_cur ^ 1]);
+      push.tf = sc.wd_tf_buf[sc.wd_cur ^ 1];
+      push.next_ctr = &gctrl->wd_next;
+      push.zero_ctr = &gctrl->wd_zero_next;
+      fused = &push;
+    }
+    if (sc.mode == kModeWDF) {
+      // ---- the item list the previous step appended: load it as the table
+      const WdItem* it_in = reinterpret_cast<const WdItem*>(sc.wd_items_buf[sc.wd_cur]);
+      const int ni = (int)sc.wd_items;
+      for (int j = tid; j < ni; j += kSmallThreads) {
+        const WdItem it = it_in[j];
+        s_pre[j] = it.pre;
+        s_base[j] = it.base;
+        s_dn[j] = dist_cg<D>(rx.cells, it.node);  // dn at node entry (workload.py:131,140)
+      }
+      if (tid == 0) {
+        s_pre[ni] = (uint32_t)sc.wd_total;
+        s_total = sc.wd_total;
+      }
+      __syncthreads();
+      wd_tiles<D, W>(rx, cursor, qout, s_pre, s_base, s_dn, ni, (uint32_t)sc.wd_total, gt, c,
+                     fused);
+    } else if (sc.mode == kModeWD) {
       // ---- scan of remaining degrees, replicated in every CTA (items
       //      contiguous per thread), so each holds the whole item table
       const long long window = sc.window;
@@ -192,37 +277,8 @@ __global__ void __cluster_dims__(kSmallCtas, 1, 1) __launch_bounds__(kSmallThrea
         }
         if (tid == 0) s_pre[tot_i] = (uint32_t)tot_e;
         __syncthreads();
-        // ---- equal edges per thread across the cluster: f = gt + r * 8192
-        constexpr int K = 4;
-        const uint32_t total = (uint32_t)tot_e;
-        for (uint32_t f0 = gt; f0 < total; f0 += (uint32_t)K * kSmallAll) {
-          uint32_t e[K];
-          D d[K];
-          unsigned valid = 0;
-#pragma unroll
-          for (int k = 0; k < K; ++k) {
-            const uint32_t f = f0 + (uint32_t)k * kSmallAll;
-            if (f < total) {
-              int lo = 0, hi = tot_i;  // last item with s_pre <= f
-              while (hi - lo > 1) {
-                const int mid = (lo + hi) >> 1;
-                if (s_pre[mid] <= f)
-                  lo = mid;
-                else
-                  hi = mid;
-              }
-              e[k] = s_base[lo] + f;
-              d[k] = s_dn[lo];
-              if (d[k] != DistTraits<D>::kInf)
-                valid |= 1u << k;
-              else
-                ++c.work;
-            }
-          }
-          uint32_t v[K];
-          D cand[K];
-          small_relax<K>(rx, cursor, qout, e, d, valid, c, v, cand);
-        }
+        wd_tiles<D, W>(rx, cursor, qout, s_pre, s_base, s_dn, tot_i, (uint32_t)tot_e, gt, c,
+                       fused);
       }
     } else {
       // ---- BS / NS: thread per worklist node (node i -> cluster thread i mod 8192)
@@ -293,7 +349,7 @@ __global__ void __cluster_dims__(kSmallCtas, 1, 1) __launch_bounds__(kSmallThrea
       } else {
         const unsigned produced = __ldcg(cursor);
         cc->qcount[cc->out] = produced;
-        const bool wd_empty = cc->mode == kModeWD && s_total == 0;
+        const bool wd_empty = (cc->mode == kModeWD || cc->mode == kModeWDF) && s_total == 0;
         if (rank == 0 && !wd_empty && cc->nrec < cc->rec_cap) {
           DevRecord& rec = cc->recs[cc->nrec];
           rec.iteration = cc->iteration;
@@ -315,13 +371,19 @@ __global__ void __cluster_dims__(kSmallCtas, 1, 1) __launch_bounds__(kSmallThrea
           hp_end_super(cc);
         } else if (wd_empty) {
           cc->done = 1;
+        } else if (cc->wd_fused) {
+          ctl_wd_fused_advance(cc, __ldcg(&gctrl->wd_next), __ldcg(&gctrl->wd_zero_next));
         } else {
           ctl_simple_advance(cc);
         }
         if (cc->done) cc->mode = kModeDone;
         s_go = small_eligible(cc);
         if (rank == 0) {
-          if (s_go) __stcg(&gctrl->qcount[cc->out], 0u);  // the next iteration's out cursor
+          if (s_go) {  // the next iteration's out cursors
+            __stcg(&gctrl->qcount[cc->out], 0u);
+            __stcg(&gctrl->wd_next, 0ull);
+            __stcg(&gctrl->wd_zero_next, 0u);
+          }
           for (int k = 0; k < 5; ++k) s_acc[k] = 0;
           s_t0 = gtime();
         }

@@ -39,6 +39,8 @@ libs = []
 for path in a.libs:
     L = ctypes.CDLL(str(Path(path).resolve()))
     for name, (res, args) in _lib.SIGNATURES.items():
+        if not hasattr(L, name):  # older builds lack newer entry points
+            continue
         fn = getattr(L, name)
         fn.restype = res
         fn.argtypes = args
