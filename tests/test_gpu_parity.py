@@ -6,6 +6,7 @@ the reference cannot reach quickly, the pinned C oracle (oracle/).
 """
 
 import math
+import os
 
 import numpy as np
 import pytest
@@ -25,8 +26,19 @@ def need_gpu():
     assert _lib.device_count() > 0, "no CUDA device visible to libgraphlb_b200.so"
 
 
+# Execution variants of the same strategies: the CTA-cluster small-frontier
+# loop (default; it takes every iteration of these small graphs), the
+# grid-wide kernels alone (GLB_NO_SMALL), and WD's fused item pushes.
+VARIANTS = {"default": {}, "grid_kernels": {"GLB_NO_SMALL": "1"},
+            "wd_fused": {"GLB_WD_FUSED": "1"},
+            "grid_fused": {"GLB_NO_SMALL": "1", "GLB_WD_FUSED": "1"}}
+
+
+@pytest.mark.parametrize("variant", list(VARIANTS))
 @pytest.mark.parametrize("loop", ["host", "graph"])
-def test_corpus_all_strategies_match_reference(golden, loop):
+def test_corpus_all_strategies_match_reference(golden, loop, variant, monkeypatch):
+    for k, v in VARIANTS[variant].items():
+        monkeypatch.setenv(k, v)
     cfg = pkg.KernelConfig(loop=loop)
     for gid, spec in gs.CORPUS.items():
         g = gs.build(pkg, spec)
@@ -217,6 +229,29 @@ def test_records_and_counters():
     assert sd["EP"] < sd["BS"] and sd["WD"] < sd["BS"] and sd["NS"] < sd["BS"], sd
 
 
+@pytest.mark.parametrize("variant", ["grid_kernels", "wd_fused"])
+def test_random_graphs_execution_variants(oracle, variant, monkeypatch):
+    for k, v in VARIANTS[variant].items():
+        monkeypatch.setenv(k, v)
+    rng = np.random.default_rng(321)
+    for trial in range(10):
+        n = int(rng.integers(1, 3000))
+        m = int(rng.integers(0, 8 * n))
+        src = rng.integers(0, n, size=m)
+        if m:
+            src[: m // 3] = rng.integers(0, max(1, n // 50), size=m // 3)  # hubs
+        dst = rng.integers(0, n, size=m)
+        w = rng.integers(0, 300, size=m) if trial % 2 else None
+        g = pkg.CsrGraph.from_edges(n, src, dst, w)
+        s = int(rng.integers(0, n))
+        for algo in ("bfs", "sssp"):
+            exp = oracle.oracle_distances(g, s, algo)
+            for tag in TAGS:
+                for loop in ("host", "graph"):
+                    r = pkg.run_strategy(tag, g, s, pkg.RelaxOp(algo), pkg.KernelConfig(loop=loop))
+                    assert np.array_equal(r.dist.array, exp), (variant, trial, algo, tag, loop)
+
+
 @pytest.fixture(scope="module")
 def c1_graph():
     return pkg.generate_rmat(16, 16, seed=1, max_weight=255)
@@ -232,6 +267,12 @@ def test_c1_all_strategies(c1_graph, oracle, golden):
             for loop in ("host", "graph"):
                 r = pkg.run_strategy(tag, g, 0, pkg.RelaxOp(algo), pkg.KernelConfig(loop=loop))
                 assert np.array_equal(r.dist.array, exp), (algo, tag, loop)
+        os.environ["GLB_WD_FUSED"] = "1"
+        try:
+            r = pkg.run_strategy("WD", g, 0, pkg.RelaxOp(algo), pkg.KernelConfig(loop="graph"))
+            assert np.array_equal(r.dist.array, exp), (algo, "WD fused")
+        finally:
+            del os.environ["GLB_WD_FUSED"]
 
 
 @pytest.mark.slow
