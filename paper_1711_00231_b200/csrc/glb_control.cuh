@@ -148,6 +148,8 @@ __device__ __forceinline__ void ctl_reset_timers(DevCtrl* c) {
   c->t_relax.start = c->t_scan.start = ~0ull;
   c->t_relax.end = c->t_scan.end = 0;
   c->scan_ticket = c->relax_ticket = 0;
+  c->hp_big_ctr = 0;
+  c->hp_big_done = c->hp_piece_next = 0;
 }
 
 // The host has written the static fields (qptr, strategy, mdt, thresholds,

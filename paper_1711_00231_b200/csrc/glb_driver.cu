@@ -164,6 +164,7 @@ class Runner {
   DevRecord* drecs_ = nullptr;
   HostMirror* h_ = nullptr;
   // WD workspace
+  HpBig* hp_big_ = nullptr;
   WdItem* items_[2] = {nullptr, nullptr};
   unsigned* tile_first_[2] = {nullptr, nullptr};
   LookbackState<2> lb_{};
@@ -233,7 +234,11 @@ class Runner {
       cap_scan_ = cap((const void*)k_wd_scan<D>);
       cap_wd_ = cap((const void*)k_wd_relax<D, W>);
     }
-    if (p_.strategy == GLB_HP) cap_hp_ = std::max(cap((const void*)k_hp_window<D, W>), g_->num_sms);
+    if (p_.strategy == GLB_HP) {
+      cap_hp_ = std::max(cap((const void*)k_hp_window<D, W>), g_->num_sms);
+      // CTA-bin entries: every long window holds >= kHpCtaThreshold edges
+      hp_big_ = (HpBig*)ensure(ws.hp_big, ((size_t)g_->m / kHpCtaThreshold + 64) * sizeof(HpBig));
+    }
     if (p_.strategy != GLB_EP)
       GLB_CUDA_TRY(cudaFuncSetAttribute((const void*)k_small_loop<D, W>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -268,6 +273,7 @@ class Runner {
     // Fused item pushes (no scan between WD steps) measured slower on C2 than
     // scan + relax (the pushes' row loads sit on the relax kernel's critical
     // path), so they are opt-in.
+    c.hp_big = hp_big_;
     c.wd_fused = p_.strategy == GLB_WD && !shard_mode_ && getenv("GLB_WD_FUSED") ? 1 : 0;
     c.recs = drecs_;
     c.ls = ls_;

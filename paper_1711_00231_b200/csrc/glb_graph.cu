@@ -791,7 +791,8 @@ int glb_graph_destroy(glb_graph* g) {
                          &ws.scan_flags, &ws.scan_vals, &ws.stats, &ws.ctrl, &ws.ns_row,
                          &ws.ns_col, &ws.ns_w,   &ws.ns_parent, &ws.ns_cs,  &ws.ns_tmp,
                          &ws.ep_src, &ws.eq[0],  &ws.eq[1],    &ws.out64,   &ws.misc,
-                         &ws.recs,   &ws.hist,   &ws.tile_node};
+                         &ws.recs,   &ws.hist,   &ws.tile_node, &ws.misc_small,
+                         &ws.shard_tmp, &ws.hp_big};
   delete g->shard;
   g->shard = nullptr;
   for (auto& kv : g->gexec) cudaGraphExecDestroy(kv.second);

@@ -115,6 +115,15 @@ enum StepMode : int {
 };
 constexpr int kNumModes = 6;
 
+// One long HP window [lo, hi) of node u at distance dn, relaxed in 2048-edge
+// pieces claimed by any CTA (hierarchical processing's CTA granularity).
+struct HpBig {
+  unsigned long long dn;
+  long long lo, hi;
+  unsigned int qbase;        // first piece of this window in the step's piece space
+  unsigned int pad;
+};
+
 struct StepTimer {  // %globaltimer ns, min over CTA starts / max over CTA ends
   unsigned long long start;
   unsigned long long end;
@@ -165,6 +174,11 @@ struct DevCtrl {
   int wd_cur;
   unsigned long long wd_next;   // (items << 32) | edges appended to list [wd_cur ^ 1]
   unsigned int wd_zero_next;    // zero-degree nodes pushed (counted for the record only)
+  // ---- HP: windows >= kHpCtaThreshold edges form a grid-wide CTA bin
+  struct HpBig* hp_big;         // bin entries of the current window step
+  unsigned long long hp_big_ctr;  // (entries << 32) | pieces reserved, in one atomic
+  unsigned int hp_big_done;     // CTAs done producing (software grid barrier)
+  unsigned int hp_piece_next;   // next piece ticket
   // ---- HP super-iteration state (hierarchical.py:54-136)
   int sup_in, sup_out, cur, spare;
   long long s;
@@ -197,6 +211,7 @@ struct Workspace {
   DevBuf hist;                               // histogram counts
   DevBuf tile_node;                          // first node of every edge tile
   DevBuf misc_small, shard_tmp;              // sharded-run counters / local split
+  DevBuf hp_big;                             // HP CTA-bin entries
 };
 
 }  // namespace glb

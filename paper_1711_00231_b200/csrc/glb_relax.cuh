@@ -899,6 +899,8 @@ __global__ void __launch_bounds__(kBlock, GLB_WD_MINB) k_wd_relax(
 // (each thread finds its edge's node by binary search over the 256 window
 // offsets in shared memory), so lanes walk consecutive edges.
 constexpr long long kHpCtaThreshold = 2048;
+constexpr long long kHpPiece = 2048;  // edges per CTA-bin piece
+constexpr int kHpQbCache = 2048;      // CTA-bin windows whose piece index is cached in smem
 
 template <typename D, bool W>
 __global__ void __launch_bounds__(kBlock, GLB_RELAX_MINB) k_hp_window(const long long* __restrict__ row,
@@ -913,6 +915,8 @@ __global__ void __launch_bounds__(kBlock, GLB_RELAX_MINB) k_hp_window(const long
   __shared__ long long s_lo, s_hi;
   __shared__ D s_dn;
   __shared__ int s_owner;
+  __shared__ long long s_chunk;
+  __shared__ unsigned s_qb[kHpQbCache];  // first piece of every CTA-bin window
   const long long n = ctrl->qcount[ctrl->in];
   if (blockIdx.x * (long long)kBlock >= n) return;  // idle CTA
   timer_begin(ctrl->t_relax);
@@ -923,8 +927,13 @@ __global__ void __launch_bounds__(kBlock, GLB_RELAX_MINB) k_hp_window(const long
   unsigned int* nnext = &ctrl->qcount[ctrl->next];
   const long long window = ctrl->window, mdt = ctrl->mdt;
   ThreadCounters c;
-  for (long long base = blockIdx.x * (long long)kBlock; base < n;
-       base += (long long)gridDim.x * kBlock) {
+  // chunks of 256 sublist nodes handed out by ticket: CTAs that drew light
+  // chunks take more, so one heavy chunk no longer sets the launch time
+  while (true) {
+    if (threadIdx.x == 0) s_chunk = (long long)atomicAdd(&ctrl->relax_ticket, 1ull);
+    __syncthreads();
+    const long long base = s_chunk * kBlock;
+    if (base >= n) break;
     const long long i = base + threadIdx.x;
     long long lo = 0, hi = 0;
     D dn = DistTraits<D>::kInf;
@@ -945,23 +954,18 @@ __global__ void __launch_bounds__(kBlock, GLB_RELAX_MINB) k_hp_window(const long
         }
       }
     }
-    // CTA granularity for long windows
-    while (true) {
-      if (threadIdx.x == 0) s_owner = -1;
-      __syncthreads();
-      if (hi - lo >= kHpCtaThreshold) s_owner = threadIdx.x;
-      __syncthreads();
-      const int o = s_owner;
-      if (o < 0) break;
-      if (threadIdx.x == o) {
-        s_lo = lo;
-        s_hi = hi;
-        s_dn = dn;
-        lo = hi;
-      }
-      __syncthreads();
-      relax_range_coop<4>(rx, bq, s_lo, s_hi, s_dn, threadIdx.x, kBlock, c);
-      bq_flush(bq, rx.qout, rx.nout);
+    // CTA granularity for long windows: into the grid-wide CTA bin, relaxed
+    // below in 2048-edge pieces by whichever CTAs are free
+    if (hi - lo >= kHpCtaThreshold) {
+      const unsigned pieces = (unsigned)((hi - lo + kHpPiece - 1) / kHpPiece);
+      const unsigned long long r =
+          atomicAdd(&ctrl->hp_big_ctr, (1ull << 32) | (unsigned long long)pieces);
+      HpBig* b = ctrl->hp_big + (unsigned)(r >> 32);
+      b->dn = (unsigned long long)dn;
+      b->lo = lo;
+      b->hi = hi;
+      b->qbase = (unsigned)r;
+      lo = hi;
     }
     // fine-grained gather of the remaining windows
     int len = (int)(hi - lo), off, total;
@@ -993,6 +997,56 @@ __global__ void __launch_bounds__(kBlock, GLB_RELAX_MINB) k_hp_window(const long
       relax_batch<K>(rx, bq, e, d, valid, c, v, cand);
     }
     bq_flush(bq, rx.qout, rx.nout);
+  }
+  // ---- the CTA bin: a software grid barrier (every CTA is resident: the
+  //      grid is sized to the occupancy) publishes all long windows, then
+  //      every CTA claims 2048-edge pieces by ticket; a piece's window is found
+  //      by binary search over the windows' first pieces (cached in smem)
+  const long long producers = (n + kBlock - 1) / kBlock < gridDim.x ? (n + kBlock - 1) / kBlock
+                                                                    : (long long)gridDim.x;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(&ctrl->hp_big_done, 1u);
+    while (*((volatile unsigned*)&ctrl->hp_big_done) < (unsigned)producers) {
+    }
+    __threadfence();
+  }
+  __syncthreads();
+  const unsigned long long bc = *((volatile unsigned long long*)&ctrl->hp_big_ctr);
+  const unsigned nbig = (unsigned)(bc >> 32), npieces = (unsigned)bc;
+  if (npieces) {
+    const bool cached = nbig <= (unsigned)kHpQbCache;
+    if (cached)
+      for (unsigned i = threadIdx.x; i < nbig; i += kBlock) s_qb[i] = ctrl->hp_big[i].qbase;
+    __syncthreads();
+    while (true) {
+      if (threadIdx.x == 0) {
+        s_owner = -1;
+        const unsigned t = atomicAdd(&ctrl->hp_piece_next, 1u);
+        if (t < npieces) {
+          unsigned lo_i = 0, hi_i = nbig;  // last window with qbase <= t
+          while (hi_i - lo_i > 1) {
+            const unsigned mid = (lo_i + hi_i) >> 1;
+            const unsigned qb = cached ? s_qb[mid] : ctrl->hp_big[mid].qbase;
+            if (qb <= t)
+              lo_i = mid;
+            else
+              hi_i = mid;
+          }
+          const HpBig b = ctrl->hp_big[lo_i];
+          const long long off = (long long)(t - b.qbase) * kHpPiece;
+          s_lo = b.lo + off;
+          s_hi = b.lo + off + kHpPiece < b.hi ? b.lo + off + kHpPiece : b.hi;
+          s_dn = (D)b.dn;
+          s_owner = 1;
+        }
+      }
+      __syncthreads();
+      if (s_owner < 0) break;
+      relax_range_coop<4>(rx, bq, s_lo, s_hi, s_dn, threadIdx.x, kBlock, c);
+      bq_flush(bq, rx.qout, rx.nout);
+    }
   }
   flush_counters(ctrl->ls, c);
   timer_end(ctrl->t_relax);
