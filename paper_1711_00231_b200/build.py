@@ -21,6 +21,8 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
          "-Xptxas", "-warn-spills", "-diag-suppress", "20054"]
 SOURCES = ["glb_memory.cu", "glb_graph.cu", "glb_driver.cu", "glb_gen.cu", "glb_peak.cu"]
+CXX_SOURCES = ["glb_host_simd.cpp"]
+CXX = os.environ.get("CXX", "g++")
 EXTRA = os.environ.get("GLB_EXTRA_FLAGS", "").split()
 
 
@@ -43,6 +45,13 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     for src in SOURCES:
         obj = BUILD / (Path(src).stem + ".o")
         cmd = [NVCC, *ARCH, *FLAGS, *EXTRA, "-c", str(CSRC / src), "-o", str(obj)]
+        if verbose:
+            print(" ".join(cmd), flush=True)
+        subprocess.run(cmd, check=True)
+        objs.append(str(obj))
+    for src in CXX_SOURCES:  # host-only C++ (AVX2 upload loops)
+        obj = BUILD / (Path(src).stem + ".o")
+        cmd = [CXX, "-O3", "-mavx2", "-fPIC", "-std=c++17", "-c", str(CSRC / src), "-o", str(obj)]
         if verbose:
             print(" ".join(cmd), flush=True)
         subprocess.run(cmd, check=True)

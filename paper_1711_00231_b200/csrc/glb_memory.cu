@@ -19,7 +19,10 @@
 // same workers.
 #include <cuda_runtime.h>
 
+#include <immintrin.h>
+
 #include <algorithm>
+#include <atomic>
 #include <condition_variable>
 #include <cstring>
 #include <functional>
@@ -31,7 +34,19 @@
 
 #include "glb_internal.cuh"
 
+extern "C" {  // glb_host_simd.cpp (AVX2, non-temporal stores)
+int glb_cpu_has_avx2(void);
+int glb_narrow_u32_avx2(const int64_t* src, uint32_t* dst, long long count, uint64_t limit);
+uint64_t glb_narrow_u8_avx2(const int64_t* src, uint8_t* dst, long long count);
+}
+
 namespace glb {
+namespace {
+bool has_avx2() {
+  static const bool v = glb_cpu_has_avx2() != 0;
+  return v;
+}
+}  // namespace
 
 // ==================================================== device memory cache ===
 // Grow-only workspaces and graph arrays are recycled across graph handles
@@ -196,24 +211,24 @@ class Workers {
     return *w;
   }
   unsigned size() const { return nt_; }
-  // f(worker, nworkers) on every worker, the caller being worker 0
+  // f(worker, nworkers) on every worker, the caller being worker 0.  Workers
+  // spin briefly between jobs (an upload issues one job per 32 MB chunk, back
+  // to back), then sleep on a condition variable.
   void run(const std::function<void(unsigned, unsigned)>& f) {
     std::lock_guard<std::mutex> serial(run_mu_);
     if (nt_ == 1) {
       f(0, 1);
       return;
     }
+    job_.store(&f, std::memory_order_relaxed);
+    pending_.store(nt_ - 1, std::memory_order_relaxed);
     {
       std::lock_guard<std::mutex> lk(mu_);
-      job_ = &f;
-      pending_ = nt_ - 1;
-      ++gen_;
+      gen_.fetch_add(1, std::memory_order_release);
     }
     cv_.notify_all();
     f(0, nt_);
-    std::unique_lock<std::mutex> lk(mu_);
-    done_.wait(lk, [&] { return pending_ == 0; });
-    job_ = nullptr;
+    while (pending_.load(std::memory_order_acquire) != 0) _mm_pause();
   }
 
  private:
@@ -225,23 +240,26 @@ class Workers {
   void loop(unsigned t) {
     unsigned seen = 0;
     while (true) {
-      const std::function<void(unsigned, unsigned)>* f;
-      {
-        std::unique_lock<std::mutex> lk(mu_);
-        cv_.wait(lk, [&] { return gen_ != seen; });
-        seen = gen_;
-        f = job_;
+      unsigned g = gen_.load(std::memory_order_acquire);
+      for (int spin = 0; g == seen && spin < (1 << 16); ++spin) {
+        _mm_pause();
+        g = gen_.load(std::memory_order_acquire);
       }
-      (*f)(t, nt_);
-      std::lock_guard<std::mutex> lk(mu_);
-      if (--pending_ == 0) done_.notify_one();
+      if (g == seen) {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [&] { return gen_.load(std::memory_order_acquire) != seen; });
+        g = gen_.load(std::memory_order_acquire);
+      }
+      seen = g;
+      (*job_.load(std::memory_order_relaxed))(t, nt_);
+      pending_.fetch_sub(1, std::memory_order_acq_rel);
     }
   }
   unsigned nt_ = 1;
   std::mutex run_mu_, mu_;
-  std::condition_variable cv_, done_;
-  const std::function<void(unsigned, unsigned)>* job_ = nullptr;
-  unsigned gen_ = 0, pending_ = 0;
+  std::condition_variable cv_;
+  std::atomic<const std::function<void(unsigned, unsigned)>*> job_{nullptr};
+  std::atomic<unsigned> gen_{0}, pending_{0};
 };
 
 // [begin, end) slice of `count` items for worker t of nt (64-item aligned)
@@ -391,10 +409,14 @@ void upload_narrow(glb_graph* g, const int64_t* src, long long count, uint32_t* 
         long long lo, hi;
         slice(len, t, nt, lo, hi);
         unsigned long long orv = 0;
-        for (long long i = lo; i < hi; ++i) {
-          const unsigned long long v = (unsigned long long)src[off + i];
-          orv |= v;
-          dst[i] = (uint8_t)v;
+        if (has_avx2()) {
+          orv = glb_narrow_u8_avx2(src + off + lo, dst + lo, hi - lo);
+        } else {
+          for (long long i = lo; i < hi; ++i) {
+            const unsigned long long v = (unsigned long long)src[off + i];
+            orv |= v;
+            dst[i] = (uint8_t)v;
+          }
         }
         if (orv > 255) wide[t] = 1;
       });
@@ -412,10 +434,14 @@ void upload_narrow(glb_graph* g, const int64_t* src, long long count, uint32_t* 
         long long lo, hi;
         slice(len, t, nt, lo, hi);
         bool badt = false;
-        for (long long i = lo; i < hi; ++i) {
-          const unsigned long long v = (unsigned long long)src[off + i];
-          badt |= v >= limit;
-          dst[i] = (uint32_t)v;
+        if (has_avx2()) {
+          badt = glb_narrow_u32_avx2(src + off + lo, dst + lo, hi - lo, limit) != 0;
+        } else {
+          for (long long i = lo; i < hi; ++i) {
+            const unsigned long long v = (unsigned long long)src[off + i];
+            badt |= v >= limit;
+            dst[i] = (uint32_t)v;
+          }
         }
         if (badt) bad[t] = 1;
       });

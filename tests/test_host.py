@@ -178,3 +178,38 @@ def test_grid_generator_shape():
     assert deg[0, 0] == 2 and deg[0, 2] == 3 and deg[2, 2] == 4
     assert g.col_indices[g.row_offsets[12]:g.row_offsets[13]].tolist() == [7, 11, 13, 17]
     assert g.weights.min() >= 1 and g.weights.max() <= 255
+
+
+def test_upload_narrowing_loops_match_numpy():
+    """The AVX2 narrowing of the upload (glb_host_simd.cpp) against numpy,
+    including unaligned tails and the range / byte checks."""
+    lib = ctypes.CDLL(str(_lib.LIB_PATH))
+    if not lib.glb_cpu_has_avx2():
+        pytest.skip("host has no AVX2")
+    f32 = lib.glb_narrow_u32_avx2
+    f32.restype = ctypes.c_int
+    f32.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_longlong, ctypes.c_uint64]
+    f8 = lib.glb_narrow_u8_avx2
+    f8.restype = ctypes.c_uint64
+    f8.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_longlong]
+    rng = np.random.default_rng(5)
+    for count in (0, 1, 7, 8, 9, 1000, 4099):
+        src = rng.integers(0, 1000, size=count).astype(np.int64)
+        dst = np.zeros(count + 64, dtype=np.uint32)
+        d = dst[: count] if dst.ctypes.data % 32 == 0 else dst[8 - (dst.ctypes.data % 32) // 4:][:count]
+        assert f32(src.ctypes.data, d.ctypes.data, count, 1000) == 0
+        assert np.array_equal(d, src.astype(np.uint32))
+        if count:
+            bad = src.copy()
+            bad[count // 2] = 1000
+            assert f32(bad.ctypes.data, d.ctypes.data, count, 1000) != 0
+            bad[count // 2] = -1
+            assert f32(bad.ctypes.data, d.ctypes.data, count, 1000) != 0
+        b = rng.integers(0, 256, size=count).astype(np.int64)
+        d8 = np.zeros(count + 16, dtype=np.uint8)
+        o = f8(b.ctypes.data, d8.ctypes.data, count)
+        assert o == (int(np.bitwise_or.reduce(b)) if count else 0)
+        assert np.array_equal(d8[:count], b.astype(np.uint8))
+        if count:
+            b[-1] = 300
+            assert f8(b.ctypes.data, d8.ctypes.data, count) > 255
