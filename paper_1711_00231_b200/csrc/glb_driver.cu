@@ -17,6 +17,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <sstream>
+#include <unordered_map>
+#include <mutex>
 #include <vector>
 
 #include "glb_control.cuh"
@@ -44,12 +46,6 @@ double now_ms() {
       .count();
 }
 
-void* ensure_zero(DevBuf& b, size_t bytes, cudaStream_t s) {
-  const bool grow = b.bytes < (bytes ? bytes : 16);
-  void* p = ensure(b, bytes);
-  if (grow) GLB_CUDA_TRY(cudaMemsetAsync(p, 0, b.bytes, s));
-  return p;
-}
 
 struct HostMirror {  // pinned layout of g->host_ctrl
   DevCtrl ctrl;
@@ -470,7 +466,7 @@ class Runner {
   // ----------------------------------------------------- graph loop ---
   std::string graph_key() const {
     std::ostringstream k;
-    k << p_.strategy << '|' << sizeof(D) << '|' << W << '|' << p_.chunked << '|' << cap_relax_
+    k << g_->device << '|' << p_.strategy << '|' << sizeof(D) << '|' << W << '|' << p_.chunked << '|' << cap_relax_
       << '|' << cap_scan_ << '|' << cap_wd_ << '|' << cap_hp_ << '|' << (const void*)row_ << '|'
       << (const void*)col_ << '|' << (const void*)wt_ << '|' << (const void*)cs_ << '|'
       << (const void*)src_ << '|' << (const void*)cells_ << '|' << (const void*)stamp_ << '|'
@@ -575,16 +571,32 @@ class Runner {
     }
   }
 
+  // Instantiated loop graphs are cached process-wide by everything captured
+  // into them (device, strategy, widths, grids and every buffer pointer).
+  // With the caching allocator a new graph of the same shape usually gets the
+  // same buffers back, so create -> run -> destroy cycles reuse the exec.
   void loop_graph() {
     const std::string key = graph_key();
     cudaGraphExec_t exec = nullptr;
-    for (auto& kv : g_->gexec)
-      if (kv.first == key) exec = kv.second;
+    {
+      std::lock_guard<std::mutex> lk(exec_cache_mu());
+      auto it = exec_cache().find(key);
+      if (it != exec_cache().end()) exec = it->second;
+    }
     if (!exec) {
       exec = build_graph();
-      g_->gexec.emplace_back(key, exec);
+      std::lock_guard<std::mutex> lk(exec_cache_mu());
+      exec_cache().emplace(key, exec);
     }
     GLB_CUDA_TRY(cudaGraphLaunch(exec, s_));
+  }
+  static std::mutex& exec_cache_mu() {
+    static std::mutex* m = new std::mutex();
+    return *m;
+  }
+  static std::unordered_map<std::string, cudaGraphExec_t>& exec_cache() {
+    static auto* c = new std::unordered_map<std::string, cudaGraphExec_t>();
+    return *c;
   }
 
   // ---------------------------------------------------------- results ---

@@ -37,12 +37,17 @@ void* ensure(DevBuf& b, size_t bytes) {
   b.bytes = 0;
   b.p = dmalloc(bytes);
   b.bytes = bytes;
-  // Workspaces start zeroed, as fresh driver allocations do in practice: the
-  // look-back flags and counters rely on it, and a recycled block holds
-  // another graph's epochs.
-  GLB_CUDA_TRY(cudaMemset(b.p, 0, bytes));
-  GLB_CUDA_TRY(cudaDeviceSynchronize());
   return b.p;
+}
+
+// A recycled block holds another graph's data: buffers whose protocol needs
+// zeros (look-back flags, stamps, counters) are cleared whenever they are
+// (re)acquired.
+void* ensure_zero(DevBuf& b, size_t bytes, cudaStream_t s) {
+  const bool grow = b.bytes < (bytes ? bytes : 16);
+  void* p = ensure(b, bytes);
+  if (grow) GLB_CUDA_TRY(cudaMemsetAsync(p, 0, b.bytes, s));
+  return p;
 }
 
 void free_buf(DevBuf& b) {
@@ -391,7 +396,8 @@ void split_device(glb_graph* g, long long mdt, long long totals_out[4]) {
   long long* totals = exc + (n + 1);
   // scan look-back state
   long long ntiles = (n + kSplitTile - 1) / kSplitTile;
-  unsigned* flags = (unsigned*)ensure(ws.scan_flags, (size_t)std::max<long long>(ntiles, 1) * 4 + 4096);
+  unsigned* flags =
+      (unsigned*)ensure_zero(ws.scan_flags, (size_t)std::max<long long>(ntiles, 1) * 4 + 4096, g->stream);
   size_t vbytes = (size_t)std::max<long long>(ntiles, 1) * sizeof(Vec<4>);
   char* vals = (char*)ensure(ws.scan_vals, 2 * vbytes + 4096);
   LookbackState<4> lb{flags, (Vec<4>*)vals, (Vec<4>*)(vals + vbytes)};
@@ -762,8 +768,6 @@ int glb_graph_restrict(glb_graph* g, int64_t v_lo, int64_t v_hi) {
     g->col = col2;
     g->wt = w2;
     g->m = m2;
-    for (auto& kv : g->gexec) cudaGraphExecDestroy(kv.second);
-    g->gexec.clear();
     DevCtrl* ctrl = (DevCtrl*)ensure(g->ws.ctrl, sizeof(DevCtrl));
     GLB_CUDA_TRY(cudaMemsetAsync(ctrl, 0, sizeof(DevCtrl), g->stream));
     k_check_rows<<<grid_for(g->n, kBlock, g->num_sms * 8), kBlock, 0, g->stream>>>(
@@ -795,8 +799,6 @@ int glb_graph_destroy(glb_graph* g) {
                          &ws.shard_tmp, &ws.hp_big};
   delete g->shard;
   g->shard = nullptr;
-  for (auto& kv : g->gexec) cudaGraphExecDestroy(kv.second);
-  g->gexec.clear();
   for (auto* b : bufs) glb::free_buf(*b);
   for (auto e : g->ev_pool) cudaEventDestroy(e);
   if (g->ev[0]) cudaEventDestroy(g->ev[0]);

@@ -247,7 +247,6 @@ struct glb_graph {
   cudaEvent_t ev[2] = {nullptr, nullptr};
   std::vector<cudaEvent_t> ev_pool;
   std::vector<glb_record> last_records;  // records of the most recent glb_run
-  std::vector<std::pair<std::string, cudaGraphExec_t>> gexec;  // instantiated loops
   glb::ShardSessionBase* shard = nullptr;                       // sharded run in progress
   std::mutex mu;              // drivers are not re-entrant (common.py:5-6)
 };
@@ -260,7 +259,8 @@ namespace glb {
 void* dmalloc(size_t bytes);
 void dfree(void* p);
 size_t release_cached(int device);  // device < 0: every device
-void* ensure(DevBuf& b, size_t bytes);  // grow-only device allocation
+void* ensure(DevBuf& b, size_t bytes);  // grow-only device allocation (contents undefined)
+void* ensure_zero(DevBuf& b, size_t bytes, cudaStream_t s);  // ... zeroed when (re)acquired
 void free_buf(DevBuf& b);
 constexpr size_t kPinnedSmallBytes = size_t(1) << 16;
 void* pinned_small_get();  // pooled pinned block of kPinnedSmallBytes
