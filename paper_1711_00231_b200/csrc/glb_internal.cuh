@@ -288,6 +288,9 @@ __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
 // L2 eviction-priority hints (sm_80+ createpolicy): the distance cells are the
 // randomly re-read working set and should outlive the single-use col/weight
 // stream in the 126 MB L2.
+#ifndef GLB_STREAM_POLICY
+#define GLB_STREAM_POLICY 1
+#endif
 #ifndef GLB_L2_HINTS
 #define GLB_L2_HINTS 0  // measured slower on C2 (evict_last cells / evict_first streams)
 #endif
@@ -303,6 +306,29 @@ __device__ __forceinline__ unsigned long long ld_cell(const unsigned long long* 
   return r;
 #else
   return *p;
+#endif
+}
+// Single-use streams (col / weights): an L2 evict-first access policy, made
+// once per thread, so a pass over the 537 MB edge arrays does not push the
+// randomly re-read distance cells out of L2 (ncu: with plain or .cs loads
+// every sector of the stream is allocated evict_normal).
+__device__ __forceinline__ unsigned long long l2_evict_first() {
+#if GLB_STREAM_POLICY
+  unsigned long long p;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+#else
+  return 0;
+#endif
+}
+__device__ __forceinline__ uint32_t ld_stream_pol(const uint32_t* p, unsigned long long pol) {
+#if GLB_STREAM_POLICY
+  uint32_t r;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(pol));
+  return r;
+#else
+  (void)pol;
+  return __ldg(p);
 #endif
 }
 __device__ __forceinline__ uint32_t ld_stream(const uint32_t* p) {

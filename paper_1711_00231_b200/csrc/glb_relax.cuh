@@ -148,17 +148,22 @@ __device__ __forceinline__ void timer_end(StepTimer& t) {
 // dn[k] != INF).  Returns the mask of edges whose atomicMin strictly lowered
 // dist[v[k]] to cand[k] (atomic_relax_min, engine.py:120-139); the ones that
 // also won the stamp claim were pushed to the CTA queue.
-template <int K, typename D, bool W>
+// STREAM: the K edges of a batch are lanes-consecutive across the warp, so
+// every col / weight line is consumed by one load instruction and can be
+// fetched evict-first; thread-serial walks (BS, NS) reuse a line over several
+// batches and keep the default policy.
+template <int K, bool STREAM = true, typename D, bool W>
 __device__ __forceinline__ unsigned relax_batch(const Relaxer<D, W>& rx, BlockQ& bq,
                                                 const long long (&e)[K], const D (&dn)[K],
                                                 unsigned valid, ThreadCounters& c,
                                                 uint32_t (&v)[K], D (&cand)[K]) {
   uint32_t w[K];
+  const unsigned long long pol = STREAM ? l2_evict_first() : 0ull;
 #pragma unroll
   for (int k = 0; k < K; ++k)
     if (valid >> k & 1u) {
-      v[k] = ld_stream(rx.col + e[k]);
-      w[k] = W ? ld_stream(rx.wt + e[k]) : 1u;
+      v[k] = STREAM ? ld_stream_pol(rx.col + e[k], pol) : __ldg(rx.col + e[k]);
+      w[k] = W ? (STREAM ? ld_stream_pol(rx.wt + e[k], pol) : __ldg(rx.wt + e[k])) : 1u;
     }
   unsigned want = 0;
 #if GLB_PRECHECK
@@ -229,7 +234,7 @@ __device__ __forceinline__ void relax_range_thread(const Relaxer<D, W>& rx, Bloc
     }
     uint32_t v[K];
     D cand[K];
-    relax_batch<K>(rx, bq, e, d, valid, c, v, cand);
+    relax_batch<K, false>(rx, bq, e, d, valid, c, v, cand);
   }
 }
 
@@ -316,7 +321,7 @@ __global__ void __launch_bounds__(kBlock) k_ns_relax(const long long* __restrict
           }
           uint32_t v[K];
           D cand[K];
-          unsigned won = relax_batch<K>(rx, bq, e, d, valid, c, v, cand);
+          unsigned won = relax_batch<K, false>(rx, bq, e, d, valid, c, v, cand);
           // reflect each improved parent's value onto its children (splitting.py:154-160)
 #pragma unroll
           for (int k = 0; k < K; ++k) {
@@ -371,6 +376,7 @@ __global__ void __launch_bounds__(kBlock) k_ep_relax(const long long* __restrict
   ThreadCounters c;
   constexpr int K = 4;
   const unsigned stride = gridDim.x * kBlock;
+  const unsigned long long pol = l2_evict_first();
   for (unsigned base = blockIdx.x * kBlock; base < n; base += stride * K) {
     uint32_t e[K], u[K], v[K], w[K];
     D du[K], cur[K], cand[K];
@@ -386,9 +392,9 @@ __global__ void __launch_bounds__(kBlock) k_ep_relax(const long long* __restrict
 #pragma unroll
     for (int k = 0; k < K; ++k)
       if (valid >> k & 1u) {
-        u[k] = __ldcs(src + e[k]);
-        v[k] = ld_stream(rx.col + e[k]);
-        w[k] = W ? ld_stream(rx.wt + e[k]) : 1u;
+        u[k] = ld_stream_pol(src + e[k], pol);
+        v[k] = ld_stream_pol(rx.col + e[k], pol);
+        w[k] = W ? ld_stream_pol(rx.wt + e[k], pol) : 1u;
       }
 #pragma unroll
     for (int k = 0; k < K; ++k)
@@ -695,6 +701,7 @@ __global__ void __launch_bounds__(kBlock, GLB_WD_MINB) k_wd_relax(
   constexpr unsigned FULL = 0xffffffffu;
   const long long stride = (long long)gridDim.x * kWdWarps;
   const uint32_t last_item = (uint32_t)(nitems - 1);
+  const unsigned long long pol = l2_evict_first();
 
   auto load_items = [&](long long tt, WdMeta<D>& mm, uint32_t (&node)[kWdPre]) {
     const uint32_t te0 = (uint32_t)(tt * kWdTile);
@@ -806,8 +813,8 @@ __global__ void __launch_bounds__(kBlock, GLB_WD_MINB) k_wd_relax(
 #pragma unroll
     for (int k = 0; k < kWdEPL; ++k)
       if (valid >> k & 1u) {
-        v[k] = __ldg(rx.col + e[k]);
-        w[k] = W ? __ldg(rx.wt + e[k]) : 1u;
+        v[k] = ld_stream_pol(rx.col + e[k], pol);
+        w[k] = W ? ld_stream_pol(rx.wt + e[k], pol) : 1u;
       }
     WdMeta<D> nm;
     nm.j0 = nm.j1 = 0;
