@@ -111,6 +111,14 @@ __device__ __forceinline__ void hp_decide_sub(DevCtrl* c) {
   }
 }
 
+// WD over a frontier holding at least 1/kDenseDiv of the nodes scans the
+// cells in id order (packed cells only: the generation marks the worklist).
+constexpr long long kDenseDiv = 8;
+__device__ __forceinline__ void ctl_choose_dense(DevCtrl* c) {
+  c->wd_dense = c->dense_ok && c->strategy == GLB_WD && c->mode == kModeWD && !c->use_small &&
+                (long long)c->qcount[c->in] * kDenseDiv >= c->n_nodes;
+}
+
 __device__ __forceinline__ int ctl_step_kind(const DevCtrl* c) {
   return c->use_small ? (int)kModeSmall : c->mode;
 }
@@ -218,6 +226,7 @@ __global__ void k_control(DevCtrl* c, cudaGraphConditionalHandle h_loop,
   if (c->small_exit) {  // k_small_loop recorded and advanced its own iterations
     c->small_exit = 0;
     c->use_small = 0;
+    ctl_choose_dense(c);
     ctl_set_conditionals(c, h_loop, h_mode, graph_mode);
     return;
   }
@@ -275,6 +284,7 @@ __global__ void k_control(DevCtrl* c, cudaGraphConditionalHandle h_loop,
   }
   if (c->done && !c->paused) c->mode = kModeDone;
   c->use_small = small_eligible(c);
+  ctl_choose_dense(c);
   ctl_set_conditionals(c, h_loop, h_mode, graph_mode);
 }
 

@@ -270,6 +270,12 @@ class Runner {
     // scan + relax (the pushes' row loads sit on the relax kernel's critical
     // path), so they are opt-in.
     c.hp_big = hp_big_;
+    c.n_nodes = n_all_;
+    // Dense-frontier scans (cells in id order) speed the relax kernel up per
+    // edge but the id-ordered processing does ~10 % more re-relaxation on C2,
+    // a wash overall, so they are opt-in.
+    c.dense_ok = p_.strategy == GLB_WD && !shard_mode_ && Cell<D>::kPacked &&
+                 getenv("GLB_WD_DENSE") ? 1 : 0;
     c.wd_fused = p_.strategy == GLB_WD && !shard_mode_ && getenv("GLB_WD_FUSED") ? 1 : 0;
     c.recs = drecs_;
     c.ls = ls_;
@@ -353,7 +359,7 @@ class Runner {
     GLB_CHECK_LAUNCH();
   }
   void launch_wd_scan(unsigned grid) {
-    k_wd_scan<D><<<grid, kBlock, 0, s_>>>(row_, lb_,
+    k_wd_scan<D><<<grid, kBlock, 0, s_>>>(row_, cells_, lb_,
                                           ctrl_);
     GLB_CHECK_LAUNCH();
   }
@@ -426,7 +432,7 @@ class Runner {
             ev.o1 = event();
             GLB_CUDA_TRY(cudaEventRecord(ev.o0, s_));
           }
-          launch_wd_scan(grid_for(n_in, kWdScanTile, cap_scan_));
+          launch_wd_scan(grid_for(c.wd_dense ? n_all_ : n_in, kWdScanTile, cap_scan_));
           if (timing) GLB_CUDA_TRY(cudaEventRecord(ev.o1, s_));
           if (timing) GLB_CUDA_TRY(cudaEventRecord(ev.k0, s_));
           launch_wd_relax(cap_wd_);

@@ -174,6 +174,9 @@ struct DevCtrl {
   int wd_cur;
   unsigned long long wd_next;   // (items << 32) | edges appended to list [wd_cur ^ 1]
   unsigned int wd_zero_next;    // zero-degree nodes pushed (counted for the record only)
+  int wd_dense;                 // the WD scan reads the frontier from the cells, not the queue
+  int dense_ok;                 // packed cells, WD strategy, not sharded
+  long long n_nodes;            // nodes of the traversed graph
   // ---- HP: windows >= kHpCtaThreshold edges form a grid-wide CTA bin
   struct HpBig* hp_big;         // bin entries of the current window step
   unsigned long long hp_big_ctr;  // (entries << 32) | pieces reserved, in one atomic

@@ -41,6 +41,9 @@
 #ifndef GLB_RELAX_MINB
 #define GLB_RELAX_MINB 3  // CTAs per SM the HP window kernel is register-capped for
 #endif
+#ifndef GLB_CELL_POLICY
+#define GLB_CELL_POLICY 0  // evict-last hint on the cell gathers (A/B switch)
+#endif
 #ifndef GLB_WD_MINB
 #define GLB_WD_MINB 2  // the pipelined WD relax: 2 CTAs/SM without spills beat 3 with (C2 A/B)
 #endif
@@ -112,8 +115,17 @@ struct Relaxer {
   uint32_t* qout;
   unsigned int* nout;
   unsigned int* ovf;
+  unsigned long long keep;    // L2 evict-last policy for the cells (GLB_CELL_POLICY)
 
-  __device__ __forceinline__ D dist(uint32_t u) const { return Cell<D>::dist(ld_cell(cells + u)); }
+  __device__ __forceinline__ D dist(uint32_t u) const {
+#if GLB_CELL_POLICY
+    unsigned long long r;
+    asm("ld.global.L2::cache_hint.u64 %0, [%1], %2;" : "=l"(r) : "l"(cells + u), "l"(keep));
+    return Cell<D>::dist(r);
+#else
+    return Cell<D>::dist(ld_cell(cells + u));
+#endif
+  }
   // push claim after a strict decrease (first = packed-cell verdict)
   __device__ __forceinline__ bool claim_push(uint32_t v, bool first) const {
     if (Cell<D>::kPacked) return first;
@@ -128,6 +140,9 @@ __device__ __forceinline__ Relaxer<D, W> bind(Relaxer<D, W> rx, DevCtrl* ctrl) {
   rx.gen = ctrl->gen;
   rx.qout = ctrl->qptr[ctrl->out];
   rx.nout = &ctrl->qcount[ctrl->out];
+#if GLB_CELL_POLICY
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(rx.keep));
+#endif
   return rx;
 }
 
@@ -487,13 +502,21 @@ struct __align__(16) WdItem {
 // start of find_offsets (workload.py:45-72) at warp-tile granularity.
 template <typename D>
 __global__ void __launch_bounds__(kBlock) k_wd_scan(const long long* __restrict__ row,
+                                                    const unsigned long long* __restrict__ cells,
                                                     LookbackState<2> lb, DevCtrl* ctrl) {
   WdItem* __restrict__ items = reinterpret_cast<WdItem*>(ctrl->wd_items_buf[ctrl->wd_cur]);
   unsigned int* __restrict__ tile_first = ctrl->wd_tf_buf[ctrl->wd_cur];
   using TS = TileScan<2, kBlock>;
   __shared__ typename TS::Storage st;
   __shared__ long long s_tile;
-  const long long n = ctrl->qcount[ctrl->in];
+  // Dense frontier (a large fraction of all nodes): the worklist is exactly
+  // {v : cell generation == the generation that pushed it}, so scan the nodes
+  // in id order instead of the queue.  Items then come out sorted, their
+  // CSR segments touch, and the relax kernel's col / weight reads become
+  // contiguous runs instead of one partial sector per short segment.
+  const bool dense = ctrl->wd_dense != 0;
+  const uint32_t in_gen = ctrl->gen - 1u;
+  const long long n = dense ? ctrl->n_nodes : ctrl->qcount[ctrl->in];
   const long long ntiles = (n + kWdScanTile - 1) / kWdScanTile;
   if (ntiles == 0) {
     if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -519,7 +542,14 @@ __global__ void __launch_bounds__(kBlock) k_wd_scan(const long long* __restrict_
     uint32_t v[kWdIPT];
     long long beg[kWdIPT], rem[kWdIPT];
     Vec<2> sum;
-    if (first + kWdIPT <= n) {  // two 128-bit loads of worklist items
+    unsigned act = 0xFFu;
+    if (dense) {
+#pragma unroll
+      for (int k = 0; k < kWdIPT; ++k) {
+        v[k] = (uint32_t)(first + k);
+        if (first + k >= n || Cell<D>::gen(cells[first + k]) != in_gen) act &= ~(1u << k);
+      }
+    } else if (first + kWdIPT <= n) {  // two 128-bit loads of worklist items
       const uint4 a = *reinterpret_cast<const uint4*>(q + first);
       const uint4 b = *reinterpret_cast<const uint4*>(q + first + 4);
       v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
@@ -531,7 +561,7 @@ __global__ void __launch_bounds__(kBlock) k_wd_scan(const long long* __restrict_
 #pragma unroll
     for (int k = 0; k < kWdIPT; ++k) {
       rem[k] = 0;
-      if (first + k < n) {
+      if (first + k < n && (act >> k & 1u)) {
         const long long lo = row[v[k]], hi = row[v[k] + 1];
         const long long b = hi - lo < window ? hi - lo : window;
         beg[k] = lo + b;

@@ -31,7 +31,8 @@ def need_gpu():
 # grid-wide kernels alone (GLB_NO_SMALL), and WD's fused item pushes.
 VARIANTS = {"default": {}, "grid_kernels": {"GLB_NO_SMALL": "1"},
             "wd_fused": {"GLB_WD_FUSED": "1"},
-            "grid_fused": {"GLB_NO_SMALL": "1", "GLB_WD_FUSED": "1"}}
+            "grid_fused": {"GLB_NO_SMALL": "1", "GLB_WD_FUSED": "1"},
+            "grid_dense": {"GLB_NO_SMALL": "1", "GLB_WD_DENSE": "1"}}
 
 
 @pytest.mark.parametrize("variant", list(VARIANTS))
@@ -229,7 +230,7 @@ def test_records_and_counters():
     assert sd["EP"] < sd["BS"] and sd["WD"] < sd["BS"] and sd["NS"] < sd["BS"], sd
 
 
-@pytest.mark.parametrize("variant", ["grid_kernels", "wd_fused"])
+@pytest.mark.parametrize("variant", ["grid_kernels", "wd_fused", "grid_dense"])
 def test_random_graphs_execution_variants(oracle, variant, monkeypatch):
     for k, v in VARIANTS[variant].items():
         monkeypatch.setenv(k, v)
