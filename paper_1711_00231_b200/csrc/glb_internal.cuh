@@ -414,15 +414,19 @@ __device__ __forceinline__ void flush_counters(LaunchStats* ls, const ThreadCoun
     unsigned long long o = __shfl_xor_sync(0xffffffffu, mx, off);
     mx = o > mx ? o : mx;
   }
-  __shared__ unsigned long long s_acc[5];
-  if (threadIdx.x < 5) s_acc[threadIdx.x] = 0;
+  // sums in 64-bit shared atomics (native adds); the per-thread maximum in a
+  // 32-bit one (a 64-bit shared atomicMax is a CAS loop)
+  __shared__ unsigned long long s_acc[4];
+  __shared__ unsigned int s_max;
+  if (threadIdx.x < 4) s_acc[threadIdx.x] = 0;
+  if (threadIdx.x == 0) s_max = 0;
   __syncthreads();
   if (lane_id() == 0) {
     atomicAdd(&s_acc[0], w);
     atomicAdd(&s_acc[1], r);
     atomicAdd(&s_acc[2], p);
     atomicAdd(&s_acc[3], sq);
-    atomicMax(&s_acc[4], mx);
+    atomicMax(&s_max, mx > 0xFFFFFFFFull ? 0xFFFFFFFFu : (unsigned)mx);
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -431,7 +435,7 @@ __device__ __forceinline__ void flush_counters(LaunchStats* ls, const ThreadCoun
     if (s_acc[1]) atomicAdd(&s.relax, s_acc[1]);
     if (s_acc[2]) atomicAdd(&s.push, s_acc[2]);
     if (s_acc[3]) atomicAdd(&s.work_sq, s_acc[3]);
-    if (s_acc[4]) atomicMax(&s.work_max, s_acc[4]);
+    if (s_max) atomicMax(&s.work_max, (unsigned long long)s_max);
   }
 }
 

@@ -42,7 +42,7 @@
 #define GLB_RELAX_MINB 3  // CTAs per SM the HP window kernel is register-capped for
 #endif
 #ifndef GLB_CELL_POLICY
-#define GLB_CELL_POLICY 0  // evict-last hint on the cell gathers (A/B switch)
+#define GLB_CELL_POLICY 1  // evict-last L2 hint on the cell gathers (C2: -3 % WD, -4 % HP)
 #endif
 #ifndef GLB_WD_MINB
 #define GLB_WD_MINB 2  // the pipelined WD relax: 2 CTAs/SM without spills beat 3 with (C2 A/B)

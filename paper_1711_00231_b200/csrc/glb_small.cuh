@@ -179,6 +179,7 @@ __global__ void __cluster_dims__(kSmallCtas, 1, 1) __launch_bounds__(kSmallThrea
   } s_scan;
   __shared__ DevCtrl sc;                 // this CTA's copy of the control block
   __shared__ unsigned long long s_acc[5];  // CTA 0: the cluster's iteration counters
+  __shared__ unsigned int s_max;           // CTA 0: per-thread work maximum (32-bit: native atomicMax)
   __shared__ long long s_total;
   __shared__ int s_go;
   __shared__ unsigned long long s_t0;
@@ -188,6 +189,7 @@ __global__ void __cluster_dims__(kSmallCtas, 1, 1) __launch_bounds__(kSmallThrea
   const unsigned tid = threadIdx.x;
   const unsigned gt = rank * kSmallThreads + tid;
   unsigned long long* acc0 = cluster.map_shared_rank(s_acc, 0);
+  unsigned int* max0 = cluster.map_shared_rank(&s_max, 0);
 
   if (tid == 0) {
     sc = *gctrl;
@@ -195,6 +197,7 @@ __global__ void __cluster_dims__(kSmallCtas, 1, 1) __launch_bounds__(kSmallThrea
     s_t0 = gtime();
   }
   if (tid < 5) s_acc[tid] = 0;
+  if (tid == 0) s_max = 0;
   cluster.sync();
   while (s_go) {
     const unsigned n = sc.qcount[sc.in];
@@ -338,7 +341,7 @@ __global__ void __cluster_dims__(kSmallCtas, 1, 1) __launch_bounds__(kSmallThrea
         if (r) atomicAdd(&acc0[1], r);
         if (p) atomicAdd(&acc0[2], p);
         if (sq) atomicAdd(&acc0[3], sq);
-        if (mx) atomicMax(&acc0[4], mx);
+        if (mx) atomicMax(max0, mx > 0xFFFFFFFFull ? 0xFFFFFFFFu : (unsigned)mx);
       }
     }
     cluster.sync();  // every push and counter of the iteration has landed
@@ -360,7 +363,7 @@ __global__ void __cluster_dims__(kSmallCtas, 1, 1) __launch_bounds__(kSmallThrea
           rec.work = (long long)s_acc[0];
           rec.relax = (long long)s_acc[1];
           rec.push = (long long)s_acc[2];
-          rec.work_max = (long long)s_acc[4];
+          rec.work_max = (long long)s_max;
           rec.work_sumsq = (double)s_acc[3];
           rec.k0 = s_t0;
           rec.k1 = gtime();
@@ -385,6 +388,7 @@ __global__ void __cluster_dims__(kSmallCtas, 1, 1) __launch_bounds__(kSmallThrea
             __stcg(&gctrl->wd_zero_next, 0u);
           }
           for (int k = 0; k < 5; ++k) s_acc[k] = 0;
+          s_max = 0;
           s_t0 = gtime();
         }
       }

@@ -1,0 +1,38 @@
+"""Small workload for compute-sanitizer (memcheck / racecheck / synccheck):
+every strategy x {bfs, sssp} x {host, graph loop} on small graphs with the
+corpus quirks, plus the grid-kernel and fused/dense WD variants, each checked
+against the oracle.
+
+    compute-sanitizer --tool memcheck python tools/sanitize_run.py
+"""
+import os
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+import numpy as np  # noqa: E402
+
+import paper_1711_00231_b200 as pkg  # noqa: E402
+from oracle import oracle  # noqa: E402
+from tests import graph_specs as gs  # noqa: E402
+
+oracle.build()
+graphs = [gs.build(pkg, gs.CORPUS[k]) for k in ("rmat10_skew", "quirks", "grid24", "degrees", "er_empty")]
+graphs.append(pkg.generate_rmat(13, 8, seed=2, max_weight=255))
+variants = [{}, {"GLB_NO_SMALL": "1"}, {"GLB_NO_SMALL": "1", "GLB_WD_FUSED": "1"},
+            {"GLB_NO_SMALL": "1", "GLB_WD_DENSE": "1"}]
+bad = 0
+for var in variants:
+    for k in ("GLB_NO_SMALL", "GLB_WD_FUSED", "GLB_WD_DENSE"):
+        os.environ.pop(k, None)
+    os.environ.update(var)
+    for g in graphs:
+        for algo in ("bfs", "sssp"):
+            exp = oracle.oracle_distances(g, 0, algo)
+            for tag in pkg.STRATEGY_TAGS:
+                for loop in ("host", "graph"):
+                    r = pkg.run_strategy(tag, g, 0, pkg.RelaxOp(algo), pkg.KernelConfig(loop=loop))
+                    if not np.array_equal(r.dist.array, exp):
+                        bad += 1
+                        print("MISMATCH", var, g.num_nodes, algo, tag, loop)
+print("sanitize workload done, mismatches:", bad)
