@@ -45,6 +45,7 @@ extern "C" {
 #define GLB_ENOMEM 5
 #define GLB_EOVERFLOW 6
 #define GLB_ENODEV 7
+#define GLB_EPARSE 8   /* malformed graph file: glb_last_error() is "<line>\t<message>", line -1 = whole file */
 
 /* strategy ids (STRATEGY_TAGS order, strategies/__init__.py:14) */
 #define GLB_BS 0
@@ -189,6 +190,18 @@ int glb_shard_local(glb_graph* g, int64_t* send_counts, void* send_buf,
 int glb_shard_apply(glb_graph* g, const void* recv_buf, int64_t nrecv);
 int glb_shard_advance(glb_graph* g, int64_t* frontier);
 int glb_shard_finish(glb_graph* g, int64_t* dist_owned, glb_run_stats* stats);
+
+/* ---- graph files (io.py) ---- */
+/* read_csr_bin (io.py:141-170) straight into HBM: the "CSRG" v1 cache is
+ * memory-mapped and streamed through glb_graph_create's narrowing upload. */
+int glb_graph_load_csrg(const char* path, int device, glb_graph** out);
+/* load_dimacs_gr (io.py:26-81, kind 0) / load_edge_list (io.py:84-122, kind 1
+ * unweighted, kind 2 weighted), grouped like CsrGraph.from_edges; the int64
+ * arrays (row n+1, col m, w m or NULL) are malloc'd by the library: release
+ * them with glb_free. */
+int glb_read_text_graph(const char* path, int kind, int64_t* n, int64_t* m, int* weighted,
+                        int64_t** row, int64_t** col, int64_t** w);
+void glb_free(void* p);
 
 /* ---- measurement ---- */
 /* Ceilings of the relaxation's memory pattern measured on this graph's own

@@ -8,7 +8,8 @@ kernels in libgraphlb_b200.so through a C-ABI (include/graphlb_b200.h).
 
 Not provided here (outside the hot path): the CPU launch emulation
 (launch_kernel, ThreadCtx, Worklist, atomic_relax_min), the sequential oracles
-(they live in oracle/ as test infrastructure), file loaders, reports and CLI.
+(they live in oracle/ as test infrastructure), reports and CLI.  The file
+loaders (io.py) are native and read the binary cache straight into HBM.
 """
 
 from .analysis import (
@@ -40,6 +41,7 @@ from .graph import (
     ring_graph,
     star_graph,
 )
+from .io import ParseError, load_dimacs_gr, load_edge_list, read_csr_bin, write_csr_bin
 from .runtime import INF, DistArray, KernelConfig, KernelLaunchError, MetricsRecord, resolve_threads
 from .strategies import (
     FALLBACK_TAG,

@@ -24,6 +24,7 @@ GLB_ECUDA = 4
 GLB_ENOMEM = 5
 GLB_EOVERFLOW = 6
 GLB_ENODEV = 7
+GLB_EPARSE = 8
 
 GLB_BS, GLB_EP, GLB_WD, GLB_NS, GLB_HP = range(5)
 GLB_TAG_WD_FALLBACK = 5
@@ -94,6 +95,12 @@ SIGNATURES = {
                                ctypes.POINTER(RunStats), ctypes.POINTER(Record), _i64]),
     "glb_run_records": (ctypes.c_int, [ctypes.c_void_p, _i64, ctypes.POINTER(Record), _i64,
                                        _p64]),
+    "glb_graph_load_csrg": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_int,
+                                           ctypes.POINTER(ctypes.c_void_p)]),
+    "glb_read_text_graph": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_int, _p64, _p64,
+                                           ctypes.POINTER(ctypes.c_int), ctypes.POINTER(_p64),
+                                           ctypes.POINTER(_p64), ctypes.POINTER(_p64)]),
+    "glb_free": (None, [ctypes.c_void_p]),
     "glb_measure_gather": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_double)]),
     "glb_degree_stats": (ctypes.c_int, [ctypes.c_void_p, _p64, _p64,
                                         ctypes.POINTER(ctypes.c_double)]),

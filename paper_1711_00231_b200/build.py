@@ -21,7 +21,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
          "-Xptxas", "-warn-spills", "-diag-suppress", "20054"]
 SOURCES = ["glb_memory.cu", "glb_graph.cu", "glb_driver.cu", "glb_gen.cu", "glb_peak.cu"]
-CXX_SOURCES = ["glb_host_simd.cpp"]
+CXX_SOURCES = ["glb_host_simd.cpp", "glb_io.cpp"]
 CXX = os.environ.get("CXX", "g++")
 EXTRA = os.environ.get("GLB_EXTRA_FLAGS", "").split()
 

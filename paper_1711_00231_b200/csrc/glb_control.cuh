@@ -135,7 +135,10 @@ __device__ __forceinline__ void ctl_set_conditionals(DevCtrl* c, cudaGraphCondit
 // Small-frontier steps that k_small_loop (glb_small.cuh) can run: BS / NS
 // node steps, WD steps, and HP's super-list WD-fallback.
 constexpr int kSmallItemsCtl = 8192;
-constexpr long long kSmallEdgesCtl = 16384;  // WD: active edges one cluster iteration takes
+#ifndef GLB_SMALL_EDGES
+#define GLB_SMALL_EDGES 16384
+#endif
+constexpr long long kSmallEdgesCtl = GLB_SMALL_EDGES;  // WD: active edges one cluster iteration takes
 __device__ __forceinline__ bool small_eligible(const DevCtrl* c) {
   if (!c->small_ok || c->done || c->shard_mode) return false;
   if (c->qcount[c->in] > (unsigned)kSmallItemsCtl) return false;

@@ -236,6 +236,9 @@ class Runner {
       hp_big_ = (HpBig*)ensure(ws.hp_big, ((size_t)g_->m / kHpCtaThreshold + 64) * sizeof(HpBig));
     }
     if (p_.strategy != GLB_EP)
+      if (kSmallCtas > 8)
+        GLB_CUDA_TRY(cudaFuncSetAttribute((const void*)k_small_loop<D, W>,
+                                          cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
       GLB_CUDA_TRY(cudaFuncSetAttribute((const void*)k_small_loop<D, W>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)small_smem_bytes<D>()));

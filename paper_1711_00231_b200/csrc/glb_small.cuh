@@ -35,7 +35,10 @@ namespace glb {
 
 namespace cg = cooperative_groups;
 
-constexpr int kSmallCtas = 8;                     // cluster size (portable maximum)
+#ifndef GLB_SMALL_CTAS
+#define GLB_SMALL_CTAS 8
+#endif
+constexpr int kSmallCtas = GLB_SMALL_CTAS;        // cluster size (8 = portable maximum, 16 opt-in)
 constexpr int kSmallThreads = 1024;               // threads per CTA
 constexpr int kSmallAll = kSmallCtas * kSmallThreads;
 constexpr int kSmallItems = kSmallItemsCtl;       // worklist nodes one iteration may hold
