@@ -160,7 +160,7 @@ __device__ __forceinline__ void ctl_reset_timers(DevCtrl* c) {
   c->t_relax.end = c->t_scan.end = 0;
   c->scan_ticket = c->relax_ticket = 0;
   c->hp_big_ctr = 0;
-  c->hp_big_done = c->hp_piece_next = 0;
+  c->hp_piece_next = 0;
 }
 
 // The host has written the static fields (qptr, strategy, mdt, thresholds,
@@ -223,7 +223,7 @@ __global__ void k_control(DevCtrl* c, cudaGraphConditionalHandle h_loop,
   }
   if (lane != 0) return;
   // this control kernel + the step's kernels (WD: scan + relax)
-  c->kernels += c->small_exit || c->done ? 2 : (c->mode == kModeWD ? 3 : 2);
+  c->kernels += c->small_exit || c->done ? 2 : (c->mode == kModeWD || c->mode == kModeHP ? 3 : 2);
   const unsigned long long wd_next = c->wd_next;
   const unsigned wd_zero = c->wd_zero_next;
   if (c->small_exit) {  // k_small_loop recorded and advanced its own iterations

@@ -374,6 +374,8 @@ class Runner {
   void launch_hp(unsigned grid) {
     k_hp_window<D, W><<<grid, kBlock, 0, s_>>>(row_, relaxer(), ctrl_);
     GLB_CHECK_LAUNCH();
+    k_hp_bigbin<D, W><<<cap_hp_, kBlock, 0, s_>>>(relaxer(), ctrl_);
+    GLB_CHECK_LAUNCH();
   }
   void launch_small() {
     k_small_loop<D, W><<<kSmallCtas, kSmallThreads, small_smem_bytes<D>(), s_>>>(

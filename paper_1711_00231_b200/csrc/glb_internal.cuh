@@ -180,7 +180,6 @@ struct DevCtrl {
   // ---- HP: windows >= kHpCtaThreshold edges form a grid-wide CTA bin
   struct HpBig* hp_big;         // bin entries of the current window step
   unsigned long long hp_big_ctr;  // (entries << 32) | pieces reserved, in one atomic
-  unsigned int hp_big_done;     // CTAs done producing (software grid barrier)
   unsigned int hp_piece_next;   // next piece ticket
   // ---- HP super-iteration state (hierarchical.py:54-136)
   int sup_in, sup_out, cur, spare;

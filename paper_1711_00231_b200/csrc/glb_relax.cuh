@@ -953,7 +953,6 @@ __global__ void __launch_bounds__(kBlock, GLB_RELAX_MINB) k_hp_window(const long
   __shared__ D s_dn;
   __shared__ int s_owner;
   __shared__ long long s_chunk;
-  __shared__ unsigned s_qb[kHpQbCache];  // first piece of every CTA-bin window
   const long long n = ctrl->qcount[ctrl->in];
   if (blockIdx.x * (long long)kBlock >= n) return;  // idle CTA
   timer_begin(ctrl->t_relax);
@@ -992,7 +991,7 @@ __global__ void __launch_bounds__(kBlock, GLB_RELAX_MINB) k_hp_window(const long
       }
     }
     // CTA granularity for long windows: into the grid-wide CTA bin, relaxed
-    // below in 2048-edge pieces by whichever CTAs are free
+    // in 2048-edge pieces by every CTA of the next launch (k_hp_bigbin)
     if (hi - lo >= kHpCtaThreshold) {
       const unsigned pieces = (unsigned)((hi - lo + kHpPiece - 1) / kHpPiece);
       const unsigned long long r =
@@ -1035,55 +1034,60 @@ __global__ void __launch_bounds__(kBlock, GLB_RELAX_MINB) k_hp_window(const long
     }
     bq_flush(bq, rx.qout, rx.nout);
   }
-  // ---- the CTA bin: a software grid barrier (every CTA is resident: the
-  //      grid is sized to the occupancy) publishes all long windows, then
-  //      every CTA claims 2048-edge pieces by ticket; a piece's window is found
-  //      by binary search over the windows' first pieces (cached in smem)
-  const long long producers = (n + kBlock - 1) / kBlock < gridDim.x ? (n + kBlock - 1) / kBlock
-                                                                    : (long long)gridDim.x;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    atomicAdd(&ctrl->hp_big_done, 1u);
-    while (*((volatile unsigned*)&ctrl->hp_big_done) < (unsigned)producers) {
-    }
-    __threadfence();
-  }
-  __syncthreads();
-  const unsigned long long bc = *((volatile unsigned long long*)&ctrl->hp_big_ctr);
+  flush_counters(ctrl->ls, c);
+  timer_end(ctrl->t_relax);
+}
+
+// The CTA bin of the window step: a second launch (so no CTA ever waits for
+// another to be scheduled) where every CTA claims 2048-edge pieces of the long
+// windows by ticket; a piece's window is found by binary search over the
+// windows' first pieces (cached in shared memory).
+template <typename D, bool W>
+__global__ void __launch_bounds__(kBlock, GLB_RELAX_MINB) k_hp_bigbin(Relaxer<D, W> rx0,
+                                                                      DevCtrl* ctrl) {
+  __shared__ uint32_t s_q[kQCap];
+  __shared__ BlockQ bq;
+  __shared__ long long s_lo, s_hi;
+  __shared__ D s_dn;
+  __shared__ int s_owner;
+  __shared__ unsigned s_qb[kHpQbCache];  // first piece of every CTA-bin window
+  const unsigned long long bc = ctrl->hp_big_ctr;
   const unsigned nbig = (unsigned)(bc >> 32), npieces = (unsigned)bc;
-  if (npieces) {
-    const bool cached = nbig <= (unsigned)kHpQbCache;
-    if (cached)
-      for (unsigned i = threadIdx.x; i < nbig; i += kBlock) s_qb[i] = ctrl->hp_big[i].qbase;
-    __syncthreads();
-    while (true) {
-      if (threadIdx.x == 0) {
-        s_owner = -1;
-        const unsigned t = atomicAdd(&ctrl->hp_piece_next, 1u);
-        if (t < npieces) {
-          unsigned lo_i = 0, hi_i = nbig;  // last window with qbase <= t
-          while (hi_i - lo_i > 1) {
-            const unsigned mid = (lo_i + hi_i) >> 1;
-            const unsigned qb = cached ? s_qb[mid] : ctrl->hp_big[mid].qbase;
-            if (qb <= t)
-              lo_i = mid;
-            else
-              hi_i = mid;
-          }
-          const HpBig b = ctrl->hp_big[lo_i];
-          const long long off = (long long)(t - b.qbase) * kHpPiece;
-          s_lo = b.lo + off;
-          s_hi = b.lo + off + kHpPiece < b.hi ? b.lo + off + kHpPiece : b.hi;
-          s_dn = (D)b.dn;
-          s_owner = 1;
+  if (npieces == 0 || blockIdx.x >= npieces) return;
+  timer_begin(ctrl->t_relax);
+  bq_init(bq, s_q);
+  const Relaxer<D, W> rx = bind(rx0, ctrl);
+  ThreadCounters c;
+  const bool cached = nbig <= (unsigned)kHpQbCache;
+  if (cached)
+    for (unsigned i = threadIdx.x; i < nbig; i += kBlock) s_qb[i] = ctrl->hp_big[i].qbase;
+  __syncthreads();
+  while (true) {
+    if (threadIdx.x == 0) {
+      s_owner = -1;
+      const unsigned t = atomicAdd(&ctrl->hp_piece_next, 1u);
+      if (t < npieces) {
+        unsigned lo_i = 0, hi_i = nbig;  // last window with qbase <= t
+        while (hi_i - lo_i > 1) {
+          const unsigned mid = (lo_i + hi_i) >> 1;
+          const unsigned qb = cached ? s_qb[mid] : ctrl->hp_big[mid].qbase;
+          if (qb <= t)
+            lo_i = mid;
+          else
+            hi_i = mid;
         }
+        const HpBig b = ctrl->hp_big[lo_i];
+        const long long off = (long long)(t - b.qbase) * kHpPiece;
+        s_lo = b.lo + off;
+        s_hi = b.lo + off + kHpPiece < b.hi ? b.lo + off + kHpPiece : b.hi;
+        s_dn = (D)b.dn;
+        s_owner = 1;
       }
-      __syncthreads();
-      if (s_owner < 0) break;
-      relax_range_coop<4>(rx, bq, s_lo, s_hi, s_dn, threadIdx.x, kBlock, c);
-      bq_flush(bq, rx.qout, rx.nout);
     }
+    __syncthreads();
+    if (s_owner < 0) break;
+    relax_range_coop<4>(rx, bq, s_lo, s_hi, s_dn, threadIdx.x, kBlock, c);
+    bq_flush(bq, rx.qout, rx.nout);
   }
   flush_counters(ctrl->ls, c);
   timer_end(ctrl->t_relax);
