@@ -217,11 +217,11 @@ class Runner {
         q_[i] = (i < 2 || p_.strategy == GLB_HP) ? (uint32_t*)ensure(ws.q[i], nb * 4) : q_[1];
     }
     if (p_.strategy == GLB_WD || p_.strategy == GLB_HP) {
-      items_[0] = (WdItem*)ensure(ws.c_pre, nb * sizeof(WdItem));
-      items_[1] = (WdItem*)ensure(ws.c_base, nb * sizeof(WdItem));
+      items_[0] = (WdItem*)ensure(ws.wd_items[0], nb * sizeof(WdItem));
+      items_[1] = (WdItem*)ensure(ws.wd_items[1], nb * sizeof(WdItem));
       const long long max_tiles = (g_->m + kWdTile - 1) / kWdTile + 2;
-      tile_first_[0] = (unsigned*)ensure(ws.tile_first, (size_t)max_tiles * 4);
-      tile_first_[1] = (unsigned*)ensure(ws.tile_node, (size_t)max_tiles * 4);
+      tile_first_[0] = (unsigned*)ensure(ws.wd_tiles[0], (size_t)max_tiles * 4);
+      tile_first_[1] = (unsigned*)ensure(ws.wd_tiles[1], (size_t)max_tiles * 4);
       const long long stiles = ((long long)nb + kWdScanTile - 1) / kWdScanTile + 1;
       unsigned* flags = (unsigned*)ensure_zero(ws.scan_flags, (size_t)stiles * 4 + 4096, s_);
       const size_t vb = (size_t)stiles * sizeof(Vec<2>);

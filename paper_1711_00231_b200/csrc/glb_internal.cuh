@@ -201,7 +201,7 @@ struct DevBuf {
 
 struct Workspace {
   DevBuf dist, stamp, q[4];
-  DevBuf c_pre, c_base, c_node, tile_first;  // WD compacted frontier
+  DevBuf wd_items[2], wd_tiles[2];           // WD item lists + tile_first (double-buffered)
   DevBuf scan_flags, scan_vals;              // decoupled look-back state
   DevBuf stats;                              // LaunchStats[kMaxLaunchSlots]
   DevBuf ctrl;                               // DevCtrl
@@ -287,29 +287,6 @@ inline unsigned int grid_for(long long items, int per_block, int cap) {
 // ------------------------------------------------------ device helpers ---
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
 
-// L2 eviction-priority hints (sm_80+ createpolicy): the distance cells are the
-// randomly re-read working set and should outlive the single-use col/weight
-// stream in the 126 MB L2.
-#ifndef GLB_STREAM_POLICY
-#define GLB_STREAM_POLICY 1
-#endif
-#ifndef GLB_L2_HINTS
-#define GLB_L2_HINTS 0  // measured slower on C2 (evict_last cells / evict_first streams)
-#endif
-__device__ __forceinline__ unsigned long long ld_cell(const unsigned long long* p) {
-#if GLB_L2_HINTS
-  unsigned long long r;
-  asm volatile(
-      "{\n\t.reg .b64 pol;\n\t"
-      "createpolicy.fractional.L2::evict_last.b64 pol, 1.0;\n\t"
-      "ld.global.L2::cache_hint.u64 %0, [%1], pol;\n\t}"
-      : "=l"(r)
-      : "l"(p));
-  return r;
-#else
-  return *p;
-#endif
-}
 // Single-use streams (col / weights): an L2 evict-first access policy, made
 // once per thread, so a pass over the 537 MB edge arrays does not push the
 // randomly re-read distance cells out of L2 (ncu: with plain or .cs loads
@@ -331,20 +308,6 @@ __device__ __forceinline__ uint32_t ld_stream_pol(const uint32_t* p, unsigned lo
 #else
   (void)pol;
   return __ldg(p);
-#endif
-}
-__device__ __forceinline__ uint32_t ld_stream(const uint32_t* p) {
-#if GLB_L2_HINTS
-  uint32_t r;
-  asm volatile(
-      "{\n\t.reg .b64 pol;\n\t"
-      "createpolicy.fractional.L2::evict_first.b64 pol, 1.0;\n\t"
-      "ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], pol;\n\t}"
-      : "=r"(r)
-      : "l"(p));
-  return r;
-#else
-  return __ldcs(p);
 #endif
 }
 

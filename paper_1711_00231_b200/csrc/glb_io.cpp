@@ -30,11 +30,6 @@ void set_error(const std::string& msg);  // glb_graph.cu: the glb_last_error() t
 
 namespace {
 
-struct ParseFail {
-  long long line;  // -1: whole file
-  std::string msg;
-};
-
 // Reference ParseError text: "<path>:<line>: <message>" (io.py:17-23); the
 // Python side rebuilds the exception from "<line>\t<message>".
 int fail(long long line, const std::string& msg) {

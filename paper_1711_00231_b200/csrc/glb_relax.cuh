@@ -123,7 +123,7 @@ struct Relaxer {
     asm("ld.global.L2::cache_hint.u64 %0, [%1], %2;" : "=l"(r) : "l"(cells + u), "l"(keep));
     return Cell<D>::dist(r);
 #else
-    return Cell<D>::dist(ld_cell(cells + u));
+    return Cell<D>::dist(cells[u]);
 #endif
   }
   // push claim after a strict decrease (first = packed-cell verdict)

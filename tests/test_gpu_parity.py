@@ -338,3 +338,17 @@ def test_sharded_virtual_ranks_match_reference(golden):
         for tag in sharded.SHARD_TAGS:
             d, _ = sharded.run_virtual(tag, shards, 0, pkg.RelaxOp(algo))
             assert np.array_equal(d, exp), (algo, tag)
+
+
+def test_high_diameter_grid_all_strategies(oracle):
+    """C3's shape at k=256 (511 BFS levels, ~530 SSSP iterations): long runs of
+    small frontiers through the cluster loop, alternating with grid steps."""
+    g = pkg.grid_graph(256, seed=1, max_weight=255)
+    for algo in ("bfs", "sssp"):
+        exp = oracle.oracle_distances(g, 0, algo)
+        for tag in TAGS:
+            for loop in ("host", "graph"):
+                r = pkg.run_strategy(tag, g, 0, pkg.RelaxOp(algo), pkg.KernelConfig(loop=loop))
+                assert np.array_equal(r.dist.array, exp), (algo, tag, loop)
+            r = pkg.run_strategy(tag, g, 1000, pkg.RelaxOp(algo), pkg.KernelConfig(loop="graph"))
+            assert np.array_equal(r.dist.array, oracle.oracle_distances(g, 1000, algo)), (algo, tag)
