@@ -155,13 +155,15 @@ class CudaShard:
                                               sg.parts, sg.rank), "glb_shard_begin")
 
     def local(self):
+        """Relax to the iteration boundary; returns (per-owner send counts, send
+        buffer, number of owned vertices already in the next frontier)."""
         counts = np.zeros(self.sg.parts, dtype=np.int64)
         nxt = ctypes.c_int64()
         _lib.check(_lib.lib().glb_shard_local(self.h, _lib.ptr64(counts),
                                               ctypes.c_void_p(self.send.data_ptr()),
                                               self.send.numel(), ctypes.byref(nxt)),
                    "glb_shard_local")
-        return counts, self.send
+        return counts, self.send, int(nxt.value)
 
     def apply(self, recv, n: int):
         if n:
@@ -195,14 +197,22 @@ class DistTransport:
         # gloo moves host tensors only: stage device buffers through the host
         self.host = dist.get_backend(group) == "gloo"
 
-    def exchange(self, counts: np.ndarray, send):
+    def exchange(self, counts: np.ndarray, send, work: int = 0):
+        """All-to-all of the owner buckets.  The count exchange also carries each
+        rank's pending work (next-frontier vertices it keeps + updates it sends),
+        so the caller learns the global total without a separate all-reduce."""
         torch, dist = self.torch, self.dist
         dev = torch.device("cpu") if self.host else send.device
-        c_send = torch.as_tensor(counts, dtype=torch.int64).to(dev)
+        c2 = np.empty((counts.shape[0], 2), dtype=np.int64)
+        c2[:, 0] = counts
+        c2[:, 1] = work
+        c_send = torch.as_tensor(c2).to(dev)
         c_recv = torch.empty_like(c_send)
         dist.all_to_all_single(c_recv, c_send, group=self.group)
+        c_host = c_recv.cpu()
+        self.global_work = int(c_host[:, 1].sum())
         in_split = [int(x) for x in counts]
-        out_split = [int(x) for x in c_recv.cpu()]
+        out_split = [int(x) for x in c_host[:, 0]]
         total_out = sum(out_split)
         recv = torch.empty(max(total_out, 1), dtype=torch.int64, device=dev)
         dist.all_to_all_single(recv[:total_out], send[:sum(in_split)].to(dev), out_split,
@@ -217,15 +227,19 @@ class DistTransport:
 
 
 def bsp_loop(shard, transport, device, max_iterations: int | None = None) -> int:
-    """One rank of the bulk-synchronous loop; returns the iteration count."""
+    """One rank of the bulk-synchronous loop; returns the iteration count.
+
+    Termination rides on the bucket-count exchange: when no rank keeps a
+    next-frontier vertex and none sends an update, every frontier is empty
+    after this iteration (one all-to-all per iteration, no all-reduce)."""
     it = 0
     while True:
-        counts, send = shard.local()
-        recv, n = transport.exchange(counts, send)
+        counts, send, keep = shard.local()
+        recv, n = transport.exchange(counts, send, keep + int(counts.sum()))
         shard.apply(recv, n)
-        front = shard.advance()
+        shard.advance()
         it += 1
-        if transport.allreduce_sum(front, device) == 0:
+        if transport.global_work == 0:
             return it
         if max_iterations is not None and it >= max_iterations:
             raise RuntimeError("sharded run did not converge")
@@ -257,7 +271,7 @@ def run_virtual(tag: str, shards: list[ShardGraph], source: int, op: RelaxOp,
     parts = len(shards)
     iters = 0
     while True:
-        outs = [r.local() for r in ranks]
+        outs = [r.local()[:2] for r in ranks]
         offs = []
         for me, (counts, _) in enumerate(outs):
             o, run = np.zeros(parts, dtype=np.int64), 0

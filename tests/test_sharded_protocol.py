@@ -57,7 +57,7 @@ class NumpyShard:
         self.out = keep
         counts = np.array([len(b) for b in buckets], dtype=np.int64)
         flat = [x for b in buckets for x in b]
-        return counts, torch.tensor(flat + [0], dtype=torch.int64)
+        return counts, torch.tensor(flat + [0], dtype=torch.int64), len(keep)
 
     def apply(self, recv, n):
         for x in recv[:n].tolist():
