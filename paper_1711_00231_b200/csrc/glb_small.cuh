@@ -181,8 +181,16 @@ __global__ void __cluster_dims__(kSmallCtas, 1, 1) __launch_bounds__(kSmallThrea
     typename IScan::TempStorage i;
   } s_scan;
   __shared__ DevCtrl sc;                 // this CTA's copy of the control block
-  __shared__ unsigned long long s_acc[5];  // CTA 0: the cluster's iteration counters
-  __shared__ unsigned int s_max;           // CTA 0: per-thread work maximum (32-bit: native atomicMax)
+  // CTA 0 holds the cluster's per-iteration cursors and counters in THREE
+  // rotating slots: iteration k uses slot k % 3, all CTAs read it after the
+  // one cluster barrier of iteration k, and rank 0 clears slot (k + 2) % 3
+  // (read by everybody before that barrier, next written after the next one)
+  // -- one barrier per iteration instead of two.
+  __shared__ unsigned int s_cur[3];            // out-list cursor
+  __shared__ unsigned long long s_acc[3][4];   // work, relax, push, work^2
+  __shared__ unsigned int s_max[3];            // per-thread work maximum (native 32-bit atomicMax)
+  __shared__ unsigned long long s_wdn[3];      // fused WD: (items << 32) | edges appended
+  __shared__ unsigned int s_wdz[3];            // fused WD: zero-degree pushes
   __shared__ long long s_total;
   __shared__ int s_go;
   __shared__ unsigned long long s_t0;
@@ -191,22 +199,31 @@ __global__ void __cluster_dims__(kSmallCtas, 1, 1) __launch_bounds__(kSmallThrea
   const unsigned rank = cluster.block_rank();
   const unsigned tid = threadIdx.x;
   const unsigned gt = rank * kSmallThreads + tid;
-  unsigned long long* acc0 = cluster.map_shared_rank(s_acc, 0);
-  unsigned int* max0 = cluster.map_shared_rank(&s_max, 0);
+  unsigned int* cur0 = cluster.map_shared_rank(s_cur, 0);
+  unsigned long long* acc0 = cluster.map_shared_rank(&s_acc[0][0], 0);
+  unsigned int* max0 = cluster.map_shared_rank(s_max, 0);
+  unsigned long long* wdn0 = cluster.map_shared_rank(s_wdn, 0);
+  unsigned int* wdz0 = cluster.map_shared_rank(s_wdz, 0);
 
   if (tid == 0) {
     sc = *gctrl;
     s_go = small_eligible(&sc);
     s_t0 = gtime();
   }
-  if (tid < 5) s_acc[tid] = 0;
-  if (tid == 0) s_max = 0;
+  if (tid < 3) {
+    s_cur[tid] = 0;
+    s_max[tid] = 0;
+    s_wdn[tid] = 0;
+    s_wdz[tid] = 0;
+    for (int k = 0; k < 4; ++k) s_acc[tid][k] = 0;
+  }
   cluster.sync();
-  while (s_go) {
+  for (unsigned it = 0; s_go; ++it) {
+    const unsigned slot = it % 3u;
     const unsigned n = sc.qcount[sc.in];
     const uint32_t* qin = sc.qptr[sc.in];
     uint32_t* qout = sc.qptr[sc.out];
-    unsigned* cursor = &gctrl->qcount[sc.out];  // zero at iteration start (see below)
+    unsigned* cursor = cur0 + slot;
     Relaxer<D, W> rx = rx0;
     rx.gen = sc.gen;
     ThreadCounters c;
@@ -217,8 +234,8 @@ __global__ void __cluster_dims__(kSmallCtas, 1, 1) __launch_bounds__(kSmallThrea
       push.row = row;
       push.out = reinterpret_cast<WdItem*>(sc.wd_items_buf[sc.wd_cur ^ 1]);
       push.tf = sc.wd_tf_buf[sc.wd_cur ^ 1];
-      push.next_ctr = &gctrl->wd_next;
-      push.zero_ctr = &gctrl->wd_zero_next;
+      push.next_ctr = wdn0 + slot;
+      push.zero_ctr = wdz0 + slot;
       fused = &push;
     }
     if (sc.mode == kModeWDF) {
@@ -340,11 +357,12 @@ __global__ void __cluster_dims__(kSmallCtas, 1, 1) __launch_bounds__(kSmallThrea
         mx = o > mx ? o : mx;
       }
       if (lane_id() == 0) {
-        if (w) atomicAdd(&acc0[0], w);
-        if (r) atomicAdd(&acc0[1], r);
-        if (p) atomicAdd(&acc0[2], p);
-        if (sq) atomicAdd(&acc0[3], sq);
-        if (mx) atomicMax(max0, mx > 0xFFFFFFFFull ? 0xFFFFFFFFu : (unsigned)mx);
+        unsigned long long* a = acc0 + slot * 4;
+        if (w) atomicAdd(&a[0], w);
+        if (r) atomicAdd(&a[1], r);
+        if (p) atomicAdd(&a[2], p);
+        if (sq) atomicAdd(&a[3], sq);
+        if (mx) atomicMax(max0 + slot, mx > 0xFFFFFFFFull ? 0xFFFFFFFFu : (unsigned)mx);
       }
     }
     cluster.sync();  // every push and counter of the iteration has landed
@@ -353,7 +371,7 @@ __global__ void __cluster_dims__(kSmallCtas, 1, 1) __launch_bounds__(kSmallThrea
       if (!ran) {
         s_go = 0;
       } else {
-        const unsigned produced = __ldcg(cursor);
+        const unsigned produced = *(volatile unsigned*)cursor;
         cc->qcount[cc->out] = produced;
         const bool wd_empty = (cc->mode == kModeWD || cc->mode == kModeWDF) && s_total == 0;
         if (rank == 0 && !wd_empty && cc->nrec < cc->rec_cap) {
@@ -363,11 +381,11 @@ __global__ void __cluster_dims__(kSmallCtas, 1, 1) __launch_bounds__(kSmallThrea
           rec.tag = cc->tag;
           rec.active = n;
           rec.threads = kSmallAll;
-          rec.work = (long long)s_acc[0];
-          rec.relax = (long long)s_acc[1];
-          rec.push = (long long)s_acc[2];
-          rec.work_max = (long long)s_max;
-          rec.work_sumsq = (double)s_acc[3];
+          rec.work = (long long)s_acc[slot][0];
+          rec.relax = (long long)s_acc[slot][1];
+          rec.push = (long long)s_acc[slot][2];
+          rec.work_max = (long long)s_max[slot];
+          rec.work_sumsq = (double)s_acc[slot][3];
           rec.k0 = s_t0;
           rec.k1 = gtime();
           rec.o0 = rec.o1 = 0;
@@ -378,26 +396,27 @@ __global__ void __cluster_dims__(kSmallCtas, 1, 1) __launch_bounds__(kSmallThrea
         } else if (wd_empty) {
           cc->done = 1;
         } else if (cc->wd_fused) {
-          ctl_wd_fused_advance(cc, __ldcg(&gctrl->wd_next), __ldcg(&gctrl->wd_zero_next));
+          ctl_wd_fused_advance(cc, *(volatile unsigned long long*)(wdn0 + slot),
+                               *(volatile unsigned*)(wdz0 + slot));
         } else {
           ctl_simple_advance(cc);
         }
         if (cc->done) cc->mode = kModeDone;
         s_go = small_eligible(cc);
-        if (rank == 0) {
-          if (s_go) {  // the next iteration's out cursors
-            __stcg(&gctrl->qcount[cc->out], 0u);
-            __stcg(&gctrl->wd_next, 0ull);
-            __stcg(&gctrl->wd_zero_next, 0u);
-          }
-          for (int k = 0; k < 5; ++k) s_acc[k] = 0;
-          s_max = 0;
+        if (rank == 0) {  // clear the slot of iteration it + 2 (see above)
+          const unsigned z = (it + 2u) % 3u;
+          s_cur[z] = 0;
+          s_max[z] = 0;
+          s_wdn[z] = 0;
+          s_wdz[z] = 0;
+          for (int k = 0; k < 4; ++k) s_acc[z][k] = 0;
           s_t0 = gtime();
         }
       }
     }
-    cluster.sync();  // transitions agree; the next out cursor is zero
+    __syncthreads();  // this CTA's threads see the transition (identical in every CTA)
   }
+  cluster.sync();  // no CTA leaves while others may still read its shared memory
   if (rank == 0 && tid == 0) {
     sc.overflow |= __ldcg(&gctrl->overflow);  // make_cand's flag lives in the global block
     sc.small_exit = 1;
