@@ -35,6 +35,25 @@ __device__ __forceinline__ void ctl_simple_advance(DevCtrl* c) {
   c->done = produced == 0;
 }
 
+__device__ __forceinline__ void hp_end_super(DevCtrl* c);
+__device__ __forceinline__ void hp_decide_sub(DevCtrl* c);
+
+// HP after a step (hierarchical.py:54-136): a WD-fallback step finishes the
+// super-iteration; a window sub-iteration hands its unfinished nodes to the
+// next sublist.
+__device__ __forceinline__ void ctl_hp_after_step(DevCtrl* c) {
+  if (c->mode == kModeWD) {
+    if (c->in != c->sup_in) c->qcount[c->in] = 0;
+    hp_end_super(c);
+  } else {
+    if (c->cur != c->sup_in) c->qcount[c->cur] = 0;
+    c->cur = c->spare;
+    c->spare = c->cur == 2 ? 3 : 2;
+    c->s += 1;
+    hp_decide_sub(c);
+  }
+}
+
 // WD with fused pushes: the next step's item list is the one just appended
 // (run_wd's loop, workload.py:175-189; it ends when the list has no edges,
 // workload.py:181-183).
@@ -139,6 +158,7 @@ constexpr int kSmallItemsCtl = 8192;
 #define GLB_SMALL_EDGES 16384
 #endif
 constexpr long long kSmallEdgesCtl = GLB_SMALL_EDGES;  // WD: active edges one cluster iteration takes
+constexpr long long kSmallMaxWindow = 64;   // HP: thread-per-node windows the cluster walks
 __device__ __forceinline__ bool small_eligible(const DevCtrl* c) {
   if (!c->small_ok || c->done || c->shard_mode) return false;
   if (c->qcount[c->in] > (unsigned)kSmallItemsCtl) return false;
@@ -148,8 +168,8 @@ __device__ __forceinline__ bool small_eligible(const DevCtrl* c) {
       return c->mode == kModeRelax;
     case GLB_WD:
       return c->mode == kModeWD || (c->mode == kModeWDF && c->wd_total <= kSmallEdgesCtl);
-    case GLB_HP:
-      return c->mode == kModeWD && c->sub < 0 && c->window == 0;
+    case GLB_HP:  // WD-fallback steps, and window sub-iterations of short windows
+      return c->mode == kModeWD || (c->mode == kModeHP && c->mdt <= kSmallMaxWindow);
     default:
       return false;
   }
@@ -270,16 +290,7 @@ __global__ void k_control(DevCtrl* c, cudaGraphConditionalHandle h_loop,
       }
       break;
     case GLB_HP:
-      if (c->mode == kModeWD) {
-        if (c->in != c->sup_in) c->qcount[c->in] = 0;
-        hp_end_super(c);
-      } else {  // window sub-iteration: unfinished nodes form the next sublist
-        if (c->cur != c->sup_in) c->qcount[c->cur] = 0;
-        c->cur = c->spare;
-        c->spare = c->cur == 2 ? 3 : 2;
-        c->s += 1;
-        hp_decide_sub(c);
-      }
+      ctl_hp_after_step(c);
       break;
     default:
       if (!ctl_pause(c)) ctl_simple_advance(c);

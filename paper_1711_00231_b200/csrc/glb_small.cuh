@@ -187,6 +187,7 @@ __global__ void __cluster_dims__(kSmallCtas, 1, 1) __launch_bounds__(kSmallThrea
   // (read by everybody before that barrier, next written after the next one)
   // -- one barrier per iteration instead of two.
   __shared__ unsigned int s_cur[3];            // out-list cursor
+  __shared__ unsigned int s_nxt[3];            // HP: next-sublist cursor (unfinished windows)
   __shared__ unsigned long long s_acc[3][4];   // work, relax, push, work^2
   __shared__ unsigned int s_max[3];            // per-thread work maximum (native 32-bit atomicMax)
   __shared__ unsigned long long s_wdn[3];      // fused WD: (items << 32) | edges appended
@@ -200,6 +201,7 @@ __global__ void __cluster_dims__(kSmallCtas, 1, 1) __launch_bounds__(kSmallThrea
   const unsigned tid = threadIdx.x;
   const unsigned gt = rank * kSmallThreads + tid;
   unsigned int* cur0 = cluster.map_shared_rank(s_cur, 0);
+  unsigned int* nxt0 = cluster.map_shared_rank(s_nxt, 0);
   unsigned long long* acc0 = cluster.map_shared_rank(&s_acc[0][0], 0);
   unsigned int* max0 = cluster.map_shared_rank(s_max, 0);
   unsigned long long* wdn0 = cluster.map_shared_rank(s_wdn, 0);
@@ -212,6 +214,7 @@ __global__ void __cluster_dims__(kSmallCtas, 1, 1) __launch_bounds__(kSmallThrea
   }
   if (tid < 3) {
     s_cur[tid] = 0;
+    s_nxt[tid] = 0;
     s_max[tid] = 0;
     s_wdn[tid] = 0;
     s_wdz[tid] = 0;
@@ -222,7 +225,9 @@ __global__ void __cluster_dims__(kSmallCtas, 1, 1) __launch_bounds__(kSmallThrea
     const unsigned slot = it % 3u;
     const unsigned n = sc.qcount[sc.in];
     const uint32_t* qin = sc.qptr[sc.in];
-    uint32_t* qout = sc.qptr[sc.out];
+    // appends go after what the out list already holds (HP's super-out list
+    // accumulates over the sub-iterations of a super-iteration)
+    uint32_t* qout = sc.qptr[sc.out] + sc.qcount[sc.out];
     unsigned* cursor = cur0 + slot;
     Relaxer<D, W> rx = rx0;
     rx.gen = sc.gen;
@@ -303,6 +308,41 @@ __global__ void __cluster_dims__(kSmallCtas, 1, 1) __launch_bounds__(kSmallThrea
         wd_tiles<D, W>(rx, cursor, qout, s_pre, s_base, s_dn, tot_i, (uint32_t)tot_e, gt, c,
                        fused);
       }
+    } else if (sc.mode == kModeHP) {
+      // ---- HP window sub-iteration (hierarchical.py:95-120): thread per
+      //      sublist node relaxes [s*mdt, (s+1)*mdt) of its edges; nodes with
+      //      edges left carry into the next sublist
+      uint32_t* qnext = sc.qptr[sc.next] + sc.qcount[sc.next];
+      unsigned* ncur = nxt0 + slot;
+      const long long window = sc.window, mdt = sc.mdt;
+      for (unsigned i = gt; i < n; i += kSmallAll) {
+        const uint32_t u = __ldcg(qin + i);
+        const long long r0 = row[u], r1 = row[u + 1];
+        const long long start = r0 + window;
+        if (start >= r1) continue;
+        const long long end = start + mdt < r1 ? start + mdt : r1;
+        if (end < r1) {
+          g_append(qnext, ncur, u);
+          ++c.push;
+        }
+        const D du = dist_cg<D>(rx.cells, u);
+        if (du == DistTraits<D>::kInf) continue;
+        constexpr int K = 4;
+        for (uint32_t b = (uint32_t)start; b < (uint32_t)end; b += K) {
+          uint32_t e[K];
+          D d[K];
+          unsigned valid = 0;
+#pragma unroll
+          for (int k = 0; k < K; ++k) {
+            e[k] = b + k;
+            d[k] = du;
+            if (b + k < (uint32_t)end) valid |= 1u << k;
+          }
+          uint32_t v[K];
+          D cand[K];
+          small_relax<K>(rx, cursor, qout, e, d, valid, c, v, cand);
+        }
+      }
     } else {
       // ---- BS / NS: thread per worklist node (node i -> cluster thread i mod 8192)
       for (unsigned i = gt; i < n; i += kSmallAll) {
@@ -372,7 +412,8 @@ __global__ void __cluster_dims__(kSmallCtas, 1, 1) __launch_bounds__(kSmallThrea
         s_go = 0;
       } else {
         const unsigned produced = *(volatile unsigned*)cursor;
-        cc->qcount[cc->out] = produced;
+        cc->qcount[cc->out] += produced;
+        if (cc->mode == kModeHP) cc->qcount[cc->next] += *(volatile unsigned*)(nxt0 + slot);
         const bool wd_empty = (cc->mode == kModeWD || cc->mode == kModeWDF) && s_total == 0;
         if (rank == 0 && !wd_empty && cc->nrec < cc->rec_cap) {
           DevRecord& rec = cc->recs[cc->nrec];
@@ -391,8 +432,8 @@ __global__ void __cluster_dims__(kSmallCtas, 1, 1) __launch_bounds__(kSmallThrea
           rec.o0 = rec.o1 = 0;
         }
         if (!wd_empty) cc->nrec += 1;
-        if (cc->strategy == GLB_HP) {  // super-list fallback done (hierarchical.py:134-137)
-          hp_end_super(cc);
+        if (cc->strategy == GLB_HP) {  // hierarchical.py:54-136
+          ctl_hp_after_step(cc);
         } else if (wd_empty) {
           cc->done = 1;
         } else if (cc->wd_fused) {
@@ -406,6 +447,7 @@ __global__ void __cluster_dims__(kSmallCtas, 1, 1) __launch_bounds__(kSmallThrea
         if (rank == 0) {  // clear the slot of iteration it + 2 (see above)
           const unsigned z = (it + 2u) % 3u;
           s_cur[z] = 0;
+          s_nxt[z] = 0;
           s_max[z] = 0;
           s_wdn[z] = 0;
           s_wdz[z] = 0;
