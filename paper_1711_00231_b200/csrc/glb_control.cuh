@@ -159,12 +159,15 @@ constexpr int kSmallItemsCtl = 8192;
 #endif
 constexpr long long kSmallEdgesCtl = GLB_SMALL_EDGES;  // WD: active edges one cluster iteration takes
 constexpr long long kSmallMaxWindow = 64;   // HP: thread-per-node windows the cluster walks
+constexpr unsigned kSmallListCtl = 32768;    // BS / NS / EP / HP-window worklists (no item table)
 __device__ __forceinline__ bool small_eligible(const DevCtrl* c) {
   if (!c->small_ok || c->done || c->shard_mode) return false;
-  if (c->qcount[c->in] > (unsigned)kSmallItemsCtl) return false;
+  const bool table = c->mode == kModeWD || c->mode == kModeWDF;  // WD builds an smem item table
+  if (c->qcount[c->in] > (table ? (unsigned)kSmallItemsCtl : kSmallListCtl)) return false;
   switch (c->strategy) {
     case GLB_BS:
     case GLB_NS:
+    case GLB_EP:
       return c->mode == kModeRelax;
     case GLB_WD:
       return c->mode == kModeWD || (c->mode == kModeWDF && c->wd_total <= kSmallEdgesCtl);

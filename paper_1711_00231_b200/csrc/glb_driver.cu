@@ -235,13 +235,12 @@ class Runner {
       // CTA-bin entries: every long window holds >= kHpCtaThreshold edges
       hp_big_ = (HpBig*)ensure(ws.hp_big, ((size_t)g_->m / kHpCtaThreshold + 64) * sizeof(HpBig));
     }
-    if (p_.strategy != GLB_EP)
-      if (kSmallCtas > 8)
-        GLB_CUDA_TRY(cudaFuncSetAttribute((const void*)k_small_loop<D, W>,
-                                          cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    if (kSmallCtas > 8)
       GLB_CUDA_TRY(cudaFuncSetAttribute((const void*)k_small_loop<D, W>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)small_smem_bytes<D>()));
+                                        cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    GLB_CUDA_TRY(cudaFuncSetAttribute((const void*)k_small_loop<D, W>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)small_smem_bytes<D>()));
     if (relax_kernel()) cap_relax_ = std::max(cap(relax_kernel()), g_->num_sms);
     pin_cells_in_l2(nb * 8);
     ctrl_ = (DevCtrl*)ensure(ws.ctrl, sizeof(DevCtrl));
@@ -264,7 +263,7 @@ class Runner {
     c.scan_epoch = g_->scan_epoch + 1;
     c.rec_cap = kMaxRecords;
     c.shard_mode = shard_mode_ ? 1 : 0;
-    c.small_ok = !shard_mode_ && p_.strategy != GLB_EP && !getenv("GLB_NO_SMALL") ? 1 : 0;
+    c.small_ok = !shard_mode_ && !getenv("GLB_NO_SMALL") ? 1 : 0;
     for (int i = 0; i < 2; ++i) {
       c.wd_items_buf[i] = items_[i];
       c.wd_tf_buf[i] = tile_first_[i];
@@ -379,7 +378,8 @@ class Runner {
   }
   void launch_small() {
     k_small_loop<D, W><<<kSmallCtas, kSmallThreads, small_smem_bytes<D>(), s_>>>(
-        row_, p_.strategy == GLB_NS ? cs_ : nullptr, g_->n, relaxer(), ctrl_);
+        row_, p_.strategy == GLB_NS ? cs_ : nullptr, g_->n,
+        p_.strategy == GLB_EP ? src_ : nullptr, p_.chunked != 0, relaxer(), ctrl_);
     GLB_CHECK_LAUNCH();
   }
   void launch_control(cudaGraphConditionalHandle hl, cudaGraphConditionalHandle hm, int gm) {
@@ -558,11 +558,9 @@ class Runner {
         launch_relax(cap_relax_);
         end_capture();
       }
-      if (p_.strategy != GLB_EP) {
-        capture_into(sp.conditional.phGraph_out[kModeSmall], nullptr, 0);
-        launch_small();
-        end_capture();
-      }
+      capture_into(sp.conditional.phGraph_out[kModeSmall], nullptr, 0);
+      launch_small();
+      end_capture();
       capture_into(body, &snode, 1);
       launch_control(h_loop, h_mode, 1);
       end_capture();

@@ -169,7 +169,8 @@ __device__ __forceinline__ void wd_tiles(const Relaxer<D, W>& rx, unsigned* curs
 template <typename D, bool W>
 __global__ void __cluster_dims__(kSmallCtas, 1, 1) __launch_bounds__(kSmallThreads, 1)
     k_small_loop(const long long* __restrict__ row, const long long* __restrict__ cs,
-                 long long n_orig, Relaxer<D, W> rx0, DevCtrl* gctrl) {
+                 long long n_orig, const uint32_t* __restrict__ ep_src, bool ep_chunked,
+                 Relaxer<D, W> rx0, DevCtrl* gctrl) {
   extern __shared__ __align__(16) unsigned char s_dyn[];
   D* s_dn = reinterpret_cast<D*>(s_dyn);                                   // [kSmallItems]
   uint32_t* s_pre = reinterpret_cast<uint32_t*>(s_dyn + kSmallItems * sizeof(D));  // [+1]
@@ -341,6 +342,40 @@ __global__ void __cluster_dims__(kSmallCtas, 1, 1) __launch_bounds__(kSmallThrea
           uint32_t v[K];
           D cand[K];
           small_relax<K>(rx, cursor, qout, e, d, valid, c, v, cand);
+        }
+      }
+    } else if (ep_src) {
+      // ---- EP (edge_based.py:70-87): thread per worklist edge; an improved
+      //      destination appends its whole out-edge range with one
+      //      reservation (work chunking) or one per edge
+      for (unsigned i = gt; i < n; i += kSmallAll) {
+        const uint32_t e = __ldcg(qin + i);
+        const uint32_t u = __ldg(ep_src + e);
+        const uint32_t v = __ldg(rx.col + e);
+        const uint32_t w = W ? __ldg(rx.wt + e) : 1u;
+        ++c.work;
+        const D du = dist_cg<D>(rx.cells, u);
+        if (du == DistTraits<D>::kInf) continue;
+        ++c.relax;
+        D cand;
+        if (!make_cand<D>(du, w, cand, rx.ovf) || cand >= dist_cg<D>(rx.cells, v)) continue;
+        const unsigned long long old = atomicMin(rx.cells + v, Cell<D>::make(cand, rx.gen));
+        if (cand >= Cell<D>::dist(old)) continue;
+        const bool first = Cell<D>::kPacked ? Cell<D>::gen(old) != rx.gen
+                                            : atomicExch(rx.stamp + v, rx.gen) != rx.gen;
+        if (!first) continue;
+        const long long lo = row[v];
+        const unsigned len = (unsigned)(row[v + 1] - lo);
+        if (len == 0) continue;
+        if (ep_chunked) {
+          ++c.push;
+          const unsigned b = atomicAdd(cursor, len);
+          for (unsigned j = 0; j < len; ++j) qout[b + j] = (uint32_t)(lo + j);
+        } else {
+          for (unsigned j = 0; j < len; ++j) {
+            ++c.push;
+            qout[atomicAdd(cursor, 1u)] = (uint32_t)(lo + j);
+          }
         }
       }
     } else {
