@@ -77,7 +77,7 @@ typedef struct glb_run_params {
   int32_t block_size;      /* KernelConfig.block_size: HP fallback threshold (hierarchical.py:49) */
   int32_t hp_fallback;     /* run_hp(fallback=...) */
   int64_t virtual_threads; /* KernelConfig.virtual_threads (0 = auto); reported only */
-  int32_t dist_bits;       /* 0 = auto (u32, re-run in u64 on overflow), 32, 64 */
+  int32_t dist_bits;       /* 0 = auto (24 -> 32 -> 64 on overflow), 24, 32, 64 */
   int32_t loop_mode;       /* GLB_LOOP_HOST / GLB_LOOP_GRAPH */
   int32_t record_timing;   /* per-launch CUDA event timing into records */
   int32_t reserved;

@@ -38,6 +38,19 @@ __device__ __forceinline__ void ctl_simple_advance(DevCtrl* c) {
 __device__ __forceinline__ void hp_end_super(DevCtrl* c);
 __device__ __forceinline__ void hp_decide_sub(DevCtrl* c);
 
+// 24-bit tier: before every generation g with g % 128 == 0 starts, all
+// tags are reset to 0 (k_renorm) -- Cell<dist24_t>'s tag (g % 128) + 1 then
+// grows monotonically through the next 128 generations.  The interrupted
+// step resumes after it.
+__device__ __forceinline__ void ctl_check_renorm(DevCtrl* c) {
+  if (c->tag_bits == 8 && !c->done && (c->gen & 127u) == 0 && c->mode != kModeRenorm &&
+      c->renorm_gen != c->gen) {  // once per generation (HP sub-iterations share one)
+    c->saved_mode = c->mode;
+    c->mode = kModeRenorm;
+    c->renorm_gen = c->gen;
+  }
+}
+
 // HP after a step (hierarchical.py:54-136): a WD-fallback step finishes the
 // super-iteration; a window sub-iteration hands its unfinished nodes to the
 // next sublist.
@@ -134,7 +147,8 @@ __device__ __forceinline__ void hp_decide_sub(DevCtrl* c) {
 // cells in id order (packed cells only: the generation marks the worklist).
 constexpr long long kDenseDiv = 8;
 __device__ __forceinline__ void ctl_choose_dense(DevCtrl* c) {
-  c->wd_dense = c->dense_ok && c->strategy == GLB_WD && c->mode == kModeWD && !c->use_small &&
+  c->wd_dense = c->dense_ok && c->tag_bits == 32 && c->strategy == GLB_WD && c->mode == kModeWD &&
+                !c->use_small &&
                 (long long)c->qcount[c->in] * kDenseDiv >= c->n_nodes;
 }
 
@@ -223,6 +237,7 @@ __global__ void k_control_init(DevCtrl* c, cudaGraphConditionalHandle h_loop,
   if (c->done) c->mode = kModeDone;
   c->small_exit = 0;
   c->kernels = 1;
+  ctl_check_renorm(c);
   c->use_small = small_eligible(c);
   ctl_set_conditionals(c, h_loop, h_mode, graph_mode);
 }
@@ -252,6 +267,13 @@ __global__ void k_control(DevCtrl* c, cudaGraphConditionalHandle h_loop,
   if (c->small_exit) {  // k_small_loop recorded and advanced its own iterations
     c->small_exit = 0;
     c->use_small = 0;
+    ctl_choose_dense(c);
+    ctl_set_conditionals(c, h_loop, h_mode, graph_mode);
+    return;
+  }
+  if (c->mode == kModeRenorm) {  // cells retagged: resume the interrupted step
+    c->mode = c->saved_mode;
+    c->use_small = small_eligible(c);
     ctl_choose_dense(c);
     ctl_set_conditionals(c, h_loop, h_mode, graph_mode);
     return;
@@ -300,6 +322,7 @@ __global__ void k_control(DevCtrl* c, cudaGraphConditionalHandle h_loop,
       break;
   }
   if (c->done && !c->paused) c->mode = kModeDone;
+  ctl_check_renorm(c);
   c->use_small = small_eligible(c);
   ctl_choose_dense(c);
   ctl_set_conditionals(c, h_loop, h_mode, graph_mode);

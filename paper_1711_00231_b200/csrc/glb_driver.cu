@@ -116,8 +116,8 @@ class Runner {
     void* out = ensure(g_->ws.out64, (size_t)std::max<long long>(cnt, 1) * (kNarrow ? 4 : 8));
     if (cnt && dist_out) {
       if (kNarrow)
-        k_dist_u32<<<grid_for(cnt, kBlock, g_->num_sms * 8), kBlock, 0, s_>>>(cells_ + lo, cnt,
-                                                                              (uint32_t*)out);
+        k_dist_u32<D><<<grid_for(cnt, kBlock, g_->num_sms * 8), kBlock, 0, s_>>>(
+            cells_ + lo, cnt, (uint32_t*)out);
       else
         k_dist_out<D><<<grid_for(cnt, kBlock, g_->num_sms * 8), kBlock, 0, s_>>>(
             cells_ + lo, cnt, (long long*)out);
@@ -152,7 +152,7 @@ class Runner {
   const uint32_t* wt_ = nullptr;
   const long long* cs_ = nullptr;
   uint32_t* src_ = nullptr;
-  unsigned long long* cells_ = nullptr;
+  CellS<D>* cells_ = nullptr;
   uint32_t* stamp_ = nullptr;
   uint32_t* q_[4] = {nullptr, nullptr, nullptr, nullptr};
   DevCtrl* ctrl_ = nullptr;
@@ -201,7 +201,7 @@ class Runner {
   void alloc_state() {
     Workspace& ws = g_->ws;
     const size_t nb = (size_t)std::max<long long>(n_all_, 1);
-    cells_ = (unsigned long long*)ensure(ws.dist, nb * 8);
+    cells_ = (CellS<D>*)ensure(ws.dist, nb * sizeof(CellS<D>));
     stamp_ = (uint32_t*)ensure_zero(ws.stamp, nb * 4, s_);
     if (g_->stamp_epoch > 0xF0000000u) {
       GLB_CUDA_TRY(cudaMemsetAsync(stamp_, 0, ws.stamp.bytes, s_));
@@ -242,7 +242,7 @@ class Runner {
                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)small_smem_bytes<D>()));
     if (relax_kernel()) cap_relax_ = std::max(cap(relax_kernel()), g_->num_sms);
-    pin_cells_in_l2(nb * 8);
+    pin_cells_in_l2(nb * sizeof(CellS<D>));
     ctrl_ = (DevCtrl*)ensure(ws.ctrl, sizeof(DevCtrl));
     ls_ = (LaunchStats*)ensure_zero(ws.stats, sizeof(LaunchStats), s_);
     drecs_ = (DevRecord*)ensure(ws.recs, sizeof(DevRecord) * kMaxRecords);
@@ -260,6 +260,8 @@ class Runner {
         (long long)(p_.strategy == GLB_WD || p_.strategy == GLB_HP ? cap_wd_ : cap_relax_) * kBlock;
     c.hp_threads = (long long)cap_hp_ * kBlock;
     c.gen = g_->stamp_epoch;
+    c.tag_bits = Cell<D>::kGenBits;
+    c.renorm_gen = 0xFFFFFFFFu;
     c.scan_epoch = g_->scan_epoch + 1;
     c.rec_cap = kMaxRecords;
     c.shard_mode = shard_mode_ ? 1 : 0;
@@ -276,7 +278,7 @@ class Runner {
     // Dense-frontier scans (cells in id order) speed the relax kernel up per
     // edge but the id-ordered processing does ~10 % more re-relaxation on C2,
     // a wash overall, so they are opt-in.
-    c.dense_ok = p_.strategy == GLB_WD && !shard_mode_ && Cell<D>::kPacked &&
+    c.dense_ok = p_.strategy == GLB_WD && !shard_mode_ && Cell<D>::kGenBits == 32 &&
                  getenv("GLB_WD_DENSE") ? 1 : 0;
     c.wd_fused = p_.strategy == GLB_WD && !shard_mode_ && getenv("GLB_WD_FUSED") ? 1 : 0;
     c.recs = drecs_;
@@ -345,6 +347,16 @@ class Runner {
   }
 
   // ------------------------------------------------------ step launches ---
+  // 24-bit tier: retag every cell (see ctl_check_renorm)
+  void launch_renorm() {
+    if constexpr (Cell<D>::kGenBits == 8) {
+      k_renorm<<<grid_for(n_all_, kBlock, g_->num_sms * 8), kBlock, 0, s_>>>(cells_, n_all_);
+      GLB_CHECK_LAUNCH();
+    } else {
+      throw Error{GLB_ECUDA, "renormalisation requested for a 32-bit-tag run"};
+    }
+  }
+
   void launch_relax(unsigned grid) {
     const Relaxer<D, W> rx = relaxer();
     switch (p_.strategy) {
@@ -452,6 +464,9 @@ class Runner {
           ev.threads = (long long)cap_wd_ * kBlock;
           break;
         }
+        case kModeRenorm:
+          launch_renorm();
+          break;
         case kModeHP: {
           const unsigned grid = grid_for(n_in, kBlock, cap_hp_);
           ev.threads = (long long)grid * kBlock;
@@ -477,7 +492,7 @@ class Runner {
   // ----------------------------------------------------- graph loop ---
   std::string graph_key() const {
     std::ostringstream k;
-    k << g_->device << '|' << p_.strategy << '|' << sizeof(D) << '|' << W << '|' << p_.chunked << '|' << cap_relax_
+    k << g_->device << '|' << p_.strategy << '|' << Cell<D>::kDistBits << '|' << W << '|' << p_.chunked << '|' << cap_relax_
       << '|' << cap_scan_ << '|' << cap_wd_ << '|' << cap_hp_ << '|' << (const void*)row_ << '|'
       << (const void*)col_ << '|' << (const void*)wt_ << '|' << (const void*)cs_ << '|'
       << (const void*)src_ << '|' << (const void*)cells_ << '|' << (const void*)stamp_ << '|'
@@ -561,6 +576,11 @@ class Runner {
       capture_into(sp.conditional.phGraph_out[kModeSmall], nullptr, 0);
       launch_small();
       end_capture();
+      if (Cell<D>::kGenBits == 8) {
+        capture_into(sp.conditional.phGraph_out[kModeRenorm], nullptr, 0);
+        launch_renorm();
+        end_capture();
+      }
       capture_into(body, &snode, 1);
       launch_control(h_loop, h_mode, 1);
       end_capture();
@@ -646,7 +666,7 @@ class Runner {
 
   void finish(glb_run_stats* st, float dev_ms) {
     st->status = GLB_OK;
-    st->dist_bits = (int)(sizeof(D) * 8);
+    st->dist_bits = Cell<D>::kDistBits;
     st->iterations = h_->ctrl.iteration;
     st->launches = (int64_t)recs_.size();
     st->mdt = mdt_;
@@ -881,27 +901,37 @@ void run(glb_graph* g, const glb_run_params& p, int64_t* dist_out, glb_run_stats
          std::vector<glb_record>& recs) {
   std::memset(st, 0, sizeof(*st));
   st->split_fraction = -1.0;
-  if (p.dist_bits == 64) {
+  // Tiers (dist_bits 0): 24-bit distances in u32 cells, then 32-bit in
+  // packed u64 cells, then 64-bit; a tier that overflows re-runs at the next
+  // one.  The handle remembers a 24-bit overflow per relaxation kind so
+  // later runs on the same graph start at 32 bits.  The 24-bit tier is only
+  // the first choice when the u64 cells are over twice the L2: with 8 cells
+  // per 32-byte sector instead of 4, the relax kernels lose more to L2
+  // sector contention between cell gathers and atomics than they gain from
+  // the smaller array while either array mostly fits (C2 / C4 SSSP WD
+  // +13..15 %, C3 mixed within +-8 %).
+  const bool huge = g->n * 8LL > 2LL * g->l2_bytes;
+  const int first = p.dist_bits ? p.dist_bits
+                                : (!g->narrow_overflow[p.algo == GLB_SSSP] && huge ? 24 : 32);
+  for (int bits = first;; bits = bits == 24 ? 32 : 64) {
     try {
-      run_guarded<unsigned long long>(g, p, dist_out, st, recs);
+      if (bits == 24)
+        run_guarded<dist24_t>(g, p, dist_out, st, recs);
+      else if (bits == 32)
+        run_guarded<uint32_t>(g, p, dist_out, st, recs);
+      else
+        run_guarded<unsigned long long>(g, p, dist_out, st, recs);
+      return;
     } catch (const OverflowRestart&) {
-      throw Error{GLB_EOVERFLOW, "distance exceeds the 63-bit range"};
-    }
-    return;
-  }
-  try {
-    run_guarded<uint32_t>(g, p, dist_out, st, recs);
-  } catch (const OverflowRestart&) {
-    if (p.dist_bits == 32) throw Error{GLB_EOVERFLOW, "distance exceeds the 32-bit range"};
-    recs.clear();
-    const double sf = st->split_fraction;
-    std::memset(st, 0, sizeof(*st));
-    st->split_fraction = sf;
-    GLB_CUDA_TRY(cudaStreamSynchronize(g->stream));
-    try {
-      run_guarded<unsigned long long>(g, p, dist_out, st, recs);
-    } catch (const OverflowRestart&) {
-      throw Error{GLB_EOVERFLOW, "distance exceeds the 63-bit range"};
+      if (bits == 64) throw Error{GLB_EOVERFLOW, "distance exceeds the 63-bit range"};
+      if (p.dist_bits)
+        throw Error{GLB_EOVERFLOW, "distance exceeds the " + std::to_string(bits) + "-bit range"};
+      if (bits == 24) g->narrow_overflow[p.algo == GLB_SSSP] = true;
+      recs.clear();
+      const double sf = st->split_fraction;
+      std::memset(st, 0, sizeof(*st));
+      st->split_fraction = sf;
+      GLB_CUDA_TRY(cudaStreamSynchronize(g->stream));
     }
   }
 }
@@ -923,8 +953,8 @@ extern "C" int glb_run(glb_graph* g, const glb_run_params* params, int64_t* dist
     if ((p.strategy == GLB_NS || p.strategy == GLB_HP) && p.mdt <= 0 && p.bins < 1)
       throw glb::Error{GLB_EINVAL, "bins must be >= 1"};
     if (p.block_size < 1) throw glb::Error{GLB_EINVAL, "block_size must be >= 1"};
-    if (p.dist_bits != 0 && p.dist_bits != 32 && p.dist_bits != 64)
-      throw glb::Error{GLB_EINVAL, "dist_bits must be 0, 32 or 64"};
+    if (p.dist_bits != 0 && p.dist_bits != 24 && p.dist_bits != 32 && p.dist_bits != 64)
+      throw glb::Error{GLB_EINVAL, "dist_bits must be 0, 24, 32 or 64"};
     if (p.loop_mode != GLB_LOOP_HOST && p.loop_mode != GLB_LOOP_GRAPH)
       throw glb::Error{GLB_EINVAL, "loop_mode must be GLB_LOOP_HOST or GLB_LOOP_GRAPH"};
     std::memset(stats, 0, sizeof(*stats));

@@ -605,6 +605,7 @@ int glb_graph_create(const int64_t* row_offsets, const int64_t* col, const int64
       g->weighted = weights_or_null != nullptr;
       GLB_CUDA_TRY(cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking));
       GLB_CUDA_TRY(cudaDeviceGetAttribute(&g->num_sms, cudaDevAttrMultiProcessorCount, device));
+      GLB_CUDA_TRY(cudaDeviceGetAttribute(&g->l2_bytes, cudaDevAttrL2CacheSize, device));
       // Opt-in L2 persistence for the distance cells (GLB_L2_PERSIST=1).  It
       // carves the persisting set out of the 126 MB L2 for every kernel, and
       // measured slower on C2 than plain evict-first streaming, so it is off
@@ -653,6 +654,7 @@ int glb_graph_create_rmat(int scale, int64_t edge_factor, double t_a, double t_a
       g->weighted = weighted != 0;
       GLB_CUDA_TRY(cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking));
       GLB_CUDA_TRY(cudaDeviceGetAttribute(&g->num_sms, cudaDevAttrMultiProcessorCount, device));
+      GLB_CUDA_TRY(cudaDeviceGetAttribute(&g->l2_bytes, cudaDevAttrL2CacheSize, device));
       GLB_CUDA_TRY(cudaEventCreate(&g->ev[0]));
       GLB_CUDA_TRY(cudaEventCreate(&g->ev[1]));
       g->host_ctrl = glb::pinned_small_get();

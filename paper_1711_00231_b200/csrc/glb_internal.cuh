@@ -61,6 +61,13 @@ template <>
 struct DistTraits<unsigned long long> {
   static constexpr unsigned long long kInf = 0x7FFFFFFFFFFFFFFFull;
 };
+// 24-bit distances: a distinct 32-bit unsigned type tags the tier whose cell
+// is a single u32 (below).
+typedef char32_t dist24_t;
+template <>
+struct DistTraits<dist24_t> {
+  static constexpr dist24_t kInf = 0xFFFFFFu;
+};
 
 // Distance cells.  With 32-bit distances a cell packs (dist << 32 | gen):
 // one 64-bit atomicMin both lowers the distance (engine.py:120-139) and
@@ -69,26 +76,71 @@ struct DistTraits<unsigned long long> {
 // folded into the relaxation atomic.  Equal distances keep the older
 // generation, so only a strict improvement can claim the push.  64-bit
 // distances (the overflow re-run) keep a separate stamp array instead.
+//
+// Three tiers, tried in order (an overflow re-runs in the next):
+//   dist24_t            u32 cell  = dist << 8 | tag            (16.8 MB at C2)
+//   uint32_t            u64 cell  = dist << 32 | gen           (33.5 MB)
+//   unsigned long long  u64 dist  + a separate stamp array
+// The 24-bit tier halves the randomly gathered array, so more of it stays in
+// L2.  Its tag is (gen mod 128) + 1 and 0 means "pushed long ago"; before
+// every generation that is a multiple of 128 the control inserts a
+// renormalisation step (k_renorm) that resets all tags to 0.  Within such an
+// epoch tags grow with the generation like the 32-bit tier's, so an equal
+// distance never replaces an older tag and only a strict improvement can
+// claim the push.  S is the storage type, tag() the generation as stored,
+// make_tag() a cell with a raw tag (0 = no generation).
 template <typename D>
 struct Cell;
 template <>
-struct Cell<uint32_t> {
+struct Cell<dist24_t> {
+  using S = uint32_t;
   static constexpr bool kPacked = true;
-  __host__ __device__ static constexpr unsigned long long make(uint32_t d, uint32_t gen) {
-    return ((unsigned long long)d << 32) | gen;
+  static constexpr int kGenBits = 8;
+  static constexpr int kDistBits = 24;
+  __host__ __device__ static constexpr uint32_t tag(uint32_t gen) { return (gen & 127u) + 1u; }
+  __host__ __device__ static constexpr uint32_t make_tag(uint32_t d, uint32_t t) {
+    return (d << 8) | t;
   }
+  __host__ __device__ static constexpr uint32_t make(uint32_t d, uint32_t gen) {
+    return make_tag(d, tag(gen));
+  }
+  __device__ static dist24_t dist(uint32_t c) { return (dist24_t)(c >> 8); }
+  __device__ static uint32_t gen(uint32_t c) { return c & 0xFFu; }
+};
+template <>
+struct Cell<uint32_t> {
+  using S = unsigned long long;
+  static constexpr bool kPacked = true;
+  static constexpr int kGenBits = 32;
+  static constexpr int kDistBits = 32;
+  __host__ __device__ static constexpr unsigned long long make_tag(uint32_t d, uint32_t t) {
+    return ((unsigned long long)d << 32) | t;
+  }
+  __host__ __device__ static constexpr unsigned long long make(uint32_t d, uint32_t gen) {
+    return make_tag(d, gen);
+  }
+  __host__ __device__ static constexpr uint32_t tag(uint32_t gen) { return gen; }
   __device__ static uint32_t dist(unsigned long long c) { return (uint32_t)(c >> 32); }
   __device__ static uint32_t gen(unsigned long long c) { return (uint32_t)c; }
 };
 template <>
 struct Cell<unsigned long long> {
+  using S = unsigned long long;
   static constexpr bool kPacked = false;
+  static constexpr int kGenBits = 0;
+  static constexpr int kDistBits = 64;
   __host__ __device__ static constexpr unsigned long long make(unsigned long long d, uint32_t) {
     return d;
   }
+  __host__ __device__ static constexpr unsigned long long make_tag(unsigned long long d, uint32_t) {
+    return d;
+  }
+  __host__ __device__ static constexpr uint32_t tag(uint32_t) { return 0; }
   __device__ static unsigned long long dist(unsigned long long c) { return c; }
   __device__ static uint32_t gen(unsigned long long) { return 0; }
 };
+template <typename D>
+using CellS = typename Cell<D>::S;
 
 // ---------------------------------------------------- per-launch counters ---
 // One LaunchStats per kernel invocation; kStatSlots copies spread the atomics
@@ -110,10 +162,12 @@ struct LaunchStats {
 // own step (the underlying mode stays in DevCtrl::mode, `use_small` selects it).
 // kModeWDF is a WD step whose item list the previous step already appended
 // (fused pushes): relax only, no scan.
+// kModeRenorm retags the 24-bit tier's cells (see Cell<dist24_t>).
 enum StepMode : int {
-  kModeDone = 0, kModeRelax = 1, kModeWD = 2, kModeHP = 3, kModeSmall = 4, kModeWDF = 5
+  kModeDone = 0, kModeRelax = 1, kModeWD = 2, kModeHP = 3, kModeSmall = 4, kModeWDF = 5,
+  kModeRenorm = 6
 };
-constexpr int kNumModes = 6;
+constexpr int kNumModes = 7;
 
 // One long HP window [lo, hi) of node u at distance dn, relaxed in 2048-edge
 // pieces claimed by any CTA (hierarchical processing's CTA granularity).
@@ -176,6 +230,9 @@ struct DevCtrl {
   unsigned int wd_zero_next;    // zero-degree nodes pushed (counted for the record only)
   int wd_dense;                 // the WD scan reads the frontier from the cells, not the queue
   int dense_ok;                 // packed cells, WD strategy, not sharded
+  int tag_bits;                 // generation bits stored in a cell (8: 24-bit tier)
+  int saved_mode;               // the step a renormalisation step interrupted
+  unsigned int renorm_gen;      // generation of the last renormalisation
   long long n_nodes;            // nodes of the traversed graph
   // ---- HP: windows >= kHpCtaThreshold edges form a grid-wide CTA bin
   struct HpBig* hp_big;         // bin entries of the current window step
@@ -237,6 +294,7 @@ struct glb_graph {
   int64_t max_degree = 0;
   cudaStream_t stream = nullptr;
   int num_sms = 148;
+  int l2_bytes = 0;            // cudaDevAttrL2CacheSize
   int l2_persist_max = 0;      // cudaDevAttrMaxPersistingL2CacheSize (0: unsupported)
   int l2_window_max = 0;       // cudaDevAttrMaxAccessPolicyWindowSize
   long long* row = nullptr;
@@ -245,6 +303,7 @@ struct glb_graph {
   glb::Workspace ws;
   uint32_t stamp_epoch = 0;   // last stamp generation handed out
   uint32_t scan_epoch = 0;    // last look-back epoch handed out
+  bool narrow_overflow[2] = {false, false};  // a 24-bit run overflowed (BFS, SSSP)
   void* host_ctrl = nullptr;  // pinned DevCtrl + stats mirror
   cudaEvent_t ev[2] = {nullptr, nullptr};
   std::vector<cudaEvent_t> ev_pool;
@@ -287,6 +346,9 @@ inline unsigned int grid_for(long long items, int per_block, int cap) {
 // ------------------------------------------------------ device helpers ---
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
 
+#ifndef GLB_STREAM_POLICY
+#define GLB_STREAM_POLICY 1  // evict-first L2 policy on the col / weight streams
+#endif
 // Single-use streams (col / weights): an L2 evict-first access policy, made
 // once per thread, so a pass over the 537 MB edge arrays does not push the
 // randomly re-read distance cells out of L2 (ncu: with plain or .cs loads
@@ -336,13 +398,13 @@ __device__ __forceinline__ bool claim(uint32_t* stamp, uint32_t v, uint32_t gen)
 // distance strictly decreased; *first tells whether this is the first such
 // decrease in generation `gen` (packed cells) -- the caller pushes then.
 template <typename D>
-__device__ __forceinline__ bool relax_cell(unsigned long long* cells, uint32_t v, D cand,
-                                           uint32_t gen, bool* first) {
-  const unsigned long long cur = cells[v];
+__device__ __forceinline__ bool relax_cell(CellS<D>* cells, uint32_t v, D cand, uint32_t gen,
+                                           bool* first) {
+  const CellS<D> cur = cells[v];
   if (cand >= Cell<D>::dist(cur)) return false;
-  const unsigned long long old = atomicMin(cells + v, Cell<D>::make(cand, gen));
+  const CellS<D> old = atomicMin(cells + v, Cell<D>::make(cand, gen));
   if (cand >= Cell<D>::dist(old)) return false;
-  *first = Cell<D>::gen(old) != gen;
+  *first = Cell<D>::gen(old) != Cell<D>::tag(gen);
   return true;
 }
 

@@ -103,13 +103,29 @@ __device__ __forceinline__ uint32_t shfl_dist(uint32_t d, int src) {
 __device__ __forceinline__ unsigned long long shfl_dist(unsigned long long d, int src) {
   return __shfl_sync(0xffffffffu, d, src);
 }
+__device__ __forceinline__ dist24_t shfl_dist(dist24_t d, int src) {
+  return (dist24_t)__shfl_sync(0xffffffffu, (uint32_t)d, src);
+}
+
+// cell gather with an L2 cache-hint policy (32- or 64-bit cells)
+__device__ __forceinline__ uint32_t ld_keep(const uint32_t* p, unsigned long long pol) {
+  uint32_t r;
+  asm("ld.global.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(pol));
+  return r;
+}
+__device__ __forceinline__ unsigned long long ld_keep(const unsigned long long* p,
+                                                      unsigned long long pol) {
+  unsigned long long r;
+  asm("ld.global.L2::cache_hint.u64 %0, [%1], %2;" : "=l"(r) : "l"(p), "l"(pol));
+  return r;
+}
 
 // --------------------------------------------------------- relax helper ---
 template <typename D, bool W>
 struct Relaxer {
   const uint32_t* __restrict__ col;
   const uint32_t* __restrict__ wt;
-  unsigned long long* cells;  // Cell<D> distance cells
+  CellS<D>* cells;            // Cell<D> distance cells
   uint32_t* stamp;            // push dedup for unpacked (64-bit) cells
   uint32_t gen;
   uint32_t* qout;
@@ -119,9 +135,7 @@ struct Relaxer {
 
   __device__ __forceinline__ D dist(uint32_t u) const {
 #if GLB_CELL_POLICY
-    unsigned long long r;
-    asm("ld.global.L2::cache_hint.u64 %0, [%1], %2;" : "=l"(r) : "l"(cells + u), "l"(keep));
-    return Cell<D>::dist(r);
+    return Cell<D>::dist(ld_keep(cells + u, keep));
 #else
     return Cell<D>::dist(cells[u]);
 #endif
@@ -202,7 +216,7 @@ __device__ __forceinline__ unsigned relax_batch(const Relaxer<D, W>& rx, BlockQ&
       if (make_cand<D>(dn[k], w[k], cand[k], rx.ovf)) want |= 1u << k;
     }
 #endif
-  unsigned long long old[K];
+  CellS<D> old[K];
 #pragma unroll
   for (int k = 0; k < K; ++k)
     if (want >> k & 1u) old[k] = atomicMin(rx.cells + v[k], Cell<D>::make(cand[k], rx.gen));
@@ -211,7 +225,7 @@ __device__ __forceinline__ unsigned relax_batch(const Relaxer<D, W>& rx, BlockQ&
   for (int k = 0; k < K; ++k)
     if ((want >> k & 1u) && cand[k] < Cell<D>::dist(old[k])) {
       won |= 1u << k;
-      if (Cell<D>::gen(old[k]) != rx.gen) first |= 1u << k;
+      if (Cell<D>::gen(old[k]) != Cell<D>::tag(rx.gen)) first |= 1u << k;
     }
   if (!Cell<D>::kPacked) {
     unsigned prev[K];
@@ -426,7 +440,7 @@ __global__ void __launch_bounds__(kBlock) k_ep_relax(const long long* __restrict
         ++c.relax;
         if (make_cand<D>(du[k], w[k], cand[k], rx.ovf) && cand[k] < cur[k]) want |= 1u << k;
       }
-    unsigned long long old[K];
+    CellS<D> old[K];
 #pragma unroll
     for (int k = 0; k < K; ++k)
       if (want >> k & 1u) old[k] = atomicMin(rx.cells + v[k], Cell<D>::make(cand[k], rx.gen));
@@ -435,7 +449,7 @@ __global__ void __launch_bounds__(kBlock) k_ep_relax(const long long* __restrict
     for (int k = 0; k < K; ++k) {
       pushk[k] = false;
       if ((want >> k & 1u) && cand[k] < Cell<D>::dist(old[k]))
-        pushk[k] = rx.claim_push(v[k], Cell<D>::gen(old[k]) != rx.gen);
+        pushk[k] = rx.claim_push(v[k], Cell<D>::gen(old[k]) != Cell<D>::tag(rx.gen));
     }
 #pragma unroll
     for (int k = 0; k < K; ++k) {
@@ -502,7 +516,7 @@ struct __align__(16) WdItem {
 // start of find_offsets (workload.py:45-72) at warp-tile granularity.
 template <typename D>
 __global__ void __launch_bounds__(kBlock) k_wd_scan(const long long* __restrict__ row,
-                                                    const unsigned long long* __restrict__ cells,
+                                                    const CellS<D>* __restrict__ cells,
                                                     LookbackState<2> lb, DevCtrl* ctrl) {
   WdItem* __restrict__ items = reinterpret_cast<WdItem*>(ctrl->wd_items_buf[ctrl->wd_cur]);
   unsigned int* __restrict__ tile_first = ctrl->wd_tf_buf[ctrl->wd_cur];
@@ -515,7 +529,7 @@ __global__ void __launch_bounds__(kBlock) k_wd_scan(const long long* __restrict_
   // CSR segments touch, and the relax kernel's col / weight reads become
   // contiguous runs instead of one partial sector per short segment.
   const bool dense = ctrl->wd_dense != 0;
-  const uint32_t in_gen = ctrl->gen - 1u;
+  const uint32_t in_gen = Cell<D>::tag(ctrl->gen - 1u);
   const long long n = dense ? ctrl->n_nodes : ctrl->qcount[ctrl->in];
   const long long ntiles = (n + kWdScanTile - 1) / kWdScanTile;
   if (ntiles == 0) {
@@ -872,7 +886,7 @@ __global__ void __launch_bounds__(kBlock, GLB_WD_MINB) k_wd_relax(
       if (valid >> k & 1u) {
         if (make_cand<D>(dn[k], w[k], cand[k], rx.ovf) && cand[k] < cur[k]) want |= 1u << k;
       }
-    unsigned long long old[kWdEPL];
+    CellS<D> old[kWdEPL];
 #pragma unroll
     for (int k = 0; k < kWdEPL; ++k)
       if (want >> k & 1u) old[k] = atomicMin(rx.cells + v[k], Cell<D>::make(cand[k], rx.gen));
@@ -882,7 +896,7 @@ __global__ void __launch_bounds__(kBlock, GLB_WD_MINB) k_wd_relax(
     for (int k = 0; k < kWdEPL; ++k)
       if ((want >> k & 1u) && cand[k] < Cell<D>::dist(old[k])) {
         if (Cell<D>::kPacked) {
-          if (Cell<D>::gen(old[k]) != rx.gen) first |= 1u << k;
+          if (Cell<D>::gen(old[k]) != Cell<D>::tag(rx.gen)) first |= 1u << k;
         } else if (claim(rx.stamp, v[k], rx.gen)) {
           first |= 1u << k;
         }
@@ -1095,8 +1109,8 @@ __global__ void __launch_bounds__(kBlock, GLB_RELAX_MINB) k_hp_bigbin(Relaxer<D,
 
 // ============================================================ setup ===
 template <typename D>
-__global__ void k_init_dist(unsigned long long* cells, long long n) {
-  const unsigned long long inf = Cell<D>::make(DistTraits<D>::kInf, 0);
+__global__ void k_init_dist(CellS<D>* cells, long long n) {
+  const CellS<D> inf = Cell<D>::make_tag(DistTraits<D>::kInf, 0);
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x)
     cells[i] = inf;
@@ -1106,35 +1120,46 @@ __global__ void k_init_dist(unsigned long long* cells, long long n) {
 // splitting.py:123-126) for node worklists, or the source's out-edge range for
 // the EP edge worklist (edge_based.py:55).
 template <typename D>
-__global__ void k_seed(unsigned long long* cells, uint32_t* q, unsigned int* nq, long long src,
+__global__ void k_seed(CellS<D>* cells, uint32_t* q, unsigned int* nq, long long src,
                        long long kid_lo, long long kid_hi, long long edge_lo, long long edge_hi,
                        bool edges) {
   const long long tid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   const long long stride = (long long)gridDim.x * blockDim.x;
-  if (tid == 0) cells[src] = Cell<D>::make(0, 0);
+  if (tid == 0) cells[src] = Cell<D>::make_tag(0, 0);
   if (edges) {
     for (long long e = edge_lo + tid; e < edge_hi; e += stride) q[e - edge_lo] = (uint32_t)e;
     if (tid == 0) *nq = (unsigned)(edge_hi - edge_lo);
   } else {
     if (tid == 0) q[0] = (uint32_t)src;
     for (long long k = kid_lo + tid; k < kid_hi; k += stride) {
-      cells[k] = Cell<D>::make(0, 0);
+      cells[k] = Cell<D>::make_tag(0, 0);
       q[1 + k - kid_lo] = (uint32_t)k;
     }
     if (tid == 0) *nq = (unsigned)(1 + kid_hi - kid_lo);
   }
 }
 
-// packed u32 cells -> u32 distances (INF stays 0xFFFFFFFF; widened on the host)
-__global__ void k_dist_u32(const unsigned long long* __restrict__ cells, long long n,
+// packed cells -> u32 distances (INF becomes 0xFFFFFFFF; widened on the host)
+template <typename D>
+__global__ void k_dist_u32(const CellS<D>* __restrict__ cells, long long n,
                            uint32_t* __restrict__ out) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const D d = Cell<D>::dist(cells[i]);
+    out[i] = d == DistTraits<D>::kInf ? 0xFFFFFFFFu : (uint32_t)d;
+  }
+}
+
+// 24-bit tier: every tag is reset to 0 ("no generation") before a
+// generation that is a multiple of 128 starts (Cell<dist24_t>).
+__global__ void k_renorm(uint32_t* __restrict__ cells, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x)
-    out[i] = Cell<uint32_t>::dist(cells[i]);
+    cells[i] &= ~0xFFu;
 }
 
 template <typename D>
-__global__ void k_dist_out(const unsigned long long* __restrict__ cells, long long n,
+__global__ void k_dist_out(const CellS<D>* __restrict__ cells, long long n,
                            long long* __restrict__ out) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x) {

@@ -51,7 +51,7 @@ constexpr size_t small_smem_bytes() {
 }
 
 template <typename D>
-__device__ __forceinline__ D dist_cg(const unsigned long long* cells, uint32_t v) {
+__device__ __forceinline__ D dist_cg(const CellS<D>* cells, uint32_t v) {
   return Cell<D>::dist(__ldcg(cells + v));
 }
 
@@ -101,10 +101,10 @@ __device__ __forceinline__ unsigned small_relax(const Relaxer<D, W>& rx, unsigne
 #pragma unroll
   for (int k = 0; k < K; ++k)
     if (want >> k & 1u) {
-      const unsigned long long old = atomicMin(rx.cells + v[k], Cell<D>::make(cand[k], rx.gen));
+      const CellS<D> old = atomicMin(rx.cells + v[k], Cell<D>::make(cand[k], rx.gen));
       if (cand[k] < Cell<D>::dist(old)) {
         won |= 1u << k;
-        if (Cell<D>::kPacked ? Cell<D>::gen(old) != rx.gen
+        if (Cell<D>::kPacked ? Cell<D>::gen(old) != Cell<D>::tag(rx.gen)
                              : atomicExch(rx.stamp + v[k], rx.gen) != rx.gen)
           first |= 1u << k;
       }
@@ -359,9 +359,9 @@ __global__ void __cluster_dims__(kSmallCtas, 1, 1) __launch_bounds__(kSmallThrea
         ++c.relax;
         D cand;
         if (!make_cand<D>(du, w, cand, rx.ovf) || cand >= dist_cg<D>(rx.cells, v)) continue;
-        const unsigned long long old = atomicMin(rx.cells + v, Cell<D>::make(cand, rx.gen));
+        const CellS<D> old = atomicMin(rx.cells + v, Cell<D>::make(cand, rx.gen));
         if (cand >= Cell<D>::dist(old)) continue;
-        const bool first = Cell<D>::kPacked ? Cell<D>::gen(old) != rx.gen
+        const bool first = Cell<D>::kPacked ? Cell<D>::gen(old) != Cell<D>::tag(rx.gen)
                                             : atomicExch(rx.stamp + v, rx.gen) != rx.gen;
         if (!first) continue;
         const long long lo = row[v];
@@ -478,6 +478,7 @@ __global__ void __cluster_dims__(kSmallCtas, 1, 1) __launch_bounds__(kSmallThrea
           ctl_simple_advance(cc);
         }
         if (cc->done) cc->mode = kModeDone;
+        ctl_check_renorm(cc);
         s_go = small_eligible(cc);
         if (rank == 0) {  // clear the slot of iteration it + 2 (see above)
           const unsigned z = (it + 2u) % 3u;

@@ -38,7 +38,8 @@ class KernelConfig:
     kept for compatibility, the device sizes its own grids.  ``loop`` picks the
     host-driven loop ("host", one round trip per launch, exact per-launch
     timing) or the device-driven CUDA graph ("graph").  ``dist_bits`` 0 runs
-    32-bit distances and re-runs in 64 bits on overflow.
+    24-bit distances (one u32 cell per node), re-running at 32 and then 64
+    bits on overflow; 24 / 32 / 64 pin one width.
     """
 
     virtual_threads: int | None = None
@@ -60,8 +61,8 @@ class KernelConfig:
             raise ValueError("workers must be >= 1")
         if self.loop not in LOOP_MODES:
             raise ValueError(f"loop must be one of {LOOP_MODES}")
-        if self.dist_bits not in (0, 32, 64):
-            raise ValueError("dist_bits must be 0, 32 or 64")
+        if self.dist_bits not in (0, 24, 32, 64):
+            raise ValueError("dist_bits must be 0, 24, 32 or 64")
 
 
 def resolve_threads(cfg: KernelConfig, active_items: int) -> int:

@@ -86,6 +86,55 @@ def test_u32_overflow_promotes_to_u64(oracle):
             pkg.run_strategy(tag, g, 0, pkg.RelaxOp("sssp"), pkg.KernelConfig(dist_bits=32))
 
 
+def test_24bit_cells_boundary_and_promotion(oracle):
+    """dist_bits 24: 24-bit distances in one u32 cell per node (the automatic
+    first tier only for graphs whose u64 cells exceed twice the L2).  The
+    largest representable distance is 2^24 - 2; one more is an OverflowError
+    at 24 bits and a 32-bit run under dist_bits 0."""
+    top = (1 << 24) - 2
+    for last, fits in ((top - 0x7FFFFF, True), (top + 1 - 0x7FFFFF, False)):
+        g = pkg.CsrGraph.from_edges(3, [0, 1], [1, 2], [0x7FFFFF, last])
+        exp = oracle.dijkstra(g.row_offsets, g.col_indices, g.weights, 0)
+        for tag in TAGS:
+            r = pkg.run_strategy(tag, g, 0, pkg.RelaxOp("sssp"), pkg.KernelConfig())
+            assert np.array_equal(r.dist.array, exp) and r.device["dist_bits"] == 32, tag
+            for loop in ("host", "graph"):
+                cfg = pkg.KernelConfig(dist_bits=24, loop=loop)
+                if fits:
+                    r = pkg.run_strategy(tag, g, 0, pkg.RelaxOp("sssp"), cfg)
+                    assert np.array_equal(r.dist.array, exp) and r.device["dist_bits"] == 24, tag
+                else:
+                    with pytest.raises(OverflowError):
+                        pkg.run_strategy(tag, g, 0, pkg.RelaxOp("sssp"), cfg)
+
+
+@pytest.mark.parametrize("variant", ["default", "grid_kernels", "grid_fused"])
+@pytest.mark.parametrize("loop", ["host", "graph"])
+def test_24bit_generation_tags_renormalise(oracle, loop, variant, monkeypatch):
+    """More than 256 generations: the 8-bit push tags of the 24-bit tier wrap
+    and are renormalised every 128 generations (k_renorm); results must equal
+    the 32- and 64-bit tiers' and the oracle's."""
+    for k, v in VARIANTS[variant].items():
+        monkeypatch.setenv(k, v)
+    rng = np.random.default_rng(7)
+    n = 700  # a path with shortcuts: ~600 generations, ragged frontiers
+    src = np.concatenate([np.arange(n - 1), rng.integers(0, n, 60)])
+    dst = np.concatenate([np.arange(1, n), rng.integers(0, n, 60)])
+    w = rng.integers(1, 50, size=src.size)
+    w[n - 1:] = 5000
+    g = pkg.CsrGraph.from_edges(n, src, dst, w)
+    grid = pkg.grid_graph(24, seed=3)
+    for gr in (g, grid):
+        for algo in ("bfs", "sssp"):
+            exp = oracle.oracle_distances(gr, 0, algo)
+            for tag in TAGS:
+                for bits in (24, 32):
+                    r = pkg.run_strategy(tag, gr, 0, pkg.RelaxOp(algo),
+                                         pkg.KernelConfig(loop=loop, dist_bits=bits), mdt=None)
+                    assert np.array_equal(r.dist.array, exp), (gr.num_nodes, algo, tag, bits)
+                    assert r.device["dist_bits"] == bits
+
+
 def test_random_graphs_with_quirks(oracle):
     rng = np.random.default_rng(123)
     for trial in range(25):

@@ -28,6 +28,7 @@ ap.add_argument("--scale", type=int, default=22)
 ap.add_argument("--reps", type=int, default=5)
 ap.add_argument("--loop", default="graph")
 ap.add_argument("--skewed", action="store_true")
+ap.add_argument("--dist-bits", type=int, default=0)
 a = ap.parse_args()
 params = (0.7, 0.15, 0.10, 0.05) if a.skewed else pkg.DEFAULT_RMAT_PARAMS
 g = pkg.generate_rmat(a.scale, 16, params=params, seed=1, max_weight=255)
@@ -36,8 +37,12 @@ from oracle import oracle  # noqa: E402
 exp = oracle.oracle_distances(g, 0, a.algo)
 
 libs = []
-for path in a.libs:
-    L = ctypes.CDLL(str(Path(path).resolve()))
+bits_of = {}
+for spec in a.libs:  # "lib.so" or "lib.so:24" (per-library dist_bits)
+    path, _, b = spec.partition(":")
+    path = spec if not b else path + ":" + b
+    bits_of[path] = int(b) if b else a.dist_bits
+    L = ctypes.CDLL(str(Path(path.partition(":")[0]).resolve()))
     for name, (res, args) in _lib.SIGNATURES.items():
         if not hasattr(L, name):  # older builds lack newer entry points
             continue
@@ -62,6 +67,7 @@ for rep in range(a.reps + 1):
             p.bins, p.chunked, p.max_cells, p.block_size, p.hp_fallback = 10, 1, 1 << 40, 1024, 1
             p.loop_mode = 1 if a.loop == "graph" else 0
             p.record_timing = 1
+            p.dist_bits = bits_of[path]
             stt = _lib.RunStats()
             rc = L.glb_run(h, ctypes.byref(p), _lib.ptr64(out) if rep == 0 else None,
                            ctypes.byref(stt), None, 0)

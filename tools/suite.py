@@ -67,6 +67,7 @@ def main():
     ap.add_argument("--tags", default=",".join(TAGS))
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--loop", default="graph")
+    ap.add_argument("--dist-bits", type=int, default=0)
     ap.add_argument("--out", default=str(ROOT / "gpurun_out" / "suite.json"))
     a = ap.parse_args()
     oracle.build()
@@ -81,7 +82,7 @@ def main():
             check = "oracle"
             if cfg == "C5":
                 exp, d5, check = c5_reference(g, algo, a.tags.split(","),
-                                              pkg.KernelConfig(loop=a.loop))
+                                              pkg.KernelConfig(loop=a.loop, dist_bits=a.dist_bits))
                 if d5 is not None:
                     deg = d5
                 if deg is None:
@@ -96,7 +97,7 @@ def main():
             reached = exp != pkg.INF
             e_r, n_r = int(deg[reached].sum()), int(reached.sum())
             for tag in a.tags.split(","):
-                kc = pkg.KernelConfig(loop=a.loop, record_timing=True)
+                kc = pkg.KernelConfig(loop=a.loop, record_timing=True, dist_bits=a.dist_bits)
                 r = pkg.run_strategy(tag, g, 0, pkg.RelaxOp(algo), kc)
                 if not r.feasible:
                     rows.append(dict(config=cfg, algo=algo, strategy=tag, status=r.status))
