@@ -22,6 +22,8 @@
  *   glb_csr_to_coo       csr_to_coo                             csr.py:155-170
  *   glb_inclusive_scan   inclusive_scan                         scan.py:19-65
  *   glb_find_offsets     find_offsets                           strategies/workload.py:45-72
+ *   glb_validate         sequential_bfs / dijkstra + verify     oracles.py:13-82, as used by
+ *                        run_benchmark(verify=True)             bench.py:186-196
  *
  * Status -> Python exception mapping used by the drop-in package:
  *   GLB_EINVAL -> ValueError, GLB_ERANGE -> IndexError, GLB_EOVERFLOW -> OverflowError,
@@ -231,6 +233,16 @@ int glb_split_graph(glb_graph* g, int64_t mdt, int64_t* new_n,
  * Returns GLB_ECOO_CAPACITY when (3 if weighted else 2) * m > max_cells.
  * src_out: int64[m] (dst/weights are the CSR arrays, copied by the caller). */
 int glb_csr_to_coo(glb_graph* g, int64_t max_cells, int64_t* src_out);
+
+/* ---- distance certificate (oracles.py:13-82, bench.py:186-196) ----
+ * Proves dist (int64[n], INF = INT64_MAX) the exact BFS (algo GLB_BFS) or
+ * SSSP (GLB_SSSP) distances from source without an oracle: d[source] == 0,
+ * no edge out of a reached node can lower its head (d[v] <= d[u] + w), and
+ * every reached node is reachable from the source over tight edges
+ * (d[u] + w == d[v]).  n_bad = number of nodes violating a rule (0 = the
+ * array is correct), first_bad = the smallest such node id or -1. */
+int glb_validate(glb_graph* g, int32_t algo, int64_t source, const int64_t* dist,
+                 int64_t* n_bad, int64_t* first_bad);
 
 /* ---- device primitives on host arrays (scan.py, workload.py) ---- */
 /* out[i] = values[0] + ... + values[i]; GLB_EOVERFLOW past int64. */

@@ -7,9 +7,12 @@ five strategies (BS, EP, WD, NS, HP), executed by hand-written sm_100a CUDA
 kernels in libgraphlb_b200.so through a C-ABI (include/graphlb_b200.h).
 
 Not provided here (outside the hot path): the CPU launch emulation
-(launch_kernel, ThreadCtx, Worklist, atomic_relax_min), the sequential oracles
-(they live in oracle/ as test infrastructure), reports and CLI.  The file
-loaders (io.py) are native and read the binary cache straight into HBM.
+(launch_kernel, ThreadCtx, Worklist, atomic_relax_min) and the sequential
+oracles (they live in oracle/ as test infrastructure); results are instead
+certified on the device (validate_distances).  The file loaders (io.py) are
+native and read the binary cache straight into HBM.  The benchmark harness,
+report writer and CLI are ``.bench``, ``.report`` and ``.cli``
+(``python -m paper_1711_00231_b200``).
 """
 
 from .analysis import (
@@ -20,6 +23,7 @@ from .analysis import (
     compute_mdt,
     degree_stats,
     inclusive_scan,
+    validate_distances,
     verify,
 )
 from .graph import (

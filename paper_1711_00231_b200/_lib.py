@@ -109,6 +109,7 @@ SIGNATURES = {
     "glb_split_graph": (ctypes.c_int, [ctypes.c_void_p, _i64, _p64, _p64, _p64, _p64, _p64,
                                        _p64, _p64]),
     "glb_csr_to_coo": (ctypes.c_int, [ctypes.c_void_p, _i64, _p64]),
+    "glb_validate": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, _i64, _p64, _p64, _p64]),
     "glb_inclusive_scan": (ctypes.c_int, [_p64, _i64, _p64, ctypes.c_int]),
     "glb_find_offsets": (ctypes.c_int, [_p64, _i64, _i64, _i64, _p64, _p64, ctypes.c_int]),
 }

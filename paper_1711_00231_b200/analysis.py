@@ -111,3 +111,28 @@ def verify(expected, actual) -> VerificationReport:
         return VerificationReport(True, 0, None)
     i = int(bad[0])
     return VerificationReport(False, int(bad.shape[0]), (i, int(e[i]), int(a[i])))
+
+
+def validate_distances(g: CsrGraph, source: int, algo: str, dist,
+                       device: int | None = None) -> VerificationReport:
+    """Device certificate of a BFS/SSSP distance array (glb_validate): no
+    oracle run, yet exact -- d[source] = 0, no edge out of a reached node can
+    lower its head, and every reached node is reachable from the source over
+    tight edges.  Replaces the sequential_bfs / dijkstra + verify pair of
+    run_benchmark(verify=True) (oracles.py:13-82, bench.py:186-196).
+    ``first_mismatch`` is (node, None, actual) -- a certificate knows which
+    node is wrong, not its true distance."""
+    if algo not in ("bfs", "sssp"):
+        raise ValueError(f"unknown relaxation kind {algo!r}")
+    a = np.ascontiguousarray(_cells(dist), dtype=np.int64)
+    if a.shape[0] != g.num_nodes:
+        raise ValueError(f"length mismatch: graph has {g.num_nodes} nodes, dist {a.shape[0]}")
+    if not 0 <= source < g.num_nodes:
+        raise ValueError(f"source {source} out of range for {g.num_nodes} nodes")
+    nb, fb = ctypes.c_int64(), ctypes.c_int64()
+    _lib.check(_lib.lib().glb_validate(g.device_graph(device), 0 if algo == "bfs" else 1, int(source),
+                                       _lib.ptr64(a), ctypes.byref(nb), ctypes.byref(fb)),
+               "glb_validate")
+    if nb.value == 0:
+        return VerificationReport(True, 0, None)
+    return VerificationReport(False, int(nb.value), (int(fb.value), None, int(a[fb.value])))

@@ -522,6 +522,148 @@ __global__ void k_find_offsets(const long long* __restrict__ prefix, long long s
   }
 }
 
+
+// ------------------------------------------------ distance certificate ---
+// glb_validate: proves a BFS/SSSP distance array correct without an oracle
+// (the check run_benchmark(verify=True) needs, bench.py:186-196 /
+// oracles.py:58-82).  With w(e) = 1 for BFS and unweighted SSSP:
+//   (1) d[src] == 0;
+//   (2) every edge u->v out of a reached u has d[v] <= d[u] + w  (so d is at
+//       most the true distance and every truly reachable node is reached);
+//   (3) every reached node is reachable from src over tight edges
+//       (d[u] + w == d[v]), so d[v] is the length of a real path, i.e. at
+//       least the true distance.  Zero-weight edges are fine: tightness is
+//       followed from the source, not from the node.
+// A node violating any rule gets a flag; the call returns their count and
+// the smallest flagged id.
+constexpr long long kInf64 = 0x7FFFFFFFFFFFFFFFll;
+
+__device__ __forceinline__ unsigned long long val_w(const uint32_t* wt, long long e) {
+  return wt ? (unsigned long long)__ldg(wt + e) : 1ull;
+}
+
+// (2) and (1): warp per node, lanes over its out-edges
+__global__ void k_val_edges(const long long* __restrict__ row, const uint32_t* __restrict__ col,
+                            const uint32_t* __restrict__ wt, long long n,
+                            const long long* __restrict__ d, long long src,
+                            unsigned char* __restrict__ bad) {
+  const long long warp = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+  const unsigned lane = threadIdx.x & 31u;
+  for (long long u = warp; u < n; u += nwarps) {
+    const long long du = d[u];
+    if (lane == 0 && (du < 0 || (u == src && du != 0))) bad[u] = 1;
+    if (du < 0 || du == kInf64) continue;
+    const long long lo = row[u], hi = row[u + 1];
+    for (long long e = lo + lane; e < hi; e += 32) {
+      const uint32_t v = __ldg(col + e);
+      const long long dv = d[v];
+      if (dv == kInf64 || (unsigned long long)dv > (unsigned long long)du + val_w(wt, e)) bad[v] = 1;
+    }
+  }
+}
+
+// (3): one level of the tight-edge BFS from the source, warp per node
+__global__ void k_val_tight(const long long* __restrict__ row, const uint32_t* __restrict__ col,
+                            const uint32_t* __restrict__ wt, const long long* __restrict__ d,
+                            const uint32_t* __restrict__ qin, const unsigned* nin,
+                            uint32_t* __restrict__ qout, unsigned* nout,
+                            unsigned* __restrict__ seen) {
+  const long long warp = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+  const unsigned lane = threadIdx.x & 31u;
+  const long long cnt = *nin;
+  for (long long i = warp; i < cnt; i += nwarps) {
+    const uint32_t u = qin[i];
+    const unsigned long long du = (unsigned long long)d[u];
+    const long long lo = row[u], hi = row[u + 1];
+    for (long long e = lo + lane; e < hi; e += 32) {
+      const uint32_t v = __ldg(col + e);
+      if ((unsigned long long)d[v] == du + val_w(wt, e) && atomicExch(seen + v, 1u) == 0u)
+        qout[atomicAdd(nout, 1u)] = v;
+    }
+  }
+}
+
+// reached but not tight-reachable -> flagged; then count + smallest flagged id
+__global__ void k_val_finish(const long long* __restrict__ d, const unsigned* __restrict__ seen,
+                             unsigned char* __restrict__ bad, long long n,
+                             unsigned long long* __restrict__ out /* [count, min id] */) {
+  unsigned long long c = 0, first = ~0ull;
+  for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; v < n;
+       v += (long long)gridDim.x * blockDim.x) {
+    const long long dv = d[v];
+    bool b = bad[v] != 0 || (dv >= 0 && dv != kInf64 && !seen[v]);
+    if (b) {
+      ++c;
+      if ((unsigned long long)v < first) first = (unsigned long long)v;
+    }
+  }
+  for (int off = 16; off > 0; off >>= 1) {
+    c += __shfl_xor_sync(0xffffffffu, c, off);
+    const unsigned long long o = __shfl_xor_sync(0xffffffffu, first, off);
+    first = o < first ? o : first;
+  }
+  if ((threadIdx.x & 31u) == 0 && c) {
+    atomicAdd(out, c);
+    atomicMin(out + 1, first);
+  }
+}
+
+__global__ void k_val_seed(const long long* d, long long src, uint32_t* q, unsigned* nq,
+                           unsigned* seen) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    const bool ok = d[src] == 0;
+    *nq = ok ? 1u : 0u;
+    if (ok) {
+      q[0] = (uint32_t)src;
+      seen[src] = 1u;
+    }
+  }
+}
+
+void validate(glb_graph* g, bool weights, long long src, const int64_t* dist, long long* n_bad,
+              long long* first_bad) {
+  Workspace& ws = g->ws;
+  const long long n = g->n;
+  const size_t nb = (size_t)std::max<long long>(n, 1);
+  cudaStream_t s = g->stream;
+  long long* d = (long long*)ensure(ws.out64, nb * 8);
+  uint32_t* q[2] = {(uint32_t*)ensure(ws.q[0], nb * 4), (uint32_t*)ensure(ws.q[1], nb * 4)};
+  char* flags = (char*)ensure(ws.misc, nb * 5 + 64);
+  unsigned* seen = (unsigned*)flags;
+  unsigned char* bad = (unsigned char*)(flags + nb * 4);
+  unsigned* counts = (unsigned*)ensure(ws.misc_small, 64);  // nq[2], out[2] (u64) at +16
+  unsigned long long* out = (unsigned long long*)(counts + 4);
+  GLB_CUDA_TRY(cudaMemcpyAsync(d, dist, (size_t)n * 8, cudaMemcpyHostToDevice, s));
+  GLB_CUDA_TRY(cudaMemsetAsync(flags, 0, nb * 5, s));
+  const unsigned long long init[2] = {0ull, ~0ull};
+  GLB_CUDA_TRY(cudaMemcpyAsync(out, init, 16, cudaMemcpyHostToDevice, s));
+  const uint32_t* wt = weights ? g->wt : nullptr;
+  const unsigned grid = grid_for(n * 32, kBlock, g->num_sms * 8);
+  k_val_edges<<<grid, kBlock, 0, s>>>(g->row, g->col, wt, n, d, src, bad);
+  GLB_CHECK_LAUNCH();
+  k_val_seed<<<1, 32, 0, s>>>(d, src, q[0], counts, seen);
+  GLB_CHECK_LAUNCH();
+  unsigned h_n = 1;
+  for (int lvl = 0; h_n; ++lvl) {  // tight-edge BFS, one launch per level
+    const int a = lvl & 1;
+    GLB_CUDA_TRY(cudaMemsetAsync(counts + (a ^ 1), 0, 4, s));
+    k_val_tight<<<grid, kBlock, 0, s>>>(g->row, g->col, wt, d, q[a], counts + a, q[a ^ 1],
+                                         counts + (a ^ 1), seen);
+    GLB_CHECK_LAUNCH();
+    GLB_CUDA_TRY(cudaMemcpyAsync(&h_n, counts + (a ^ 1), 4, cudaMemcpyDeviceToHost, s));
+    GLB_CUDA_TRY(cudaStreamSynchronize(s));
+  }
+  k_val_finish<<<grid_for(n, kBlock, g->num_sms * 8), kBlock, 0, s>>>(d, seen, bad, n, out);
+  GLB_CHECK_LAUNCH();
+  unsigned long long h[2];
+  GLB_CUDA_TRY(cudaMemcpyAsync(h, out, 16, cudaMemcpyDeviceToHost, s));
+  GLB_CUDA_TRY(cudaStreamSynchronize(s));
+  *n_bad = (long long)h[0];
+  *first_bad = h[0] ? (long long)h[1] : -1;
+}
+
 }  // namespace glb
 
 // ================================================================ C-ABI ===
@@ -1009,6 +1151,23 @@ int glb_find_offsets(const int64_t* prefix, int64_t size, int64_t edges_per_thre
     }
     cudaFree(base);
     cudaStreamDestroy(s);
+  });
+}
+
+int glb_validate(glb_graph* g, int32_t algo, int64_t source, const int64_t* dist,
+                 int64_t* n_bad, int64_t* first_bad) {
+  return guarded([&] {
+    if (!g || !dist || !n_bad || !first_bad) throw Error{GLB_EINVAL, "NULL argument"};
+    if (algo != GLB_BFS && algo != GLB_SSSP) throw Error{GLB_EINVAL, "unknown relaxation kind"};
+    if (source < 0 || source >= g->n)
+      throw Error{GLB_EINVAL, "source " + std::to_string(source) + " out of range for " +
+                                  std::to_string(g->n) + " nodes"};
+    std::lock_guard<std::mutex> lk(g->mu);
+    DeviceGuard dg(g->device);
+    long long nb = 0, fb = -1;
+    glb::validate(g, algo == GLB_SSSP && g->wt != nullptr, source, dist, &nb, &fb);
+    *n_bad = nb;
+    *first_bad = fb;
   });
 }
 
