@@ -156,12 +156,24 @@ __device__ __forceinline__ int ctl_step_kind(const DevCtrl* c) {
   return c->use_small ? (int)kModeSmall : c->mode;
 }
 
+// The loop graph's WHILE body chains kGraphUnroll SWITCH nodes (one step
+// each); every step's control sets all of their handles to the next step's
+// kind, so whichever SWITCH runs next picks it up (a finished run selects
+// kModeDone, which has no branch, for the rest of the body).
+constexpr int kGraphUnroll = 4;
+struct ModeHandles {
+  cudaGraphConditionalHandle h[kGraphUnroll];
+};
+
 __device__ __forceinline__ void ctl_set_conditionals(DevCtrl* c, cudaGraphConditionalHandle h_loop,
-                                                     cudaGraphConditionalHandle h_mode,
+                                                     const ModeHandles& h_mode,
                                                      int graph_mode) {
   if (graph_mode) {
     cudaGraphSetConditional(h_loop, c->done ? 0u : 1u);
-    if (h_mode) cudaGraphSetConditional(h_mode, (unsigned)ctl_step_kind(c));
+    const unsigned kind = (unsigned)ctl_step_kind(c);
+#pragma unroll
+    for (int u = 0; u < kGraphUnroll; ++u)
+      if (h_mode.h[u]) cudaGraphSetConditional(h_mode.h[u], kind);
   }
 }
 
@@ -204,7 +216,7 @@ __device__ __forceinline__ void ctl_reset_timers(DevCtrl* c) {
 // thread counts, record buffer, stamp generation base, scan epoch) and the
 // seed kernel has filled list 0.
 __global__ void k_control_init(DevCtrl* c, cudaGraphConditionalHandle h_loop,
-                               cudaGraphConditionalHandle h_mode, int graph_mode) {
+                               ModeHandles h_mode, int graph_mode) {
   if (threadIdx.x != 0) return;
   const int strategy = c->strategy;
   c->in = 0;
@@ -237,18 +249,23 @@ __global__ void k_control_init(DevCtrl* c, cudaGraphConditionalHandle h_loop,
   if (c->done) c->mode = kModeDone;
   c->small_exit = 0;
   c->kernels = 1;
+  c->tail_done = 0;
   ctl_check_renorm(c);
   c->use_small = small_eligible(c);
   ctl_set_conditionals(c, h_loop, h_mode, graph_mode);
 }
 
 // One warp: reduce the step's counters into a record, then transition.
-__global__ void k_control(DevCtrl* c, cudaGraphConditionalHandle h_loop,
-                          cudaGraphConditionalHandle h_mode, int graph_mode) {
-  const unsigned lane = threadIdx.x;
+// `fused`: running as the tail of the step's last kernel (ctl_tail), so no
+// control kernel of its own was launched.
+__device__ __forceinline__ void control_warp(DevCtrl* c, cudaGraphConditionalHandle h_loop,
+                                             const ModeHandles& h_mode, int graph_mode,
+                                             int fused) {
+  const unsigned lane = threadIdx.x & 31u;
   StatSlot& sl = c->ls->slot[lane];
-  unsigned long long w = sl.work, r = sl.relax, p = sl.push, mx = sl.work_max;
-  double sq = (double)sl.work_sq;
+  unsigned long long w = __ldcg(&sl.work), r = __ldcg(&sl.relax), p = __ldcg(&sl.push),
+                     mx = __ldcg(&sl.work_max);
+  double sq = (double)__ldcg(&sl.work_sq);
   sl.work = sl.relax = sl.push = sl.work_sq = sl.work_max = 0;
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) {
@@ -261,7 +278,8 @@ __global__ void k_control(DevCtrl* c, cudaGraphConditionalHandle h_loop,
   }
   if (lane != 0) return;
   // this control kernel + the step's kernels (WD: scan + relax)
-  c->kernels += c->small_exit || c->done ? 2 : (c->mode == kModeWD || c->mode == kModeHP ? 3 : 2);
+  c->kernels += (c->small_exit || c->done ? 2 : (c->mode == kModeWD || c->mode == kModeHP ? 3 : 2)) -
+                 (fused ? 1 : 0);
   const unsigned long long wd_next = c->wd_next;
   const unsigned wd_zero = c->wd_zero_next;
   if (c->small_exit) {  // k_small_loop recorded and advanced its own iterations
@@ -327,6 +345,53 @@ __global__ void k_control(DevCtrl* c, cudaGraphConditionalHandle h_loop,
   ctl_choose_dense(c);
   ctl_set_conditionals(c, h_loop, h_mode, graph_mode);
 }
+
+__global__ void k_control(DevCtrl* c, cudaGraphConditionalHandle h_loop, ModeHandles h_mode,
+                          int graph_mode) {
+  control_warp(c, h_loop, h_mode, graph_mode, 0);
+}
+
+// Control fused into the step's last kernel (graph loop): every CTA counts
+// itself out; the last one copies the control block into shared memory
+// (L2 reads: its L1 may hold lines from the kernel's start), runs
+// control_warp on the copy and writes it back.  Saves the k_control launch
+// of every iteration.  All threads of the CTA call it (CTA-uniform exits).
+struct CtlTail {
+  cudaGraphConditionalHandle h_loop;
+  ModeHandles h_mode;
+  int on;
+};
+
+__device__ __noinline__ void ctl_tail_last(const CtlTail& t, DevCtrl* g) {
+  __shared__ __align__(16) DevCtrl s_ctl;
+  constexpr unsigned kWords = sizeof(DevCtrl) / 8;
+  static_assert(sizeof(DevCtrl) % 8 == 0, "DevCtrl is copied in 8-byte words");
+  __threadfence();
+  for (unsigned i = threadIdx.x; i < kWords; i += blockDim.x)
+    reinterpret_cast<unsigned long long*>(&s_ctl)[i] =
+        __ldcg(reinterpret_cast<const unsigned long long*>(g) + i);
+  __syncthreads();
+  if (threadIdx.x < 32) control_warp(&s_ctl, t.h_loop, t.h_mode, 1, 1);
+  __syncthreads();
+  if (threadIdx.x == 0) s_ctl.tail_done = 0;
+  __syncthreads();
+  for (unsigned i = threadIdx.x; i < kWords; i += blockDim.x)
+    reinterpret_cast<unsigned long long*>(g)[i] = reinterpret_cast<unsigned long long*>(&s_ctl)[i];
+}
+
+__device__ __forceinline__ void ctl_tail(const CtlTail& t, DevCtrl* g) {
+  if (!t.on) return;
+  __shared__ int s_last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned total = gridDim.x * gridDim.y * gridDim.z;
+    s_last = atomicAdd(&g->tail_done, 1u) == total - 1u;
+  }
+  __syncthreads();
+  if (s_last) ctl_tail_last(t, g);
+}
+
 
 // Resume a paused sharded run: the deferred worklist swap / super-iteration
 // switch.  Global termination is the host's all-reduce, not `produced`.

@@ -166,6 +166,11 @@ class Runner {
   LookbackState<2> lb_{};
   // grids
   int cap_relax_ = 0, cap_scan_ = 0, cap_wd_ = 0, cap_hp_ = 0;
+  // graph loop: the control step runs as the tail of each step's last kernel
+  CtlTail tail_{0, {}, 0};
+  bool fused_ctl_ = getenv("GLB_NO_FUSED_CTL") == nullptr;
+  int unroll_ = getenv("GLB_GRAPH_UNROLL") ? std::max(1, std::min(kGraphUnroll, atoi(getenv("GLB_GRAPH_UNROLL"))))
+                                           : kGraphUnroll;
   double setup_ms_ = 0;
   long long seed_count_ = 0;
   bool shard_mode_ = false;
@@ -350,7 +355,8 @@ class Runner {
   // 24-bit tier: retag every cell (see ctl_check_renorm)
   void launch_renorm() {
     if constexpr (Cell<D>::kGenBits == 8) {
-      k_renorm<<<grid_for(n_all_, kBlock, g_->num_sms * 8), kBlock, 0, s_>>>(cells_, n_all_);
+      k_renorm<<<grid_for(n_all_, kBlock, g_->num_sms * 8), kBlock, 0, s_>>>(cells_, n_all_, ctrl_,
+                                                                             tail_);
       GLB_CHECK_LAUNCH();
     } else {
       throw Error{GLB_ECUDA, "renormalisation requested for a 32-bit-tag run"};
@@ -360,13 +366,13 @@ class Runner {
   void launch_relax(unsigned grid) {
     const Relaxer<D, W> rx = relaxer();
     switch (p_.strategy) {
-      case GLB_BS: k_bs_relax<D, W><<<grid, kBlock, 0, s_>>>(row_, rx, ctrl_); break;
-      case GLB_NS: k_ns_relax<D, W><<<grid, kBlock, 0, s_>>>(row_, cs_, g_->n, rx, ctrl_); break;
+      case GLB_BS: k_bs_relax<D, W><<<grid, kBlock, 0, s_>>>(row_, rx, ctrl_, tail_); break;
+      case GLB_NS: k_ns_relax<D, W><<<grid, kBlock, 0, s_>>>(row_, cs_, g_->n, rx, ctrl_, tail_); break;
       case GLB_EP:
         if (p_.chunked)
-          k_ep_relax<D, W, true><<<grid, kBlock, 0, s_>>>(row_, src_, rx, ctrl_);
+          k_ep_relax<D, W, true><<<grid, kBlock, 0, s_>>>(row_, src_, rx, ctrl_, tail_);
         else
-          k_ep_relax<D, W, false><<<grid, kBlock, 0, s_>>>(row_, src_, rx, ctrl_);
+          k_ep_relax<D, W, false><<<grid, kBlock, 0, s_>>>(row_, src_, rx, ctrl_, tail_);
         break;
       default: throw Error{GLB_EINVAL, "no relax kernel for this strategy"};
     }
@@ -378,23 +384,22 @@ class Runner {
     GLB_CHECK_LAUNCH();
   }
   void launch_wd_relax(unsigned grid) {
-    k_wd_relax<D, W><<<grid, kBlock, 0, s_>>>(relaxer(), row_,
-                                               ctrl_);
+    k_wd_relax<D, W><<<grid, kBlock, 0, s_>>>(relaxer(), row_, ctrl_, tail_);
     GLB_CHECK_LAUNCH();
   }
   void launch_hp(unsigned grid) {
     k_hp_window<D, W><<<grid, kBlock, 0, s_>>>(row_, relaxer(), ctrl_);
     GLB_CHECK_LAUNCH();
-    k_hp_bigbin<D, W><<<cap_hp_, kBlock, 0, s_>>>(relaxer(), ctrl_);
+    k_hp_bigbin<D, W><<<cap_hp_, kBlock, 0, s_>>>(relaxer(), ctrl_, tail_);
     GLB_CHECK_LAUNCH();
   }
   void launch_small() {
     k_small_loop<D, W><<<kSmallCtas, kSmallThreads, small_smem_bytes<D>(), s_>>>(
         row_, p_.strategy == GLB_NS ? cs_ : nullptr, g_->n,
-        p_.strategy == GLB_EP ? src_ : nullptr, p_.chunked != 0, relaxer(), ctrl_);
+        p_.strategy == GLB_EP ? src_ : nullptr, p_.chunked != 0, relaxer(), ctrl_, tail_);
     GLB_CHECK_LAUNCH();
   }
-  void launch_control(cudaGraphConditionalHandle hl, cudaGraphConditionalHandle hm, int gm) {
+  void launch_control(cudaGraphConditionalHandle hl, const ModeHandles& hm, int gm) {
     k_control<<<1, 32, 0, s_>>>(ctrl_, hl, hm, gm);
     GLB_CHECK_LAUNCH();
   }
@@ -407,7 +412,7 @@ class Runner {
 
   // ------------------------------------------------------- host loop ---
   void loop_host() {
-    k_control_init<<<1, 32, 0, s_>>>(ctrl_, 0, 0, 0);
+    k_control_init<<<1, 32, 0, s_>>>(ctrl_, 0, ModeHandles{}, 0);
     GLB_CHECK_LAUNCH();
     read_ctrl();
     step_host();
@@ -478,7 +483,7 @@ class Runner {
         default: throw Error{GLB_ECUDA, "control block in an unknown mode"};
       }
       const bool small = c.use_small != 0;
-      launch_control(0, 0, 0);
+      launch_control(0, ModeHandles{}, 0);
       read_ctrl();
       if (small) {  // several iterations in one launch: per-record device timers
         for (unsigned r = nrec0; r < h_->ctrl.nrec; ++r)
@@ -492,7 +497,7 @@ class Runner {
   // ----------------------------------------------------- graph loop ---
   std::string graph_key() const {
     std::ostringstream k;
-    k << g_->device << '|' << p_.strategy << '|' << Cell<D>::kDistBits << '|' << W << '|' << p_.chunked << '|' << cap_relax_
+    k << g_->device << '|' << p_.strategy << '|' << fused_ctl_ << '|' << unroll_ << '|' << Cell<D>::kDistBits << '|' << W << '|' << p_.chunked << '|' << cap_relax_
       << '|' << cap_scan_ << '|' << cap_wd_ << '|' << cap_hp_ << '|' << (const void*)row_ << '|'
       << (const void*)col_ << '|' << (const void*)wt_ << '|' << (const void*)cs_ << '|'
       << (const void*)src_ << '|' << (const void*)cells_ << '|' << (const void*)stamp_ << '|'
@@ -523,9 +528,13 @@ class Runner {
     cudaGraph_t graph;
     GLB_CUDA_TRY(cudaGraphCreate(&graph, 0));
     try {
-      cudaGraphConditionalHandle h_loop = 0, h_mode = 0;
+      // fused control: kGraphUnroll SWITCH steps per WHILE iteration
+      const int unroll = fused_ctl_ ? unroll_ : 1;
+      cudaGraphConditionalHandle h_loop = 0;
+      ModeHandles h_mode{};
       GLB_CUDA_TRY(cudaGraphConditionalHandleCreate(&h_loop, graph, 0, 0));
-      GLB_CUDA_TRY(cudaGraphConditionalHandleCreate(&h_mode, graph, 0, 0));
+      for (int u = 0; u < unroll; ++u)
+        GLB_CUDA_TRY(cudaGraphConditionalHandleCreate(&h_mode.h[u], graph, 0, 0));
       capture_into(graph, nullptr, 0);
       k_control_init<<<1, 32, 0, s_>>>(ctrl_, h_loop, h_mode, 1);
       GLB_CHECK_LAUNCH();
@@ -544,51 +553,59 @@ class Runner {
 
       // SWITCH on the step kind (StepMode): the strategy's grid kernels or
       // the CTA-resident small-frontier loop
-      alignas(cudaGraphNodeParams) unsigned char sbuf[sizeof(cudaGraphNodeParams)] = {};
-      cudaGraphNodeParams& sp = *reinterpret_cast<cudaGraphNodeParams*>(sbuf);
-      sp.type = cudaGraphNodeTypeConditional;
-      sp.conditional.handle = h_mode;
-      sp.conditional.type = cudaGraphCondTypeSwitch;
-      sp.conditional.size = kNumModes;
-      cudaGraphNode_t snode;
-      GLB_CUDA_TRY(cudaGraphAddNode(&snode, body, nullptr, 0, &sp));
-      if (p_.strategy == GLB_WD || p_.strategy == GLB_HP) {
-        capture_into(sp.conditional.phGraph_out[kModeWD], nullptr, 0);
-        launch_wd_scan(cap_scan_);
-        launch_wd_relax(cap_wd_);
+      if (fused_ctl_) tail_ = CtlTail{h_loop, h_mode, 1};
+      cudaGraphNode_t snode = nullptr;
+      for (int u = 0; u < unroll; ++u) {
+        alignas(cudaGraphNodeParams) unsigned char sbuf[sizeof(cudaGraphNodeParams)] = {};
+        cudaGraphNodeParams& sp = *reinterpret_cast<cudaGraphNodeParams*>(sbuf);
+        sp.type = cudaGraphNodeTypeConditional;
+        sp.conditional.handle = h_mode.h[u];
+        sp.conditional.type = cudaGraphCondTypeSwitch;
+        sp.conditional.size = kNumModes;
+        cudaGraphNode_t prev = snode;
+        GLB_CUDA_TRY(cudaGraphAddNode(&snode, body, prev ? &prev : nullptr, prev ? 1 : 0, &sp));
+        if (p_.strategy == GLB_WD || p_.strategy == GLB_HP) {
+          capture_into(sp.conditional.phGraph_out[kModeWD], nullptr, 0);
+          launch_wd_scan(cap_scan_);
+          launch_wd_relax(cap_wd_);
+          end_capture();
+        }
+        if (p_.strategy == GLB_WD) {
+          capture_into(sp.conditional.phGraph_out[kModeWDF], nullptr, 0);
+          launch_wd_relax(cap_wd_);
+          end_capture();
+        }
+        if (p_.strategy == GLB_HP) {
+          capture_into(sp.conditional.phGraph_out[kModeHP], nullptr, 0);
+          launch_hp(cap_hp_);
+          end_capture();
+        }
+        if (relax_kernel()) {
+          capture_into(sp.conditional.phGraph_out[kModeRelax], nullptr, 0);
+          launch_relax(cap_relax_);
+          end_capture();
+        }
+        capture_into(sp.conditional.phGraph_out[kModeSmall], nullptr, 0);
+        launch_small();
+        end_capture();
+        if (Cell<D>::kGenBits == 8) {
+          capture_into(sp.conditional.phGraph_out[kModeRenorm], nullptr, 0);
+          launch_renorm();
+          end_capture();
+        }
+      }
+      tail_ = CtlTail{0, {}, 0};
+      if (!fused_ctl_) {
+        capture_into(body, &snode, 1);
+        launch_control(h_loop, h_mode, 1);
         end_capture();
       }
-      if (p_.strategy == GLB_WD) {
-        capture_into(sp.conditional.phGraph_out[kModeWDF], nullptr, 0);
-        launch_wd_relax(cap_wd_);
-        end_capture();
-      }
-      if (p_.strategy == GLB_HP) {
-        capture_into(sp.conditional.phGraph_out[kModeHP], nullptr, 0);
-        launch_hp(cap_hp_);
-        end_capture();
-      }
-      if (relax_kernel()) {
-        capture_into(sp.conditional.phGraph_out[kModeRelax], nullptr, 0);
-        launch_relax(cap_relax_);
-        end_capture();
-      }
-      capture_into(sp.conditional.phGraph_out[kModeSmall], nullptr, 0);
-      launch_small();
-      end_capture();
-      if (Cell<D>::kGenBits == 8) {
-        capture_into(sp.conditional.phGraph_out[kModeRenorm], nullptr, 0);
-        launch_renorm();
-        end_capture();
-      }
-      capture_into(body, &snode, 1);
-      launch_control(h_loop, h_mode, 1);
-      end_capture();
       cudaGraphExec_t exec;
       GLB_CUDA_TRY(cudaGraphInstantiate(&exec, graph, 0));
       cudaGraphDestroy(graph);
       return exec;
     } catch (...) {
+      tail_ = CtlTail{0, {}, 0};
       cudaStreamCaptureStatus cs;
       if (cudaStreamIsCapturing(s_, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone) {
         cudaGraph_t junk = nullptr;
@@ -785,7 +802,7 @@ class ShardSession : public ShardSessionBase, public Runner<uint32_t, W> {
     R::prepare(&stats_);
     if (p.source < lo_ || p.source >= hi_)  // not ours: start with an empty frontier
       GLB_CUDA_TRY(cudaMemsetAsync(&this->ctrl_->qcount[0], 0, 4, this->s_));
-    k_control_init<<<1, 32, 0, this->s_>>>(this->ctrl_, 0, 0, 0);
+    k_control_init<<<1, 32, 0, this->s_>>>(this->ctrl_, 0, ModeHandles{}, 0);
     GLB_CHECK_LAUNCH();
     this->read_ctrl();
     counts_ = (unsigned long long*)ensure(g->ws.misc_small, 64 * 8 * 2);

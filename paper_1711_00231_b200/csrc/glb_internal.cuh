@@ -248,6 +248,8 @@ struct DevCtrl {
   unsigned int nrec, rec_cap;
   DevRecord* recs;
   struct LaunchStats* ls;
+  unsigned int tail_done;       // CTAs of the step's last kernel that finished (ctl_tail)
+  unsigned int tail_pad;
 };
 
 // --------------------------------------------------------- device graph ---

@@ -32,6 +32,7 @@
 
 #include <cub/block/block_scan.cuh>
 
+#include "glb_control.cuh"
 #include "glb_internal.cuh"
 #include "glb_scan.cuh"
 
@@ -291,11 +292,15 @@ __device__ __forceinline__ void relax_range_coop(const Relaxer<D, W>& rx, BlockQ
 // ============================================================ BS (K1) ===
 template <typename D, bool W>
 __global__ void __launch_bounds__(kBlock) k_bs_relax(const long long* __restrict__ row,
-                                                     Relaxer<D, W> rx0, DevCtrl* ctrl) {
+                                                     Relaxer<D, W> rx0, DevCtrl* ctrl,
+                                                     CtlTail tail) {
   __shared__ uint32_t s_q[kQCap];
   __shared__ BlockQ bq;
   const unsigned n = ctrl->qcount[ctrl->in];
-  if (blockIdx.x * kBlock >= n) return;  // idle CTA: no barriers, no atomics
+  if (blockIdx.x * kBlock >= n) {  // idle CTA: no barriers, no atomics
+    ctl_tail(tail, ctrl);
+    return;
+  }
   timer_begin(ctrl->t_relax);
   bq_init(bq, s_q);
   const Relaxer<D, W> rx = bind(rx0, ctrl);
@@ -312,6 +317,7 @@ __global__ void __launch_bounds__(kBlock) k_bs_relax(const long long* __restrict
   }
   flush_counters(ctrl->ls, c);
   timer_end(ctrl->t_relax);
+  ctl_tail(tail, ctrl);
 }
 
 // ============================================================ NS (K9) ===
@@ -320,11 +326,14 @@ template <typename D, bool W>
 __global__ void __launch_bounds__(kBlock) k_ns_relax(const long long* __restrict__ row,
                                                      const long long* __restrict__ cs,
                                                      long long n_orig, Relaxer<D, W> rx0,
-                                                     DevCtrl* ctrl) {
+                                                     DevCtrl* ctrl, CtlTail tail) {
   __shared__ uint32_t s_q[kQCap];
   __shared__ BlockQ bq;
   const unsigned n = ctrl->qcount[ctrl->in];
-  if (blockIdx.x * kBlock >= n) return;  // idle CTA: no barriers, no atomics
+  if (blockIdx.x * kBlock >= n) {  // idle CTA: no barriers, no atomics
+    ctl_tail(tail, ctrl);
+    return;
+  }
   timer_begin(ctrl->t_relax);
   bq_init(bq, s_q);
   const Relaxer<D, W> rx = bind(rx0, ctrl);
@@ -374,6 +383,7 @@ __global__ void __launch_bounds__(kBlock) k_ns_relax(const long long* __restrict
   }
   flush_counters(ctrl->ls, c);
   timer_end(ctrl->t_relax);
+  ctl_tail(tail, ctrl);
 }
 
 // ============================================================ EP (K2) ===
@@ -393,10 +403,14 @@ struct EpRanges {
 template <typename D, bool W, bool CHUNKED>
 __global__ void __launch_bounds__(kBlock) k_ep_relax(const long long* __restrict__ row,
                                                      const uint32_t* __restrict__ src,
-                                                     Relaxer<D, W> rx0, DevCtrl* ctrl) {
+                                                     Relaxer<D, W> rx0, DevCtrl* ctrl,
+                                                     CtlTail tail) {
   __shared__ EpRanges rg;
   const unsigned n = ctrl->qcount[ctrl->in];
-  if (blockIdx.x * kBlock >= n) return;  // idle CTA
+  if (blockIdx.x * kBlock >= n) {  // idle CTA
+    ctl_tail(tail, ctrl);
+    return;
+  }
   timer_begin(ctrl->t_relax);
   if (threadIdx.x == 0) rg.count = rg.total = 0;
   __syncthreads();
@@ -493,6 +507,7 @@ __global__ void __launch_bounds__(kBlock) k_ep_relax(const long long* __restrict
   }
   flush_counters(ctrl->ls, c);
   timer_end(ctrl->t_relax);
+  ctl_tail(tail, ctrl);
 }
 
 // ====================================================== WD (K4 + K5/K6) ===
@@ -720,7 +735,7 @@ struct WdMeta {
 
 template <typename D, bool W>
 __global__ void __launch_bounds__(kBlock, GLB_WD_MINB) k_wd_relax(
-    Relaxer<D, W> rx0, const long long* __restrict__ row, DevCtrl* ctrl) {
+    Relaxer<D, W> rx0, const long long* __restrict__ row, DevCtrl* ctrl, CtlTail tail) {
   const WdItem* __restrict__ items = reinterpret_cast<const WdItem*>(ctrl->wd_items_buf[ctrl->wd_cur]);
   const unsigned int* __restrict__ tile_first = ctrl->wd_tf_buf[ctrl->wd_cur];
   const bool fused = ctrl->wd_fused != 0;
@@ -731,7 +746,10 @@ __global__ void __launch_bounds__(kBlock, GLB_WD_MINB) k_wd_relax(
   const long long total = ctrl->wd_total;
   const long long nitems = ctrl->wd_items;
   const long long ntiles = (total + kWdTile - 1) / kWdTile;
-  if ((long long)blockIdx.x * kWdWarps >= ntiles) return;  // idle CTA
+  if ((long long)blockIdx.x * kWdWarps >= ntiles) {  // idle CTA
+    ctl_tail(tail, ctrl);
+    return;
+  }
   timer_begin(ctrl->t_relax);
   const Relaxer<D, W> rx = bind(rx0, ctrl);
   const unsigned lane = lane_id();
@@ -941,6 +959,7 @@ __global__ void __launch_bounds__(kBlock, GLB_WD_MINB) k_wd_relax(
   c.push = n_push;
   flush_counters(ctrl->ls, c);
   timer_end(ctrl->t_relax);
+  ctl_tail(tail, ctrl);
 }
 
 // ============================================================ HP (K10) ===
@@ -1058,7 +1077,7 @@ __global__ void __launch_bounds__(kBlock, GLB_RELAX_MINB) k_hp_window(const long
 // windows' first pieces (cached in shared memory).
 template <typename D, bool W>
 __global__ void __launch_bounds__(kBlock, GLB_RELAX_MINB) k_hp_bigbin(Relaxer<D, W> rx0,
-                                                                      DevCtrl* ctrl) {
+                                                                      DevCtrl* ctrl, CtlTail tail) {
   __shared__ uint32_t s_q[kQCap];
   __shared__ BlockQ bq;
   __shared__ long long s_lo, s_hi;
@@ -1067,7 +1086,10 @@ __global__ void __launch_bounds__(kBlock, GLB_RELAX_MINB) k_hp_bigbin(Relaxer<D,
   __shared__ unsigned s_qb[kHpQbCache];  // first piece of every CTA-bin window
   const unsigned long long bc = ctrl->hp_big_ctr;
   const unsigned nbig = (unsigned)(bc >> 32), npieces = (unsigned)bc;
-  if (npieces == 0 || blockIdx.x >= npieces) return;
+  if (npieces == 0 || blockIdx.x >= npieces) {
+    ctl_tail(tail, ctrl);
+    return;
+  }
   timer_begin(ctrl->t_relax);
   bq_init(bq, s_q);
   const Relaxer<D, W> rx = bind(rx0, ctrl);
@@ -1105,6 +1127,7 @@ __global__ void __launch_bounds__(kBlock, GLB_RELAX_MINB) k_hp_bigbin(Relaxer<D,
   }
   flush_counters(ctrl->ls, c);
   timer_end(ctrl->t_relax);
+  ctl_tail(tail, ctrl);
 }
 
 // ============================================================ setup ===
@@ -1152,10 +1175,11 @@ __global__ void k_dist_u32(const CellS<D>* __restrict__ cells, long long n,
 
 // 24-bit tier: every tag is reset to 0 ("no generation") before a
 // generation that is a multiple of 128 starts (Cell<dist24_t>).
-__global__ void k_renorm(uint32_t* __restrict__ cells, long long n) {
+__global__ void k_renorm(uint32_t* __restrict__ cells, long long n, DevCtrl* ctrl, CtlTail tail) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x)
     cells[i] &= ~0xFFu;
+  ctl_tail(tail, ctrl);
 }
 
 template <typename D>

@@ -170,7 +170,7 @@ template <typename D, bool W>
 __global__ void __cluster_dims__(kSmallCtas, 1, 1) __launch_bounds__(kSmallThreads, 1)
     k_small_loop(const long long* __restrict__ row, const long long* __restrict__ cs,
                  long long n_orig, const uint32_t* __restrict__ ep_src, bool ep_chunked,
-                 Relaxer<D, W> rx0, DevCtrl* gctrl) {
+                 Relaxer<D, W> rx0, DevCtrl* gctrl, CtlTail tail) {
   extern __shared__ __align__(16) unsigned char s_dyn[];
   D* s_dn = reinterpret_cast<D*>(s_dyn);                                   // [kSmallItems]
   uint32_t* s_pre = reinterpret_cast<uint32_t*>(s_dyn + kSmallItems * sizeof(D));  // [+1]
@@ -501,6 +501,10 @@ __global__ void __cluster_dims__(kSmallCtas, 1, 1) __launch_bounds__(kSmallThrea
     sc.use_small = 0;
     ctl_reset_timers(&sc);
     *gctrl = sc;
+  }
+  if (tail.on) {
+    cluster.sync();  // the control block is written back before any CTA counts itself out
+    ctl_tail(tail, gctrl);
   }
 }
 
