@@ -17,10 +17,15 @@ from oracle import oracle  # noqa: E402
 from tests import graph_specs as gs  # noqa: E402
 
 oracle.build()
-graphs = [gs.build(pkg, gs.CORPUS[k]) for k in ("rmat10_skew", "quirks", "grid24", "degrees", "er_empty")]
-graphs.append(pkg.generate_rmat(13, 8, seed=2, max_weight=255))
-variants = [{}, {"GLB_NO_SMALL": "1"}, {"GLB_NO_SMALL": "1", "GLB_WD_FUSED": "1"},
-            {"GLB_NO_SMALL": "1", "GLB_WD_DENSE": "1"}]
+QUICK = "--quick" in sys.argv  # racecheck-sized: fewer graphs and variants
+if QUICK:
+    graphs = [gs.build(pkg, gs.CORPUS[k]) for k in ("rmat10_skew", "quirks")]
+    variants = [{}, {"GLB_NO_SMALL": "1"}]
+else:
+    graphs = [gs.build(pkg, gs.CORPUS[k]) for k in ("rmat10_skew", "quirks", "grid24", "degrees", "er_empty")]
+    graphs.append(pkg.generate_rmat(13, 8, seed=2, max_weight=255))
+    variants = [{}, {"GLB_NO_SMALL": "1"}, {"GLB_NO_SMALL": "1", "GLB_WD_FUSED": "1"},
+                {"GLB_NO_SMALL": "1", "GLB_WD_DENSE": "1"}]
 bad = 0
 for var in variants:
     for k in ("GLB_NO_SMALL", "GLB_WD_FUSED", "GLB_WD_DENSE"):
@@ -35,4 +40,26 @@ for var in variants:
                     if not np.array_equal(r.dist.array, exp):
                         bad += 1
                         print("MISMATCH", var, g.num_nodes, algo, tag, loop)
+# 24-bit tier across renormalisations (> 256 generations), both loops, and
+# the device distance certificate
+for k in ("GLB_NO_SMALL", "GLB_WD_FUSED", "GLB_WD_DENSE"):
+    os.environ.pop(k, None)
+long_path = pkg.path_graph(300 if QUICK else 700, weighted=True, seed=3)
+for var in ({}, {"GLB_NO_SMALL": "1"}):
+    os.environ.pop("GLB_NO_SMALL", None)
+    os.environ.update(var)
+    for algo in ("bfs", "sssp"):
+        exp = oracle.oracle_distances(long_path, 0, algo)
+        for tag in (("BS", "WD", "HP") if QUICK else pkg.STRATEGY_TAGS):
+            for loop in ("host", "graph"):
+                r = pkg.run_strategy(tag, long_path, 0, pkg.RelaxOp(algo),
+                                     pkg.KernelConfig(loop=loop, dist_bits=24))
+                if not np.array_equal(r.dist.array, exp):
+                    bad += 1
+                    print("MISMATCH 24-bit", var, algo, tag, loop)
+for g in graphs[:3]:
+    exp = oracle.oracle_distances(g, 0, "sssp")
+    if not pkg.validate_distances(g, 0, "sssp", exp).matched:
+        bad += 1
+        print("CERTIFICATE rejected a correct array", g.num_nodes)
 print("sanitize workload done, mismatches:", bad)
