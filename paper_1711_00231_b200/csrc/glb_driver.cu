@@ -169,6 +169,7 @@ class Runner {
   // graph loop: the control step runs as the tail of each step's last kernel
   CtlTail tail_{0, {}, 0};
   bool fused_ctl_ = getenv("GLB_NO_FUSED_CTL") == nullptr;
+  bool pdl_ = getenv("GLB_NO_PDL") == nullptr;
   int unroll_ = getenv("GLB_GRAPH_UNROLL") ? std::max(1, std::min(kGraphUnroll, atoi(getenv("GLB_GRAPH_UNROLL"))))
                                            : kGraphUnroll;
   double setup_ms_ = 0;
@@ -384,13 +385,28 @@ class Runner {
     GLB_CHECK_LAUNCH();
   }
   void launch_wd_relax(unsigned grid) {
-    k_wd_relax<D, W><<<grid, kBlock, 0, s_>>>(relaxer(), row_, ctrl_, tail_);
+    launch_dependent(k_wd_relax<D, W>, grid, relaxer(), row_, ctrl_, tail_);
     GLB_CHECK_LAUNCH();
+  }
+  // second kernel of a step: programmatic dependent launch on the first
+  template <typename... KArgs, typename... Args>
+  void launch_dependent(void (*kernel)(KArgs...), unsigned grid, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kBlock);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = s_;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl_ ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    GLB_CUDA_TRY(cudaLaunchKernelEx(&cfg, kernel, args...));
   }
   void launch_hp(unsigned grid) {
     k_hp_window<D, W><<<grid, kBlock, 0, s_>>>(row_, relaxer(), ctrl_);
     GLB_CHECK_LAUNCH();
-    k_hp_bigbin<D, W><<<cap_hp_, kBlock, 0, s_>>>(relaxer(), ctrl_, tail_);
+    launch_dependent(k_hp_bigbin<D, W>, (unsigned)cap_hp_, relaxer(), ctrl_, tail_);
     GLB_CHECK_LAUNCH();
   }
   void launch_small() {
@@ -497,7 +513,7 @@ class Runner {
   // ----------------------------------------------------- graph loop ---
   std::string graph_key() const {
     std::ostringstream k;
-    k << g_->device << '|' << p_.strategy << '|' << fused_ctl_ << '|' << unroll_ << '|' << Cell<D>::kDistBits << '|' << W << '|' << p_.chunked << '|' << cap_relax_
+    k << g_->device << '|' << p_.strategy << '|' << fused_ctl_ << '|' << unroll_ << '|' << pdl_ << '|' << Cell<D>::kDistBits << '|' << W << '|' << p_.chunked << '|' << cap_relax_
       << '|' << cap_scan_ << '|' << cap_wd_ << '|' << cap_hp_ << '|' << (const void*)row_ << '|'
       << (const void*)col_ << '|' << (const void*)wt_ << '|' << (const void*)cs_ << '|'
       << (const void*)src_ << '|' << (const void*)cells_ << '|' << (const void*)stamp_ << '|'

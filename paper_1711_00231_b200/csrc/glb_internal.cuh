@@ -348,6 +348,12 @@ inline unsigned int grid_for(long long items, int per_block, int cap) {
 // ------------------------------------------------------ device helpers ---
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
 
+// Programmatic dependent launch: a step's first kernel lets the second one
+// launch early (its CTAs wait in griddepcontrol.wait until the first grid has
+// finished and its writes are visible), hiding the second launch's latency.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 #ifndef GLB_STREAM_POLICY
 #define GLB_STREAM_POLICY 1  // evict-first L2 policy on the col / weight streams
 #endif

@@ -533,6 +533,7 @@ template <typename D>
 __global__ void __launch_bounds__(kBlock) k_wd_scan(const long long* __restrict__ row,
                                                     const CellS<D>* __restrict__ cells,
                                                     LookbackState<2> lb, DevCtrl* ctrl) {
+  pdl_trigger();
   WdItem* __restrict__ items = reinterpret_cast<WdItem*>(ctrl->wd_items_buf[ctrl->wd_cur]);
   unsigned int* __restrict__ tile_first = ctrl->wd_tf_buf[ctrl->wd_cur];
   using TS = TileScan<2, kBlock>;
@@ -736,6 +737,7 @@ struct WdMeta {
 template <typename D, bool W>
 __global__ void __launch_bounds__(kBlock, GLB_WD_MINB) k_wd_relax(
     Relaxer<D, W> rx0, const long long* __restrict__ row, DevCtrl* ctrl, CtlTail tail) {
+  pdl_wait();
   const WdItem* __restrict__ items = reinterpret_cast<const WdItem*>(ctrl->wd_items_buf[ctrl->wd_cur]);
   const unsigned int* __restrict__ tile_first = ctrl->wd_tf_buf[ctrl->wd_cur];
   const bool fused = ctrl->wd_fused != 0;
@@ -975,6 +977,7 @@ constexpr int kHpQbCache = 2048;      // CTA-bin windows whose piece index is ca
 template <typename D, bool W>
 __global__ void __launch_bounds__(kBlock, GLB_RELAX_MINB) k_hp_window(const long long* __restrict__ row,
                                                       Relaxer<D, W> rx0, DevCtrl* ctrl) {
+  pdl_trigger();
   using BScan = cub::BlockScan<int, kBlock, cub::BLOCK_SCAN_WARP_SCANS>;
   __shared__ uint32_t s_q[kQCap];
   __shared__ BlockQ bq;
@@ -1078,6 +1081,7 @@ __global__ void __launch_bounds__(kBlock, GLB_RELAX_MINB) k_hp_window(const long
 template <typename D, bool W>
 __global__ void __launch_bounds__(kBlock, GLB_RELAX_MINB) k_hp_bigbin(Relaxer<D, W> rx0,
                                                                       DevCtrl* ctrl, CtlTail tail) {
+  pdl_wait();
   __shared__ uint32_t s_q[kQCap];
   __shared__ BlockQ bq;
   __shared__ long long s_lo, s_hi;
