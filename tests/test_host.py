@@ -65,6 +65,8 @@ def test_c_abi_rejects_bad_arguments_without_a_device():
     assert L.glb_inclusive_scan(_lib.ptr64(v), -1, _lib.ptr64(v), 0) == _lib.GLB_EINVAL
     assert L.glb_find_offsets(_lib.ptr64(v), 2, 0, 4, _lib.ptr64(v), _lib.ptr64(v), 0) == _lib.GLB_EINVAL
     assert L.glb_measure_gather(None, None) == _lib.GLB_EINVAL
+    nb, fb = ctypes.c_int64(), ctypes.c_int64()
+    assert L.glb_validate(None, 0, 0, _lib.ptr64(v), ctypes.byref(nb), ctypes.byref(fb)) == _lib.GLB_EINVAL
     n = ctypes.c_int(-1)
     assert L.glb_device_count(ctypes.byref(n)) == _lib.GLB_OK and n.value >= 0
     assert L.glb_version().decode()
@@ -123,6 +125,8 @@ def test_kernel_config_and_resolve_threads():
         pkg.KernelConfig(loop="bogus")
     with pytest.raises(ValueError):
         pkg.KernelConfig(dist_bits=16)
+    for bits in (0, 24, 32, 64):
+        assert pkg.KernelConfig(dist_bits=bits).dist_bits == bits
     cfg = pkg.KernelConfig()
     # engine.py:63-70: min(2^14, ceil(items / block) * block), at least one block
     assert pkg.resolve_threads(cfg, 0) == 1024
