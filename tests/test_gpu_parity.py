@@ -28,11 +28,16 @@ def need_gpu():
 
 # Execution variants of the same strategies: the CTA-cluster small-frontier
 # loop (default; it takes every iteration of these small graphs), the
-# grid-wide kernels alone (GLB_NO_SMALL), and WD's fused item pushes.
+# grid-wide kernels alone (GLB_NO_SMALL), WD's fused item pushes and dense
+# scans, and the graph-loop structure knobs.
 VARIANTS = {"default": {}, "grid_kernels": {"GLB_NO_SMALL": "1"},
             "wd_fused": {"GLB_WD_FUSED": "1"},
             "grid_fused": {"GLB_NO_SMALL": "1", "GLB_WD_FUSED": "1"},
-            "grid_dense": {"GLB_NO_SMALL": "1", "GLB_WD_DENSE": "1"}}
+            "grid_dense": {"GLB_NO_SMALL": "1", "GLB_WD_DENSE": "1"},
+            # graph-loop structure knobs: separate control kernel, one step per
+            # WHILE iteration without programmatic dependent launch
+            "grid_ctl_kernel": {"GLB_NO_SMALL": "1", "GLB_NO_FUSED_CTL": "1"},
+            "grid_unroll1_nopdl": {"GLB_NO_SMALL": "1", "GLB_GRAPH_UNROLL": "1", "GLB_NO_PDL": "1"}}
 
 
 @pytest.mark.parametrize("variant", list(VARIANTS))
