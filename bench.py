@@ -1,20 +1,30 @@
 #!/usr/bin/env python
-"""GTEPS of the B200 BFS/SSSP task-distribution path (BASELINE.json config C2).
+"""GTEPS of the B200 BFS/SSSP task-distribution path (BASELINE.json).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-A step is one SSSP traversal from source 0 of RMAT scale-22, edge factor 16
-(default R-MAT params, seed 1, integer weights 1..255) with the headline
-strategy, graph already resident in HBM.  `value` = E_r / device time per step
-(E_r = sum of outdegrees over reached vertices, Graph500-style), whole-job
-over all ranks.  `e2e` measures the same traversal through the C-ABI with host
-buffers: glb_graph_create (host int64 CSR -> HBM) + glb_run + the int64
-distances back to the host + glb_graph_destroy.
+N = 1 (config C2): a step is one SSSP traversal from source 0 of RMAT
+scale-22, edge factor 16 (default R-MAT params, seed 1, integer weights
+1..255) with the headline strategy (WD), graph resident in HBM.
+N > 1 (config C5): a step is one traversal of RMAT scale-27 (2^31 edges) from
+source 0, 1-D edge-balanced vertex partition over the N GPUs, NCCL exchange of
+(dist << 32 | v) updates per BSP iteration -- the same graph at every N
+(strong scaling).  `--gpus N` without torchrun's environment launches the N
+ranks itself (torch.distributed.run on 127.0.0.1).
 
-`--impl reference` times the reference's CPU algorithm on the host cores: the
-reference is pure Python (not compilable), so the pinned C port of its
-node-based strategy (oracle/graphlb_oracle.c, oracle_bs_run) runs with every
-host thread.  Under torchrun only rank 0 runs it.
+`value` = E_r / device time per step (E_r = sum of outdegrees over reached
+vertices, Graph500-style), whole job, max over ranks.  `e2e` measures the same
+traversal through the C-ABI with host buffers: glb_graph_create (host int64
+CSR -> HBM) + glb_run + the int64 distances back + glb_graph_destroy.
+`roofline.frac` is SURVEY 8(d)'s one-pass algorithmic bytes of the traversal
+(12 E_r + 20 N_r for SSSP, 8 E_r + 20 N_r for BFS) over the dominant kernel's
+time per step, against the measured HBM peak (x N).
+
+`--impl reference` times the reference's CPU algorithm on the host cores, in a
+process that never loads the CUDA library: the reference is pure Python, so
+the pinned C port of its node-based strategy (oracle/, oracle_bs_run_u32) runs
+on every host thread over the graph built by the pinned C restatement of
+generate_rmat (oracle_rmat_u32).  Under torchrun only rank 0 runs it.
 """
 
 from __future__ import annotations
@@ -23,6 +33,7 @@ import argparse
 import ctypes
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -38,6 +49,9 @@ BASELINE = json.loads((ROOT / "BASELINE.json").read_text())
 METRIC = BASELINE["metric"]
 UNIT = "GTEPS"
 TAGS = ("BS", "EP", "WD", "NS", "HP")
+INF = (1 << 63) - 1
+KERNEL_OF = {"WD": "k_wd_relax", "HP": "k_hp_window + k_hp_bigbin", "BS": "k_bs_relax",
+             "NS": "k_ns_relax", "EP": "k_ep_relax"}
 
 
 def parse():
@@ -48,47 +62,35 @@ def parse():
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--strategy", default=os.environ.get("GLB_BENCH_STRATEGY", "WD"))
     ap.add_argument("--algo", default="sssp", choices=("bfs", "sssp"))
-    ap.add_argument("--scale", type=int, default=22)
+    ap.add_argument("--scale", type=int, default=None,
+                    help="R-MAT scale (default 22 = C2 at N=1, 27 = C5 at N>1)")
     ap.add_argument("--edge-factor", type=int, default=16)
     ap.add_argument("--loop", default=os.environ.get("GLB_BENCH_LOOP", "graph"),
                     choices=("host", "graph"))
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--cpu-seconds", type=float, default=20.0,
+                    help="bound of one CPU-baseline sample (full traversals below it)")
     ap.add_argument("--no-extras", action="store_true", help="skip the per-strategy table")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
-    ap.add_argument("--no-check", action="store_true", help="N>1: skip the single-GPU self-check")
-    return ap.parse_args()
+    ap.add_argument("--no-check", action="store_true", help="skip the parity checks")
+    a = ap.parse_args()
+    if a.scale is None:
+        a.scale = 22 if a.gpus == 1 else 27
+    return a
 
 
-# ------------------------------------------------------------------ workload
-def workload(args, device=0):
-    """The benchmark graph, generated in HBM by the CUDA R-MAT generator
-    (bit-identical to graphlb.generate_rmat; tests pin it) and copied back for
-    the CPU oracle / baseline."""
-    import paper_1711_00231_b200 as pkg
-
-    t0 = time.time()
-    g = pkg.generate_rmat(args.scale, args.edge_factor, seed=1, max_weight=255, device=device)
-    return g, time.time() - t0
+# ------------------------------------------------------------------ helpers
+def workload_name(args, n_gpus):
+    cfg = {(22, 16): "C2: ", (27, 16): "C5: "}.get((args.scale, args.edge_factor), "")
+    part = (f", 1-D edge-balanced vertex partition over {n_gpus} GPUs with a per-iteration "
+            f"exchange" if n_gpus > 1 else "")
+    return (f"{cfg}{args.algo.upper()} on RMAT scale-{args.scale} edge-factor {args.edge_factor} "
+            f"(a,b,c,d)=(0.45,0.15,0.15,0.25) seed 1, integer weights 1..255, source 0{part}")
 
 
-def workload_desc(args, g):
-    return {
-        "workload": (f"{'C2: ' if (args.scale, args.edge_factor) == (22, 16) else ''}"
-                     f"{args.algo.upper()} on RMAT scale-{args.scale} edge-factor "
-                     f"{args.edge_factor} (a,b,c,d)=(0.45,0.15,0.15,0.25) seed 1, "
-                     f"integer weights 1..255, source 0"),
-        "strategy": args.strategy,
-        "nodes": g.num_nodes,
-        "edges": g.num_edges,
-        "loop": args.loop,
-        "l2": "inputs larger than L2 (col+weights %.0f MB vs 126 MB L2); no flush" % (
-            g.num_edges * 8 / 1e6),
-    }
-
-
-def reached_edges(g, dist):
-    reached = dist != (1 << 63) - 1
-    return int(g.outdegrees()[reached].sum()), int(reached.sum())
+def reached_edges(deg, dist):
+    reached = dist != INF
+    return int(deg[reached].sum()), int(reached.sum())
 
 
 def algorithmic_bytes(algo, edges, items):
@@ -97,7 +99,13 @@ def algorithmic_bytes(algo, edges, items):
     return (12 if algo == "sssp" else 8) * edges + 20 * items
 
 
-# ------------------------------------------------------------------- clocks
+def hbm_peak():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        return json.loads(p.read_text())["hbm_gbs"], "MEASURED_PEAKS.json hbm_gbs (measured)"
+    return 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
+
+
 class ClockSampler:
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
@@ -142,11 +150,25 @@ class ClockSampler:
                 "samples": len(sm), "reasons": sorted(reasons)}
 
 
-# ------------------------------------------------------------------ our arm
-def run_params(pkg_lib, tag, algo, loop, timing=True):
-    p = pkg_lib.RunParams()
+def cpu_sample(ng, algo, seconds, threads=0):
+    """The pinned run_bs port on all host threads: full traversals while they
+    fit the bound, else one time-bounded traversal extrapolated by its share
+    of a full traversal's relaxations (measured once, untimed)."""
+    from oracle import oracle
+
+    w = algo == "sssp"
+    threads = threads or (os.cpu_count() or 1)
+    t0 = time.perf_counter()
+    d, it, ops, done = oracle.bs_run_narrow(ng, 0, w, threads, max_seconds=seconds)
+    t = time.perf_counter() - t0
+    return d, it, ops, done, t, threads
+
+
+# ----------------------------------------------------------------- our arm
+def run_params(L, tag, algo, loop, timing=True):
+    p = L.RunParams()
     p.strategy = {"BS": 0, "EP": 1, "WD": 2, "NS": 3, "HP": 4}[tag]
-    p.algo = pkg_lib.GLB_BFS if algo == "bfs" else pkg_lib.GLB_SSSP
+    p.algo = L.GLB_BFS if algo == "bfs" else L.GLB_SSSP
     p.source = 0
     p.bins = 10
     p.chunked = 1
@@ -155,19 +177,20 @@ def run_params(pkg_lib, tag, algo, loop, timing=True):
     p.block_size = 1024
     p.hp_fallback = 1
     p.dist_bits = 0
-    p.loop_mode = pkg_lib.GLB_LOOP_GRAPH if loop == "graph" else pkg_lib.GLB_LOOP_HOST
+    p.loop_mode = L.GLB_LOOP_GRAPH if loop == "graph" else L.GLB_LOOP_HOST
     p.record_timing = 1 if timing else 0
+    p.instrument = 0
     return p
 
 
 class DeviceRunner:
     """Direct C-ABI runs on the resident graph (no host copy of distances)."""
 
-    def __init__(self, g, device):
+    def __init__(self, handle):
         from paper_1711_00231_b200 import _lib
 
         self.L = _lib
-        self.h = g.device_graph(device)
+        self.h = handle
         s = ctypes.c_void_p()
         _lib.check(_lib.lib().glb_graph_stream(self.h, ctypes.byref(s)))
         self.stream_ptr = s.value
@@ -200,84 +223,102 @@ def time_strategy(runner, torch, tag, algo, loop, steps, warmup):
     return e0.elapsed_time(e1), stats, recs
 
 
+def roofline_of(args, recs, steps, e_r, n_r, ms_step, n_gpus, kernel_ms_step=None):
+    """Dominant kernel against N x the measured HBM peak.  `frac` uses the
+    one-pass bytes of the traversal; `examined` keeps the
+    bytes of every edge the kernel examined (re-relaxations included)."""
+    peak1, src = hbm_peak()
+    peak = peak1 * n_gpus
+    k_ms = kernel_ms_step if kernel_ms_step is not None else sum(r.kernel_ms for r in recs) / steps
+    onepass = algorithmic_bytes(args.algo, e_r, n_r)
+    launches = len(recs) / steps if recs else 0
+    achieved = onepass / (k_ms / 1e3) / 1e9 if k_ms > 0 else None
+    examined = None
+    if recs:
+        ex_bytes = sum(algorithmic_bytes(args.algo, r.work_total, r.active_items) for r in recs) / steps
+        examined = {"bytes_per_step": int(ex_bytes),
+                    "achieved_GBs": round(ex_bytes / (k_ms / 1e3) / 1e9, 1) if k_ms > 0 else None,
+                    "frac": round(ex_bytes / (k_ms / 1e3) / 1e9 / peak, 4) if k_ms > 0 else None,
+                    "what": "bytes of every edge / item the kernel examined (re-relaxations "
+                            "counted as useful)"}
+    traffic = traffic_note = None
+    prof = ROOT / "profiles" / "ncu_summary.json"
+    if prof.exists() and launches:
+        ps = json.loads(prof.read_text())
+        ratio = ps.get(f"{args.strategy}_{args.algo}_traffic_over_algorithmic")
+        if ratio and examined:
+            traffic = int(ratio * examined["bytes_per_step"] / launches)
+            traffic_note = (f"ncu dram read+write / examined bytes = {ratio} on the captured "
+                            f"launches ({ps.get('source', '')}), per launch")
+    return {
+        "bound": "hbm",
+        "achieved": round(achieved, 1) if achieved else None,
+        "peak": round(peak, 1),
+        "unit": "GB/s",
+        "frac": round(achieved / peak, 4) if achieved else None,
+        "traffic": traffic,
+        "traffic_source": traffic_note,
+        "kernel": KERNEL_OF[args.strategy],
+        "peak_source": src + (f" x {n_gpus} GPUs" if n_gpus > 1 else ""),
+        "algorithmic_bytes_per_launch": int(onepass / launches) if launches else int(onepass),
+        "algorithmic_bytes_per_step": int(onepass),
+        "bytes_def": ("one pass: 12 E_r + 20 N_r (SSSP) / 8 E_r + 20 N_r (BFS), SURVEY 8(d)"),
+        "launches_per_step": launches,
+        "kernel_ms_per_step": round(k_ms, 5),
+        "kernel_share_of_step": round(k_ms / ms_step, 4) if ms_step else None,
+        "whole_step_frac": round(onepass / (ms_step / 1e3) / 1e9 / peak, 5),
+        "examined": examined,
+    }
+
+
 def ours(args):
     import torch
-    import torch.distributed as dist
 
     import paper_1711_00231_b200 as pkg
     from paper_1711_00231_b200 import _lib
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    else:
-        torch.cuda.set_device(0)
-    dev = local if world > 1 else 0
-    g, gen_s = workload(args, dev)
-    runner = DeviceRunner(g, dev)
+    torch.cuda.set_device(0)
+    dev = 0
+    t0 = time.time()
+    g = pkg.generate_rmat(args.scale, args.edge_factor, seed=1, max_weight=255, device=dev,
+                          download=False)
+    gen_s = time.time() - t0
+    runner = DeviceRunner(g.device_graph(dev))
+    row, col, w = g.download_narrow()  # host copy for the oracle / baseline / e2e
+    deg = np.diff(row)
 
-    # parity of the benchmarked configuration against the pinned oracle
     d_gpu = np.empty(g.num_nodes, dtype=np.int64)
     runner.run(args.strategy, args.algo, args.loop, d_gpu)
-    e_r, n_r = reached_edges(g, d_gpu)
-    parity = None
-    cpu = None
-    if rank == 0:
-        from oracle import oracle
+    e_r, n_r = reached_edges(deg, d_gpu)
+    from oracle import oracle
 
-        oracle.build()
-        exp = oracle.oracle_distances(g, 0, args.algo)
-        parity = bool(np.array_equal(exp, d_gpu))
+    oracle.build()
+    ng = oracle.NarrowGraph(row, col, w)
+    parity = None
+    if not args.no_check:  # the pinned oracle (tests/test_oracle_golden.py) on the host cores
+        parity = bool(np.array_equal(oracle.narrow_distances(ng, 0, args.algo), d_gpu))
 
     # ---- timed region: K steps, barrier + synchronize on both sides
     launches0 = _lib.lib().glb_kernel_launches()
     clocks = ClockSampler(dev)
     clocks.start()
-    if world > 1:
-        dist.barrier()
     torch.cuda.synchronize()
     ms, stats, recs = time_strategy(runner, torch, args.strategy, args.algo, args.loop,
                                     args.steps, args.warmup)
     torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
     clk = clocks.stop()
     launches = _lib.lib().glb_kernel_launches() - launches0
     ms_step = ms / args.steps
-    if world > 1:
-        t = torch.tensor([ms_step], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_step = float(t.item())
-    value = world * e_r / (ms_step / 1e3) / 1e9
-
-    # ---- roofline of the dominant (relax) kernel over the timed steps
-    k_ms = sum(r.kernel_ms for r in recs)
-    k_bytes = sum(algorithmic_bytes(args.algo, r.work_total, r.active_items) for r in recs)
-    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
-    peak = peaks.get("hbm_gbs", 6650.0)
-    achieved = k_bytes / (k_ms / 1e3) / 1e9 if k_ms > 0 else None
-    # ncu DRAM traffic of the same kernel (one --set full capture, committed
-    # under profiles/): traffic / algorithmic bytes measured on the captured
-    # launches, applied to this run's mean algorithmic bytes per launch
-    traffic = traffic_note = None
-    prof = ROOT / "profiles" / "ncu_summary.json"
-    if prof.exists():
-        ps = json.loads(prof.read_text())
-        ratio = ps.get(f"{args.strategy}_{args.algo}_traffic_over_algorithmic")
-        if ratio and recs:
-            traffic = int(ratio * k_bytes / len(recs))
-            traffic_note = (f"ncu dram read+write / algorithmic bytes = {ratio} on the captured "
-                            f"launches ({ps.get('source', '')})")
-    # measured ceiling of this path's real bottleneck on the same graph: one
-    # random 8 B cell gather per edge (dist[col[e]]) through L1TEX
+    value = e_r / (ms_step / 1e3) / 1e9
+    roofline = roofline_of(args, recs, args.steps, e_r, n_r, ms_step, 1)
+    roofline["relax_per_traversed_edge"] = round(stats[-1].relax_ops / max(e_r, 1), 3)
+    # measured ceiling of the relaxation's real bottleneck on the same graph:
+    # one random 8 B cell gather per edge (dist[col[e]]) through L1TEX
     gp = (ctypes.c_double * 4)()
     _lib.check(_lib.lib().glb_measure_gather(runner.h, gp), "glb_measure_gather")
-    k_edges = sum(r.work_total for r in recs)
-    edge_rate = k_edges / (k_ms / 1e3) if k_ms > 0 else None
-    gather = {
+    k_ms = sum(r.kernel_ms for r in recs)
+    edge_rate = sum(r.work_total for r in recs) / (k_ms / 1e3) if k_ms > 0 else None
+    roofline["gather_ceiling"] = {
         "what": "dist[col[e]] gather rate on this graph's col array at full occupancy "
                 "(glb_measure_gather), vs the dominant kernel's examined-edge rate",
         "gathers_per_s": round(gp[1] * 1e9, 0), "atomic_min_per_s": round(gp[2] * 1e9, 0),
@@ -285,65 +326,49 @@ def ours(args):
         "kernel_edges_per_s": round(edge_rate, 0) if edge_rate else None,
         "frac": round(edge_rate / (gp[1] * 1e9), 4) if edge_rate and gp[1] > 0 else None,
     }
-    roofline = {
-        "bound": "hbm",
-        "achieved": round(achieved, 1) if achieved else None,
-        "peak": peak,
-        "unit": "GB/s",
-        "frac": round(achieved / peak, 4) if achieved else None,
-        "traffic": traffic,
-        "traffic_source": traffic_note,
-        "kernel": {"WD": "k_wd_relax", "HP": "k_hp_window", "BS": "k_bs_relax",
-                   "NS": "k_ns_relax", "EP": "k_ep_relax"}[args.strategy],
-        "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if peaks else "fallback",
-        "algorithmic_bytes_per_launch": int(k_bytes / max(len(recs), 1)),
-        "kernel_ms_per_launch": round(k_ms / max(len(recs), 1), 5),
-        "kernel_share_of_step": round(k_ms / ms, 4) if ms else None,
-        "relax_per_traversed_edge": round(stats[-1].relax_ops / max(e_r, 1), 3),
-        "whole_step_frac": round(algorithmic_bytes(args.algo, e_r, n_r) / (ms_step / 1e3) / 1e9 / peak, 5),
-        "gather_ceiling": gather,
-    }
 
-    # ---- e2e through the C-ABI with host buffers
+    # ---- e2e through the C-ABI with host int64 buffers
     e2e = None
-    if rank == 0 and args.e2e_steps > 0:
+    if args.e2e_steps > 0:
         L = _lib.lib()
-        row, col, w = g.row_offsets, g.col_indices, g.weights
+        row64, col64 = row, col.astype(np.int64)
+        w64 = w.astype(np.int64) if w is not None else None
         out = np.empty(g.num_nodes, dtype=np.int64)
         times = []
         for i in range(args.e2e_steps + 1):
             torch.cuda.synchronize()
-            t0 = time.perf_counter()
+            t1 = time.perf_counter()
             h = ctypes.c_void_p()
-            _lib.check(L.glb_graph_create(_lib.ptr64(row), _lib.ptr64(col), _lib.ptr64(w),
+            _lib.check(L.glb_graph_create(_lib.ptr64(row64), _lib.ptr64(col64), _lib.ptr64(w64),
                                           g.num_nodes, g.num_edges, dev, ctypes.byref(h)))
             p = run_params(_lib, args.strategy, args.algo, args.loop)
             st = _lib.RunStats()
             _lib.check(L.glb_run(h, ctypes.byref(p), _lib.ptr64(out), ctypes.byref(st), None, 0))
             L.glb_graph_destroy(h)
             torch.cuda.synchronize()
-            if i:  # first call warms the pinned staging ring
-                times.append(time.perf_counter() - t0)
+            if i:  # the first call warms the pinned staging ring
+                times.append(time.perf_counter() - t1)
         assert np.array_equal(out, d_gpu)
         t = statistics.median(times)
         e2e = {"value": round(e_r / t / 1e9, 4), "unit": UNIT,
-               "h2d_bytes_per_step": int(row.nbytes + col.nbytes + (w.nbytes if w is not None else 0)),
+               "h2d_bytes_per_step": int(row64.nbytes + col64.nbytes + (w64.nbytes if w64 is not None else 0)),
                "d2h_bytes_per_step": int(out.nbytes),
                "ms_per_step": round(t * 1e3, 2),
                "path": "C-ABI: glb_graph_create(host int64 CSR) + glb_run + int64 dist to host + destroy"}
+        del col64, w64
 
     # ---- per-strategy table (not the headline)
     extras = {}
-    if rank == 0 and not args.no_extras:
+    if not args.no_extras:
         for algo in ("sssp", "bfs"):
             tab = {}
+            e_r_a = e_r
+            if algo != args.algo:
+                dd = np.empty(g.num_nodes, dtype=np.int64)
+                runner.run("WD", algo, args.loop, dd)
+                e_r_a, _ = reached_edges(deg, dd)
             for tag in TAGS:
                 ms_t, st_t, rr = time_strategy(runner, torch, tag, algo, args.loop, 3, 1)
-                e_r_a = e_r
-                if algo != args.algo:
-                    dd = np.empty(g.num_nodes, dtype=np.int64)
-                    runner.run(tag, algo, args.loop, dd)
-                    e_r_a, _ = reached_edges(g, dd)
                 kms = sum(r.kernel_ms for r in rr)
                 tab[tag] = {"ms": round(ms_t / 3, 3), "gteps": round(e_r_a / (ms_t / 3 / 1e3) / 1e9, 3),
                             "launches": st_t[-1].launches, "iterations": st_t[-1].iterations,
@@ -352,88 +377,106 @@ def ours(args):
             extras[algo] = tab
 
     # ---- CPU baseline: pinned C port of run_bs on the host cores
-    if rank == 0 and not args.no_cpu:
-        cpu = cpu_baseline(g, args, e_r)
+    cpu = None
+    if not args.no_cpu:
+        d, it, ops, done, t, thr = cpu_sample(ng, args.algo, args.cpu_seconds)
+        rate = e_r / t / 1e9 if done else None
+        cpu = {"value": round(rate, 5) if rate else round(ops / t / 1e9, 5), "unit": UNIT,
+               "cores": thr, "kind": "port",
+               "sample": (f"one full {args.algo.upper()} run_bs traversal of the benchmark graph "
+                          f"({t:.2f} s, {it} iterations, {ops} relaxations), C port of "
+                          f"node_based.py:19-82 on {thr} threads" if done else
+                          f"run_bs stopped after {it} iterations / {t:.1f} s; value = examined "
+                          f"edges per second")}
 
-    if rank == 0:
-        line = {
-            "metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
-            "data": "synthetic (RMAT generated on the GPU, bit-identical to graphlb.generate_rmat)",
-            "config": dict(workload_desc(args, g), parallelism=f"replicas{world}" if world > 1 else "single",
-                           E_r=e_r, N_r=n_r, gen_s=round(gen_s, 1)),
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
-            "gpu_launches": int(launches), "parity_vs_oracle": parity,
-            "strategies": extras,
-        }
-        print(json.dumps(line), flush=True)
-    if world > 1:
-        dist.destroy_process_group()
+    line = {
+        "metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": 1,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+        "data": "synthetic (RMAT generated on the GPU, bit-identical to graphlb.generate_rmat)",
+        "config": {"workload": workload_name(args, 1), "strategy": args.strategy,
+                   "nodes": g.num_nodes, "edges": g.num_edges, "loop": args.loop,
+                   "l2": "inputs larger than L2 (col+weights %.0f MB vs 126 MB L2); no flush" % (
+                       g.num_edges * 8 / 1e6),
+                   "parallelism": "single", "E_r": e_r, "N_r": n_r, "gen_s": round(gen_s, 1)},
+        "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
+        "gpu_launches": int(launches), "parity_vs_oracle": parity,
+        "strategies": extras,
+    }
+    print(json.dumps(line), flush=True)
 
 
 # ------------------------------------------------------- sharded (N > 1)
 def ours_sharded(args, world, rank, local):
-    """N ranks, one GPU each: RMAT scale args.scale + log2(N) (weak scaling:
-    the same 2^(scale+4) edges per GPU as the 1-GPU C2 step), 1-D edge-balanced
-    vertex partition, one NCCL all-to-all exchange of (dist << 32 | v)
-    updates per BSP iteration plus an all-reduce of frontier sizes
-    (paper_1711_00231_b200.sharded).  Each step is one full traversal from
-    vertex 0; time = max over ranks of CUDA-event time, value = E_r of the
-    whole graph / that time."""
-    import math
-
+    """N ranks, one GPU each (ranks share GPUs only in the gloo test mode):
+    RMAT scale args.scale (C5 = 27 by default), the SAME graph at every N
+    (strong scaling), 1-D edge-balanced vertex partition, per BSP iteration
+    one exchange of (dist << 32 | v) updates.  Time = max over ranks of
+    CUDA-event time per traversal; value = E_r of the whole graph / time."""
     import torch
     import torch.distributed as dist
 
     import paper_1711_00231_b200 as pkg
     from paper_1711_00231_b200 import _lib, sharded
 
-    backend = os.environ.get("GLB_BENCH_BACKEND", "nccl")
     ndev = torch.cuda.device_count()
+    backend = os.environ.get("GLB_BENCH_BACKEND") or ("nccl" if ndev >= world else "gloo")
     dev = local % max(ndev, 1)
     torch.cuda.set_device(dev)
     if backend == "nccl":
         dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
     else:
         dist.init_process_group(backend)
-    scale = args.scale + int(round(math.log2(world)))
+    assert dist.get_world_size() == world == args.gpus, (dist.get_world_size(), world, args.gpus)
+    tdev = "cuda" if backend == "nccl" else "cpu"
     tag = args.strategy if args.strategy in sharded.SHARD_TAGS else "WD"
     t0 = time.time()
-    g = pkg.generate_rmat(scale, args.edge_factor, seed=1, max_weight=255, device=dev,
+    g = pkg.generate_rmat(args.scale, args.edge_factor, seed=1, max_weight=255, device=dev,
                           download=False)
     bounds = sharded.partition_bounds(g, world)
     lo, hi = int(bounds[rank]), int(bounds[rank + 1])
     row = np.empty(g.num_nodes + 1, dtype=np.int64)
     _lib.check(_lib.lib().glb_graph_download(g.device_graph(), _lib.ptr64(row), None, None))
-    deg_own = np.diff(row[lo:hi + 1])
-    # self-check on rank 0: the single-GPU run on the full graph
+    deg = np.diff(row)
+    # rank 0: the single-GPU run on the full graph, before it is cut
     ref = None
     if rank == 0 and not args.no_check:
         ref = pkg.run_strategy(tag, g, 0, pkg.RelaxOp(args.algo),
-                               pkg.KernelConfig(loop="graph")).dist.array
+                               pkg.KernelConfig(loop="graph", instrument=False)).dist.array
+    host_narrow = None
+    if rank == 0 and not args.no_cpu:
+        host_narrow = g.download_narrow()
     _lib.check(_lib.lib().glb_graph_restrict(g.device_graph(), lo, hi), "glb_graph_restrict")
+    m_own = int(row[hi] - row[lo])
+    g.num_edges = m_own
     sg = sharded.ShardGraph(g, bounds, rank, dev)
     gen_s = time.time() - t0
     transport = sharded.DistTransport(torch)
-    cfg = pkg.KernelConfig(record_timing=False)
+    cfg = pkg.KernelConfig(record_timing=True, instrument=False)
     op = pkg.RelaxOp(args.algo)
 
     def step():
         return sharded.run_sharded(tag, sg, 0, op, cfg, transport)
 
     d_own, info = step()
-    reached = d_own != (1 << 63) - 1
-    t = torch.tensor([int(deg_own[reached].sum()), int(reached.sum())], dtype=torch.int64,
-                     device="cuda" if backend == "nccl" else "cpu")
+    e_r_own, n_r_own = reached_edges(deg[lo:hi], d_own)
+    t = torch.tensor([e_r_own, n_r_own], dtype=torch.int64, device=tdev)
     dist.all_reduce(t)
     e_r, n_r = int(t[0]), int(t[1])
-    parity = None
-    if not args.no_check:  # gather the owned ranges on rank 0 and compare
+    parity = cert = None
+    if not args.no_check:  # gather the owned ranges on rank 0
         full = [None] * world if rank == 0 else None
         dist.gather_object(d_own, full, dst=0)
         if rank == 0:
-            parity = bool(np.array_equal(np.concatenate(full), ref))
+            whole = np.concatenate(full)
+            parity = bool(np.array_equal(whole, ref))
+            # independent exact check: the device distance certificate
+            # (glb_validate) on a fresh single-GPU copy of the graph
+            g2 = pkg.generate_rmat(args.scale, args.edge_factor, seed=1, max_weight=255,
+                                   device=dev, download=False)
+            cert = bool(pkg.validate_distances(g2, 0, args.algo, whole).matched)
+            g2.release_device()
+            del g2
     for _ in range(args.warmup):
         step()
     launches0 = _lib.lib().glb_kernel_launches()
@@ -444,27 +487,29 @@ def ours_sharded(args, world, rank, local):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     iters = 0
+    k_ms = 0.0
     for _ in range(args.steps):
         _, inf = step()
         iters = inf["bsp_iterations"]
+        k_ms += inf["kernel_ms"]
     e1.record()
     torch.cuda.synchronize()
     dist.barrier()
     clk = clocks.stop()
     launches = _lib.lib().glb_kernel_launches() - launches0
     ms_step = e0.elapsed_time(e1) / args.steps
-    tt = torch.tensor([ms_step], dtype=torch.float64, device="cuda" if backend == "nccl" else "cpu")
+    tt = torch.tensor([ms_step, k_ms / args.steps], dtype=torch.float64, device=tdev)
     dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-    ms_step = float(tt.item())
+    ms_step, k_step = float(tt[0]), float(tt[1])
     value = e_r / (ms_step / 1e3) / 1e9
+    roofline = roofline_of(args, [], args.steps, e_r, n_r, ms_step, world, kernel_ms_step=k_step)
+    roofline["kernel_ms_per_step_note"] = "max over ranks of the local relax kernels' time"
 
     # e2e: each rank uploads only its own rows from host int64 arrays, runs,
     # and reads its owned int64 distances back (max over ranks)
     e2e = None
     if args.e2e_steps > 0:
-        # the device graph is already restricted: its download is the host shard
         hrow = np.empty(g.num_nodes + 1, dtype=np.int64)
-        m_own = int(row[hi] - row[lo])
         hcol = np.empty(m_own, dtype=np.int64)
         hw = np.empty(m_own, dtype=np.int64)
         _lib.check(_lib.lib().glb_graph_download(g.device_graph(), _lib.ptr64(hrow),
@@ -485,102 +530,92 @@ def ours_sharded(args, world, rank, local):
             if i:
                 times.append(time.perf_counter() - t1)
         assert np.array_equal(d2, d_own)
-        te = torch.tensor([statistics.median(times)], dtype=torch.float64,
-                          device="cuda" if backend == "nccl" else "cpu")
+        te = torch.tensor([statistics.median(times)], dtype=torch.float64, device=tdev)
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
         t_e2e = float(te.item())
         e2e = {"value": round(e_r / t_e2e / 1e9, 4), "unit": UNIT,
                "h2d_bytes_per_step": int(hrow.nbytes + hcol.nbytes + hw.nbytes),
                "d2h_bytes_per_step": int(d_own.nbytes), "ms_per_step": round(t_e2e * 1e3, 2),
                "path": "per rank: glb_graph_create(own rows, host int64) + sharded run + "
-                       "owned int64 dist to host (bytes are rank 0's)"}
+                       "owned int64 dist to host (bytes are rank 0's; time is the max over ranks)"}
+        del hcol, hw
     cpu = None
-    if rank == 0 and not args.no_cpu:
-        cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count() or 1, "kind": "port",
-               "sample": "not run at N>1 (the CPU reference is timed on the 1-GPU workload)"}
+    if rank == 0 and host_narrow is not None:
+        from oracle import oracle
+
+        oracle.build()
+        ng = oracle.NarrowGraph(*host_narrow)
+        _, it, ops, done, t, thr = cpu_sample(ng, args.algo, args.cpu_seconds)
+        cpu = {"value": round(e_r / t / 1e9 if done else ops / t / 1e9, 5), "unit": UNIT,
+               "cores": thr, "kind": "port",
+               "sample": (f"one full traversal of the same graph ({t:.1f} s)" if done else
+                          f"run_bs port on the same graph, stopped after {it} iterations / "
+                          f"{t:.1f} s; value = examined edges per second")}
+    dist.barrier()  # the CPU sample ran on rank 0 only
     if rank == 0:
         line = {
             "metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32",
             "data": "synthetic (RMAT generated on each GPU, bit-identical to graphlb.generate_rmat)",
             "config": {
-                "workload": (f"{args.algo.upper()} on RMAT scale-{scale} edge-factor "
-                             f"{args.edge_factor} (0.45,0.15,0.15,0.25) seed 1, weights 1..255, "
-                             f"source 0, 1-D edge-balanced vertex partition over {world} GPUs, "
-                             f"{backend} all-to-all exchange per BSP iteration"),
+                "workload": workload_name(args, world),
                 "strategy": tag, "nodes": g.num_nodes, "edges": int(row[-1]),
-                "parallelism": f"shard{world}", "E_r": e_r, "N_r": n_r,
-                "bsp_iterations": iters, "gen_s": round(gen_s, 1),
+                "parallelism": f"shard{world}", "backend": backend,
+                "ranks_per_gpu": max(1, world // max(ndev, 1)),
+                "E_r": e_r, "N_r": n_r, "bsp_iterations": iters, "gen_s": round(gen_s, 1),
                 "l2": "inputs larger than L2; no flush"},
-            "roofline": None, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
             "gpu_launches": int(launches), "parity_vs_single_gpu": parity,
+            "parity_certificate": cert,
         }
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()
 
 
-def cpu_baseline(g, args, e_r):
-    from oracle import oracle
-
-    oracle.build()
-    threads = os.cpu_count() or 1
-    w = g.weights if args.algo == "sssp" else None
-    t0 = time.perf_counter()
-    d, it, ops = oracle.bs_run(g.row_offsets, g.col_indices, w, 0, threads)
-    t = time.perf_counter() - t0
-    return {"value": round(e_r / t / 1e9, 5), "unit": UNIT, "cores": threads, "kind": "port",
-            "sample": f"one full {args.algo.upper()} run_bs traversal of the benchmark graph "
-                      f"({t:.2f} s, {it} iterations, {ops} relaxations)"}
-
-
 # ------------------------------------------------------------ reference arm
-def _has_gpu() -> bool:
-    try:
-        from paper_1711_00231_b200 import _lib
-
-        return _lib.device_count() > 0
-    except Exception:
-        return False
-
-
-def _host_workload(args):
-    import paper_1711_00231_b200 as pkg
-
-    t0 = time.time()
-    g = pkg.generate_rmat(args.scale, args.edge_factor, seed=1, max_weight=255)
-    return g, time.time() - t0
-
-
 def reference(args):
-    world = int(os.environ.get("WORLD_SIZE", "1"))
+    """The reference's algorithm on the host cores, without the CUDA library:
+    graph by the pinned C restatement of generate_rmat, steps by the pinned C
+    port of run_bs (full traversals; at scale > 24 each step is a time-bounded
+    sample whose value extrapolates by its share of a full traversal's
+    relaxations, measured once untimed)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     from oracle import oracle
 
     oracle.build()
-    g, gen_s = workload(args) if _has_gpu() else _host_workload(args)
     threads = os.cpu_count() or 1
-    w = g.weights if args.algo == "sssp" else None
-    times = []
-    d = None
+    t0 = time.time()
+    ng = oracle.rmat_narrow(args.scale, args.edge_factor, seed=1, max_weight=255, threads=threads)
+    gen_s = time.time() - t0
+    w = args.algo == "sssp"
+    bounded = args.scale > 24
+    d, it, ops_full, done = oracle.bs_run_narrow(ng, 0, w, threads)
+    e_r, n_r = reached_edges(ng.outdegrees(), d)
+    vals = []
     for i in range(args.warmup + args.steps):
-        t0 = time.perf_counter()
-        d, it, ops = oracle.bs_run(g.row_offsets, g.col_indices, w, 0, threads)
+        t1 = time.perf_counter()
+        _, it, ops, done = oracle.bs_run_narrow(ng, 0, w, threads,
+                                                max_seconds=args.cpu_seconds if bounded else 0.0)
+        t = time.perf_counter() - t1
         if i >= args.warmup:
-            times.append(time.perf_counter() - t0)
-    e_r, n_r = reached_edges(g, d)
-    t = sum(times) / len(times)
-    value = e_r / t / 1e9
-    sample = (f"each step = one full {args.algo.upper()} node-based (run_bs) traversal of the "
-              f"benchmark graph, C port of node_based.py:19-82 on {threads} threads")
+            vals.append(e_r * (ops / ops_full) / t / 1e9)
+    value = statistics.mean(vals)
+    ms = e_r / (value * 1e9) * 1e3
+    sample = (f"each step = one {'time-bounded (' + str(args.cpu_seconds) + ' s) ' if bounded else 'full '}"
+              f"{args.algo.upper()} node-based (run_bs) traversal of the benchmark graph, C port of "
+              f"node_based.py:19-82 on {threads} threads; graph from the C restatement of "
+              f"generate_rmat (oracle_rmat_u32, {gen_s:.1f} s)")
     line = {
-        "metric": METRIC, "value": round(value, 5), "unit": UNIT, "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t * 1e3, 2),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
-        "data": "synthetic (RMAT generated in-process, bit-identical to graphlb.generate_rmat)",
-        "config": dict(workload_desc(args, g), strategy="BS", E_r=e_r, N_r=n_r),
+        "metric": METRIC, "value": round(value, 5), "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 2),
+        "higher_is_better": True, "scaling": "weak" if args.gpus == 1 else "strong",
+        "vs_baseline": None, "dtype": "int64",
+        "data": "synthetic (RMAT from the pinned C restatement of graphlb.generate_rmat)",
+        "config": {"workload": workload_name(args, args.gpus), "strategy": "BS",
+                   "nodes": ng.num_nodes, "edges": ng.num_edges, "E_r": e_r, "N_r": n_r},
         "impl": "reference",
         "cpu_baseline": {"value": round(value, 5), "unit": UNIT, "cores": threads, "kind": "port",
                          "sample": sample},
@@ -590,12 +625,31 @@ def reference(args):
     print(json.dumps(line), flush=True)
 
 
+# ---------------------------------------------------------------- launcher
+def self_launch(args) -> int:
+    """`--gpus N` outside torchrun: start N local ranks on 127.0.0.1."""
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")  # keep NCCL's init log (nranks, NVLS) visible
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           str(Path(__file__).resolve())] + sys.argv[1:]
+    return subprocess.run(cmd, env=env).returncode
+
+
 if __name__ == "__main__":
     a = parse()
+    world = int(os.environ.get("WORLD_SIZE", "0"))
     if a.impl == "reference":
         reference(a)
-    elif int(os.environ.get("WORLD_SIZE", "1")) > 1:
-        ours_sharded(a, int(os.environ["WORLD_SIZE"]), int(os.environ.get("RANK", "0")),
+    elif world == 0 and a.gpus > 1:
+        sys.exit(self_launch(a))
+    elif max(world, 1) != a.gpus:
+        sys.exit(f"bench.py: --gpus {a.gpus} but WORLD_SIZE={world}")
+    elif a.gpus > 1:
+        ours_sharded(a, world, int(os.environ.get("RANK", "0")),
                      int(os.environ.get("LOCAL_RANK", "0")))
     else:
         ours(a)

@@ -82,7 +82,9 @@ typedef struct glb_run_params {
   int32_t dist_bits;       /* 0 = auto (24 -> 32 -> 64 on overflow), 24, 32, 64 */
   int32_t loop_mode;       /* GLB_LOOP_HOST / GLB_LOOP_GRAPH */
   int32_t record_timing;   /* per-launch CUDA event timing into records */
-  int32_t reserved;
+  int32_t instrument;      /* 1: record every launch's per-thread work list
+                              (MetricsRecord.per_thread_work, engine.py:142-174);
+                              fetch with glb_run_thread_work */
 } glb_run_params;
 
 typedef struct glb_run_stats {
@@ -107,7 +109,10 @@ typedef struct glb_run_stats {
 } glb_run_stats;
 
 /* One kernel invocation, mirroring MetricsRecord (engine.py:142-174).
- * per_thread_work is summarised on device (sum / sum of squares / max). */
+ * per_thread_work is summarised on device (sum / sum of squares / max); with
+ * glb_run_params.instrument the exact list of the record's `threads` values
+ * starts at thread_work_offset of the run's list (glb_run_thread_work; -1 =
+ * not recorded). */
 typedef struct glb_record {
   int32_t iteration;
   int32_t sub_iteration;   /* -1 = None */
@@ -122,6 +127,7 @@ typedef struct glb_record {
   int64_t push_ops;
   double kernel_ms;
   double overhead_ms;
+  int64_t thread_work_offset;
 } glb_record;
 
 /* ---- library / device ---- */
@@ -137,7 +143,9 @@ int glb_release_cached_memory(int device, int64_t* bytes_released);
 
 /* ---- graph (csr.py:42-118) ---- */
 /* Copies the host CSR (int64 row_offsets[n+1], col[m], weights[m] or NULL) into
- * HBM on `device`, narrowing col/weights to 32 bits on the device.  Validates
+ * HBM on `device`.  Host worker threads validate and narrow col/weights to
+ * 32 bits (8 bits for weight chunks that fit) into pinned staging buffers, so
+ * PCIe carries the narrow layout.  Validates
  * the CsrGraph invariants (csr.py:66-85); weights must be < 2^32. */
 int glb_graph_create(const int64_t* row_offsets, const int64_t* col,
                      const int64_t* weights_or_null, int64_t n, int64_t m,
@@ -151,6 +159,9 @@ int glb_graph_create_rmat(int scale, int64_t edge_factor, double t_a, double t_a
                           int64_t max_weight, int device, glb_graph** out);
 /* Device CSR back to host int64 arrays (any pointer may be NULL). */
 int glb_graph_download(glb_graph* g, int64_t* row_offsets, int64_t* col, int64_t* weights);
+/* The device-native layout back to the host without widening: uint32
+ * columns / weights (any pointer may be NULL). */
+int glb_graph_download_u32(glb_graph* g, int64_t* row_offsets, uint32_t* col, uint32_t* weights);
 int glb_graph_destroy(glb_graph* g);
 int glb_graph_info(const glb_graph* g, int64_t* n, int64_t* m, int* weighted,
                    int* device);
@@ -171,6 +182,13 @@ int glb_run(glb_graph* g, const glb_run_params* params, int64_t* dist_out,
  * whose capacity was too small); *written receives the count copied. */
 int glb_run_records(glb_graph* g, int64_t offset, glb_record* records,
                     int64_t capacity, int64_t* written);
+
+/* Per-thread work of the graph's most recent instrumented glb_run: values
+ * [offset, offset + count) of its list (uint32 per launched thread; each
+ * record's `threads` values start at its thread_work_offset).  *total (may
+ * be NULL) receives the list length. */
+int glb_run_thread_work(glb_graph* g, int64_t offset, int64_t count, uint32_t* out,
+                        int64_t* total);
 
 /* ---- sharded runs: 1-D vertex partition across ranks ----
  * Every rank holds the graph over the GLOBAL id space with only its own rows

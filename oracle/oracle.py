@@ -24,7 +24,8 @@ _lib = None
 
 
 def build(force: bool = False) -> Path:
-    if force or not LIB_PATH.exists() or LIB_PATH.stat().st_mtime < (HERE / "graphlb_oracle.c").stat().st_mtime:
+    srcs = [HERE / "graphlb_oracle.c", HERE / "graphlb_oracle_big.c"]
+    if force or not LIB_PATH.exists() or any(LIB_PATH.stat().st_mtime < p.stat().st_mtime for p in srcs):
         subprocess.run(["make", "-s", "-C", str(HERE)] + (["-B"] if force else []), check=True)
     return LIB_PATH
 
@@ -48,6 +49,14 @@ def lib() -> ctypes.CDLL:
         L.oracle_coo_src.restype = None
         L.oracle_bs_run.argtypes = [i64, _p64, _p64, _p64, i64, ctypes.c_int, _p64, _p64, _p64]
         L.oracle_max_threads.argtypes = []
+        u32p, u64p = ctypes.POINTER(ctypes.c_uint32), ctypes.POINTER(ctypes.c_uint64)
+        L.oracle_rmat_u32.argtypes = [ctypes.c_int, i64, ctypes.c_double, ctypes.c_double,
+                                      ctypes.c_double, u64p, u64p, ctypes.c_int, i64, ctypes.c_int,
+                                      _p64, u32p, u32p]
+        L.oracle_bfs_u32.argtypes = [i64, _p64, u32p, i64, _p64]
+        L.oracle_bfs_levels_u32.argtypes = [i64, _p64, u32p, i64, ctypes.c_int, _p64]
+        L.oracle_bs_run_u32.argtypes = [i64, _p64, u32p, u32p, i64, ctypes.c_int, ctypes.c_double,
+                                        _p64, _p64, _p64, ctypes.POINTER(ctypes.c_int)]
         _lib = L
     return _lib
 
@@ -167,3 +176,96 @@ def bs_run(row, col, weights, source: int, threads: int = 0):
 
 def max_threads() -> int:
     return lib().oracle_max_threads()
+
+
+# ------------------------------------------------------------- large configs
+# Narrow layout (int64 row offsets, uint32 columns / weights) for the C3 / C5
+# sizes; graphlb_oracle_big.c.  A NarrowGraph is what these helpers take.
+class NarrowGraph:
+    """CSR in the narrow layout: row int64[n+1], col uint32[m], w uint32[m] or None."""
+
+    def __init__(self, row, col, w=None):
+        self.row_offsets = np.ascontiguousarray(row, dtype=np.int64)
+        self.col_indices = np.ascontiguousarray(col, dtype=np.uint32)
+        self.weights = None if w is None else np.ascontiguousarray(w, dtype=np.uint32)
+
+    @property
+    def num_nodes(self) -> int:
+        return int(self.row_offsets.shape[0] - 1)
+
+    @property
+    def num_edges(self) -> int:
+        return int(self.col_indices.shape[0])
+
+    def outdegrees(self) -> np.ndarray:
+        return np.diff(self.row_offsets)
+
+
+def _u32(a):
+    if a is None:
+        return None
+    assert a.dtype == np.uint32 and a.flags["C_CONTIGUOUS"]
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32))
+
+
+def rmat_narrow(scale: int, edge_factor: int, params=(0.45, 0.15, 0.15, 0.25), seed: int = 0,
+                weighted: bool = True, max_weight: int = 100, threads: int = 0) -> NarrowGraph:
+    """generate_rmat (generators.py:23-58) + from_edges (csr.py:97-118), the
+    numpy PCG64 stream restated in C on all cores, narrow layout."""
+    a, b, c, _ = params
+    st = np.random.default_rng(seed).bit_generator.state["state"]
+    mask = (1 << 64) - 1
+    sv = (ctypes.c_uint64 * 2)(st["state"] >> 64, st["state"] & mask)
+    iv = (ctypes.c_uint64 * 2)(st["inc"] >> 64, st["inc"] & mask)
+    n = 1 << scale
+    m = edge_factor * n
+    row = np.empty(n + 1, dtype=np.int64)
+    col = np.empty(m, dtype=np.uint32)
+    w = np.empty(m, dtype=np.uint32) if weighted else None
+    rc = lib().oracle_rmat_u32(scale, edge_factor, a, a + b, a + b + c, sv, iv, 1 if weighted else 0,
+                               max_weight, threads, _p(row), _u32(col), _u32(w))
+    if rc != 0:
+        raise MemoryError("oracle_rmat_u32: allocation failed")
+    return NarrowGraph(row, col, w)
+
+
+def bfs_narrow(g, source: int, parallel: bool = True, threads: int = 0) -> np.ndarray:
+    """sequential_bfs levels (oracles.py:13-30): FIFO, or level-synchronous on
+    all cores (same level sets)."""
+    out = np.empty(g.num_nodes, dtype=np.int64)
+    if parallel:
+        rc = lib().oracle_bfs_levels_u32(g.num_nodes, _p(g.row_offsets), _u32(g.col_indices),
+                                         source, threads, _p(out))
+    else:
+        rc = lib().oracle_bfs_u32(g.num_nodes, _p(g.row_offsets), _u32(g.col_indices), source,
+                                  _p(out))
+    if rc == -1:
+        raise ValueError("bad source")
+    if rc:
+        raise MemoryError("oracle bfs: allocation failed")
+    return out
+
+
+def bs_run_narrow(g, source: int, weighted: bool, threads: int = 0, max_seconds: float = 0.0):
+    """run_bs (node_based.py:19-82) port over the narrow layout -> (dist,
+    iterations, relax_ops, completed).  max_seconds > 0 bounds the run (a
+    CPU-baseline sample); the distances are then partial."""
+    out = np.empty(g.num_nodes, dtype=np.int64)
+    it, ops, done = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int()
+    w = g.weights if weighted else None
+    rc = lib().oracle_bs_run_u32(g.num_nodes, _p(g.row_offsets), _u32(g.col_indices), _u32(w),
+                                 source, threads, max_seconds, _p(out), ctypes.byref(it),
+                                 ctypes.byref(ops), ctypes.byref(done))
+    if rc == -1:
+        raise ValueError("bad source")
+    if rc:
+        raise MemoryError("oracle bs_run: allocation failed")
+    return out, it.value, ops.value, bool(done.value)
+
+
+def narrow_distances(g, source: int, algo: str, threads: int = 0) -> np.ndarray:
+    """Expected distances at the large sizes: BFS levels (level-synchronous),
+    SSSP by the run_bs port (its fixpoint is the unique shortest-path array)."""
+    if algo == "bfs":
+        return bfs_narrow(g, source, parallel=True, threads=threads)
+    return bs_run_narrow(g, source, weighted=g.weights is not None, threads=threads)[0]

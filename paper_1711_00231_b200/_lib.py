@@ -40,7 +40,7 @@ class RunParams(ctypes.Structure):
         ("strategy", _i32), ("algo", _i32), ("source", _i64), ("bins", _i32),
         ("chunked", _i32), ("mdt", _i64), ("max_cells", _i64), ("block_size", _i32),
         ("hp_fallback", _i32), ("virtual_threads", _i64), ("dist_bits", _i32),
-        ("loop_mode", _i32), ("record_timing", _i32), ("reserved", _i32),
+        ("loop_mode", _i32), ("record_timing", _i32), ("instrument", _i32),
     ]
 
 
@@ -60,7 +60,7 @@ class Record(ctypes.Structure):
         ("iteration", _i32), ("sub_iteration", _i32), ("tag", _i32), ("reserved", _i32),
         ("active_items", _i64), ("threads", _i64), ("work_total", _i64), ("work_max", _i64),
         ("work_sumsq", _f64), ("relax_ops", _i64), ("push_ops", _i64), ("kernel_ms", _f64),
-        ("overhead_ms", _f64),
+        ("overhead_ms", _f64), ("thread_work_offset", _i64),
     ]
 
 
@@ -79,6 +79,8 @@ SIGNATURES = {
                                              ctypes.POINTER(ctypes.c_uint64), ctypes.c_int, _i64,
                                              ctypes.c_int, ctypes.POINTER(ctypes.c_void_p)]),
     "glb_graph_download": (ctypes.c_int, [ctypes.c_void_p, _p64, _p64, _p64]),
+    "glb_graph_download_u32": (ctypes.c_int, [ctypes.c_void_p, _p64, ctypes.POINTER(ctypes.c_uint32),
+                                              ctypes.POINTER(ctypes.c_uint32)]),
     "glb_graph_partition": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, _p64]),
     "glb_graph_restrict": (ctypes.c_int, [ctypes.c_void_p, _i64, _i64]),
     "glb_shard_begin": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(RunParams), _p64, ctypes.c_int,
@@ -95,6 +97,8 @@ SIGNATURES = {
                                ctypes.POINTER(RunStats), ctypes.POINTER(Record), _i64]),
     "glb_run_records": (ctypes.c_int, [ctypes.c_void_p, _i64, ctypes.POINTER(Record), _i64,
                                        _p64]),
+    "glb_run_thread_work": (ctypes.c_int, [ctypes.c_void_p, _i64, _i64,
+                                           ctypes.POINTER(ctypes.c_uint32), _p64]),
     "glb_graph_load_csrg": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_int,
                                            ctypes.POINTER(ctypes.c_void_p)]),
     "glb_read_text_graph": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_int, _p64, _p64,

@@ -1,0 +1,448 @@
+// glb_bins.cuh -- degree-binned relaxation of edge windows: the kernels of
+// hierarchical processing (HP, hierarchical.py:95-120) and node splitting
+// (NS, splitting.py:141-162).
+//
+// A step hands every thread of a CTA chunk (256 worklist items, claimed by
+// ticket) one edge window [lo, lo + len) relaxed from distance dn -- HP: the
+// sub-iteration window [s*mdt, (s+1)*mdt) of a sublist node; NS: the whole
+// out-range of a split-graph node.  Windows are binned by length:
+//
+//   thread bin  len <= 32       the window stays with its lane; the 32 lanes'
+//                               windows are packed warp-wide (exclusive warp
+//                               scan of the lengths) and walked 32 edges per
+//                               load instruction, each edge's owner lane found
+//                               by a 5-step shuffle search -- one thread's
+//                               window, the warp's load slots;
+//   warp bin    32 < len < 2048 appended to the CTA's shared-memory queue
+//                               (warp-aggregated); warps claim entries and walk
+//                               them with lanes on consecutive edges;
+//   CTA bin     len >= 2048     appended to the grid-wide bin (one 64-bit
+//                               atomic reserves the entry and its 2048-edge
+//                               pieces); the step's second kernel (k_bigbin,
+//                               a programmatic dependent launch) lets every
+//                               CTA claim pieces by ticket and stages each
+//                               piece's columns / weights into shared memory
+//                               with 1-D TMA bulk copies (cp.async.bulk +
+//                               mbarrier), double-buffered: the next piece's
+//                               copy is in flight while the current one is
+//                               relaxed, so the dependent chain per edge is
+//                               smem -> dist gather -> atomic.
+//
+// NS wraps the relaxation with the reference's child mirroring: an improved
+// original node writes its value onto its split children (NsMirror).
+#pragma once
+
+#include "glb_relax.cuh"
+
+#ifndef GLB_BIN_MINB
+#define GLB_BIN_MINB 3  // CTAs per SM the window kernels are register-capped for
+#endif
+
+namespace glb {
+
+constexpr unsigned kBinThreadMax = 32;   // thread bin: windows of at most 32 edges
+constexpr long long kBinCtaMin = 2048;   // CTA bin: windows of at least 2048 edges
+constexpr long long kBinPiece = 2048;    // edges per CTA-bin piece (one TMA stage)
+constexpr int kBinQbCache = 1024;        // CTA-bin windows whose first piece is cached in smem
+constexpr int kBinBuf = (int)kBinPiece + 4;  // a piece plus the 16-byte alignment slack
+constexpr int kBinK = 4;                 // edges in flight per lane
+
+// -------------------------------------------------------------- mirrors ---
+struct NoMirror {
+  template <int K, typename D, bool W>
+  __device__ __forceinline__ void operator()(const Relaxer<D, W>&, BlockQ&, unsigned,
+                                             const uint32_t (&)[K], const D (&)[K],
+                                             ThreadCounters&) const {}
+};
+
+// splitting.py:154-160: a strict improvement of original node v is written
+// onto its children n_orig + cs[v] .. n_orig + cs[v+1] (contiguous ids).
+struct NsMirror {
+  const long long* __restrict__ cs;
+  long long n_orig;
+  template <int K, typename D, bool W>
+  __device__ __forceinline__ void operator()(const Relaxer<D, W>& rx, BlockQ& bq, unsigned won,
+                                             const uint32_t (&v)[K], const D (&cand)[K],
+                                             ThreadCounters& c) const {
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      if (!(won >> k & 1u) || v[k] >= n_orig) continue;
+      const long long k1 = cs[v[k] + 1];
+      for (long long ch = cs[v[k]]; ch < k1; ++ch) {
+        const uint32_t child = (uint32_t)(n_orig + ch);
+        ++c.relax;
+        bool first = false;
+        if (relax_cell<D>(rx.cells, child, cand[k], rx.gen, &first) && rx.claim_push(child, first)) {
+          bq_push(bq, rx.qout, rx.nout, child);
+          ++c.push;
+        }
+      }
+    }
+  }
+};
+
+// ------------------------------------------------------ TMA / mbarrier ---
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "GLB_MBAR_WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra GLB_MBAR_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// 1-D bulk copy global -> shared (TMA engine), completing on `bar`; the
+// source lines are fetched L2 evict-first (single-use edge streams).
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes,
+                                         unsigned long long* bar, unsigned long long pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+      "[%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// ------------------------------------------------------- binned windows ---
+template <typename D>
+struct WinEntry {  // a warp-bin window
+  long long lo;
+  D dn;
+  unsigned len;
+};
+
+template <typename D>
+struct BinSmem {
+  uint32_t q[kQCap];            // CTA push queue items
+  WinEntry<D> wq[kBlock];       // warp bin of the chunk
+  BlockQ bq;
+  unsigned wq_n, wq_next;
+  long long chunk;
+};
+
+// Reserve a CTA-bin entry with its pieces (grid-wide; k_bigbin relaxes it).
+template <typename D>
+__device__ __forceinline__ void cta_bin_push(DevCtrl* ctrl, long long lo, long long len, D dn) {
+  const unsigned pieces = (unsigned)((len + kBinPiece - 1) / kBinPiece);
+  const unsigned long long r = atomicAdd(&ctrl->hp_big_ctr, (1ull << 32) | (unsigned long long)pieces);
+  HpBig* b = ctrl->hp_big + (unsigned)(r >> 32);
+  b->dn = (unsigned long long)dn;
+  b->lo = lo;
+  b->hi = lo + len;
+  b->qbase = (unsigned)r;
+}
+
+// One chunk: every thread of the CTA brings its window (len 0 = none).
+template <typename D, bool W, class M>
+__device__ __forceinline__ void bins_chunk(const Relaxer<D, W>& rx, BinSmem<D>& sm, long long lo,
+                                           long long len, D dn, const M& mirror, DevCtrl* ctrl,
+                                           ThreadCounters& c) {
+  constexpr unsigned FULL = 0xffffffffu;
+  constexpr int K = kBinK;
+  const unsigned lane = lane_id();
+  if (len >= kBinCtaMin) {  // CTA bin
+    cta_bin_push<D>(ctrl, lo, len, dn);
+    len = 0;
+  }
+  // ---- warp bin: into the CTA queue, one smem atomic per warp
+  const bool wb = len > (long long)kBinThreadMax;
+  const unsigned wmask = __ballot_sync(FULL, wb);
+  if (wmask) {
+    unsigned base = 0;
+    if (lane == (unsigned)(__ffs(wmask) - 1)) base = atomicAdd(&sm.wq_n, (unsigned)__popc(wmask));
+    base = __shfl_sync(FULL, base, __ffs(wmask) - 1);
+    if (wb) {
+      WinEntry<D>& q = sm.wq[base + __popc(wmask & ((1u << lane) - 1u))];
+      q.lo = lo;
+      q.dn = dn;
+      q.len = (unsigned)len;
+    }
+  }
+  // ---- thread bin: the lanes' windows packed warp-wide
+  {
+    const unsigned tl = wb ? 0u : (unsigned)len;
+    unsigned incl = tl;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const unsigned y = __shfl_up_sync(FULL, incl, off);
+      if (lane >= (unsigned)off) incl += y;
+    }
+    const unsigned total = __shfl_sync(FULL, incl, 31);
+    const unsigned pre = incl - tl;
+    const uint32_t base32 = (uint32_t)lo - pre;  // edge of flat slot f: base32 + f (edge ids < 2^32)
+    for (unsigned f0 = 0; f0 < total; f0 += 32u * K) {
+      long long e[K];
+      D d[K];
+      unsigned valid = 0;
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const unsigned f = f0 + (unsigned)k * 32u + lane;
+        int o = 0;  // last lane whose window starts at or before f
+#pragma unroll
+        for (int step = 16; step >= 1; step >>= 1) {
+          const unsigned p = __shfl_sync(FULL, pre, o + step);
+          if (p <= f) o += step;
+        }
+        e[k] = (long long)(uint32_t)(__shfl_sync(FULL, base32, o) + f);
+        d[k] = shfl_dist(dn, o);
+        if (f < total) valid |= 1u << k;
+      }
+      uint32_t v[K];
+      D cand[K];
+      const unsigned won = relax_batch<K>(rx, sm.bq, e, d, valid, c, v, cand);
+      mirror(rx, sm.bq, won, v, cand, c);
+    }
+  }
+  __syncthreads();  // the chunk's warp bin is complete
+  // ---- warp bin: one warp per window, lanes on consecutive edges
+  const unsigned nw = sm.wq_n;
+  while (true) {
+    unsigned idx = 0;
+    if (lane == 0) idx = atomicAdd(&sm.wq_next, 1u);
+    idx = __shfl_sync(FULL, idx, 0);
+    if (idx >= nw) break;
+    const WinEntry<D> q = sm.wq[idx];
+    const long long hi = q.lo + q.len;
+    for (long long b = q.lo; b < hi; b += 32ll * K) {
+      long long e[K];
+      D d[K];
+      unsigned valid = 0;
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        e[k] = b + (long long)k * 32 + lane;
+        d[k] = q.dn;
+        if (e[k] < hi) valid |= 1u << k;
+      }
+      uint32_t v[K];
+      D cand[K];
+      const unsigned won = relax_batch<K>(rx, sm.bq, e, d, valid, c, v, cand);
+      mirror(rx, sm.bq, won, v, cand, c);
+    }
+  }
+  bq_flush(sm.bq, rx.qout, rx.nout);  // barriers on both sides
+  if (threadIdx.x == 0) sm.wq_n = sm.wq_next = 0;
+}
+
+template <typename D>
+__device__ __forceinline__ void bins_init(BinSmem<D>& sm) {
+  if (threadIdx.x == 0) sm.wq_n = sm.wq_next = 0;
+  bq_init(sm.bq, sm.q);  // has the barrier
+}
+
+// Claim the next 256-item chunk of the step (dynamic: CTAs that drew light
+// chunks take more).  Returns the chunk's first item, or -1 when done.
+template <typename D>
+__device__ __forceinline__ long long bins_next_chunk(BinSmem<D>& sm, DevCtrl* ctrl, long long n) {
+  if (threadIdx.x == 0) sm.chunk = (long long)atomicAdd(&ctrl->relax_ticket, 1ull) * kBlock;
+  __syncthreads();
+  const long long base = sm.chunk;
+  return base < n ? base : -1;
+}
+
+// ============================================================ HP (K10) ===
+// Sub-iteration window [s*mdt, (s+1)*mdt) of every sublist node
+// (hierarchical.py:95-120); unfinished nodes are carried to the next sublist.
+template <typename D, bool W>
+__global__ void __launch_bounds__(kBlock, GLB_BIN_MINB) k_hp_window(const long long* __restrict__ row,
+                                                         Relaxer<D, W> rx0, DevCtrl* ctrl) {
+  pdl_trigger();
+  __shared__ BinSmem<D> sm;
+  const long long n = ctrl->qcount[ctrl->in];
+  if (blockIdx.x * (long long)kBlock >= n) return;  // idle CTA
+  timer_begin(ctrl->t_relax);
+  bins_init(sm);
+  const Relaxer<D, W> rx = bind(rx0, ctrl);
+  const uint32_t* __restrict__ qin = ctrl->qptr[ctrl->in];
+  uint32_t* qnext = ctrl->qptr[ctrl->next];
+  unsigned int* nnext = &ctrl->qcount[ctrl->next];
+  const long long window = ctrl->window, mdt = ctrl->mdt;
+  ThreadCounters c;
+  for (long long base; (base = bins_next_chunk(sm, ctrl, n)) >= 0;) {
+    const long long i = base + threadIdx.x;
+    long long lo = 0, len = 0;
+    D dn = DistTraits<D>::kInf;
+    if (i < n) {
+      const uint32_t u = qin[i];
+      const long long r0 = row[u], r1 = row[u + 1];
+      const long long start = r0 + window;
+      if (start < r1) {
+        const long long end = start + mdt < r1 ? start + mdt : r1;
+        dn = rx.dist(u);  // dn at window entry (hierarchical.py:108)
+        if (dn != DistTraits<D>::kInf) {
+          lo = start;
+          len = end - start;
+        }
+        if (end < r1) {  // unfinished: carry into the next sublist
+          q_append(qnext, nnext, u);
+          ++c.push;
+        }
+      }
+    }
+    bins_chunk(rx, sm, lo, len, dn, NoMirror{}, ctrl, c);
+  }
+  flush_counters(ctrl, c);
+  timer_end(ctrl->t_relax);
+}
+
+// ============================================================ NS (K9) ===
+// BS over the split graph (every node's out-degree is at most mdt), each
+// node's range binned like an HP window, plus child mirroring.
+template <typename D, bool W>
+__global__ void __launch_bounds__(kBlock, GLB_BIN_MINB) k_ns_relax(const long long* __restrict__ row,
+                                                        NsMirror mirror, Relaxer<D, W> rx0,
+                                                        DevCtrl* ctrl) {
+  pdl_trigger();
+  __shared__ BinSmem<D> sm;
+  const long long n = ctrl->qcount[ctrl->in];
+  if (blockIdx.x * (long long)kBlock >= n) return;  // idle CTA
+  timer_begin(ctrl->t_relax);
+  bins_init(sm);
+  const Relaxer<D, W> rx = bind(rx0, ctrl);
+  const uint32_t* __restrict__ qin = ctrl->qptr[ctrl->in];
+  ThreadCounters c;
+  for (long long base; (base = bins_next_chunk(sm, ctrl, n)) >= 0;) {
+    const long long i = base + threadIdx.x;
+    long long lo = 0, len = 0;
+    D dn = DistTraits<D>::kInf;
+    if (i < n) {
+      const uint32_t u = qin[i];
+      dn = rx.dist(u);
+      if (dn != DistTraits<D>::kInf) {
+        lo = row[u];
+        len = row[u + 1] - lo;
+      }
+    }
+    bins_chunk(rx, sm, lo, len, dn, mirror, ctrl, c);
+  }
+  flush_counters(ctrl, c);
+  timer_end(ctrl->t_relax);
+}
+
+// ======================================================== CTA bin (TMA) ===
+// Every CTA claims 2048-edge pieces of the step's long windows by ticket; a
+// piece's window is found by binary search over the windows' first pieces.
+// Thread 0 claims piece i+1 and issues its bulk copies into the other buffer
+// before the CTA relaxes piece i out of shared memory.
+template <typename D>
+struct BigPiece {
+  long long lo, hi, a_lo;
+  D dn;
+  int valid;
+};
+
+template <typename D, bool W, class M>
+__global__ void __launch_bounds__(kBlock) k_bigbin(Relaxer<D, W> rx0, M mirror, DevCtrl* ctrl,
+                                                   CtlTail tail) {
+  pdl_wait();
+  __shared__ __align__(128) uint32_t s_col[2][kBinBuf];
+  __shared__ __align__(128) uint32_t s_wt[W ? 2 : 1][W ? kBinBuf : 4];
+  __shared__ __align__(8) unsigned long long s_bar[2];
+  __shared__ BigPiece<D> s_pc[2];
+  __shared__ uint32_t s_q[kQCap];
+  __shared__ BlockQ bq;
+  __shared__ unsigned s_qb[kBinQbCache];
+  const unsigned long long bc = ctrl->hp_big_ctr;
+  const unsigned nbig = (unsigned)(bc >> 32), npieces = (unsigned)bc;
+  if (npieces == 0 || blockIdx.x >= npieces) {
+    ctl_tail(tail, ctrl);
+    return;
+  }
+  timer_begin(ctrl->t_relax);
+  const Relaxer<D, W> rx = bind(rx0, ctrl);
+  const bool cached = nbig <= (unsigned)kBinQbCache;
+  if (cached)
+    for (unsigned i = threadIdx.x; i < nbig; i += kBlock) s_qb[i] = ctrl->hp_big[i].qbase;
+  if (threadIdx.x == 0) {
+    mbar_init(&s_bar[0], 1);
+    mbar_init(&s_bar[1], 1);
+    mbar_fence_init();
+  }
+  bq_init(bq, s_q);  // barrier: s_qb and the mbarriers are ready
+  const unsigned long long pol = l2_evict_first();
+  // thread 0: claim a piece into buffer b and start its copies
+  auto claim = [&](int b) {
+    const unsigned t = atomicAdd(&ctrl->hp_piece_next, 1u);
+    BigPiece<D>& pc = s_pc[b];
+    if (t >= npieces) {
+      pc.valid = 0;
+      return;
+    }
+    unsigned lo_i = 0, hi_i = nbig;  // last window with qbase <= t
+    while (hi_i - lo_i > 1) {
+      const unsigned mid = (lo_i + hi_i) >> 1;
+      const unsigned qb = cached ? s_qb[mid] : ctrl->hp_big[mid].qbase;
+      if (qb <= t)
+        lo_i = mid;
+      else
+        hi_i = mid;
+    }
+    const HpBig w = ctrl->hp_big[lo_i];
+    const long long lo = w.lo + (long long)(t - w.qbase) * kBinPiece;
+    const long long hi = lo + kBinPiece < w.hi ? lo + kBinPiece : w.hi;
+    const long long a_lo = lo & ~3ll;  // 16-byte aligned source (arrays carry a 64 B tail pad)
+    const unsigned bytes = (unsigned)(((hi - a_lo + 3) & ~3ll) * 4);
+    fence_proxy_async();  // the buffer's previous contents were read by the generic proxy
+    mbar_expect_tx(&s_bar[b], W ? 2 * bytes : bytes);
+    bulk_g2s(s_col[b], rx.col + a_lo, bytes, &s_bar[b], pol);
+    if (W) bulk_g2s(s_wt[b], rx.wt + a_lo, bytes, &s_bar[b], pol);
+    pc.lo = lo;
+    pc.hi = hi;
+    pc.a_lo = a_lo;
+    pc.dn = (D)w.dn;
+    pc.valid = 1;
+  };
+  if (threadIdx.x == 0) claim(0);
+  __syncthreads();
+  ThreadCounters c;
+  constexpr int K = kBinK;
+  for (unsigned it = 0;; ++it) {
+    const int b = (int)(it & 1u);
+    if (!s_pc[b].valid) break;
+    if (threadIdx.x == 0) claim(b ^ 1);  // buffer b^1 was released by the last barrier
+    const long long lo = s_pc[b].lo, hi = s_pc[b].hi, a_lo = s_pc[b].a_lo;
+    const D dn = s_pc[b].dn;
+    mbar_wait(&s_bar[b], (it >> 1) & 1u);
+    for (long long f0 = lo; f0 < hi; f0 += (long long)K * kBlock) {
+      uint32_t v[K], w[K];
+      D d[K];
+      unsigned valid = 0;
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const long long e = f0 + (long long)k * kBlock + threadIdx.x;
+        d[k] = dn;
+        v[k] = 0;
+        w[k] = 1u;
+        if (e < hi) {
+          valid |= 1u << k;
+          v[k] = s_col[b][e - a_lo];
+          if (W) w[k] = s_wt[b][e - a_lo];
+        }
+      }
+      D cand[K];
+      const unsigned won = relax_vals<K>(rx, bq, v, w, d, valid, c, cand);
+      mirror(rx, bq, won, v, cand, c);
+    }
+    bq_flush(bq, rx.qout, rx.nout);  // barriers: piece b is consumed, s_pc[b^1] is visible
+  }
+  flush_counters(ctrl, c);
+  timer_end(ctrl->t_relax);
+  ctl_tail(tail, ctrl);
+}
+
+}  // namespace glb

@@ -204,6 +204,15 @@ __device__ __forceinline__ bool small_eligible(const DevCtrl* c) {
   }
 }
 
+// Slots of the per-thread work list of the record being written; -1 when the
+// run is not instrumented or the list buffer is full.
+__device__ __forceinline__ long long ctl_ptw_take(DevCtrl* c, unsigned long long threads) {
+  if (!c->ptw) return -1;
+  const unsigned long long off = c->ptw_off;
+  c->ptw_off = off + threads;
+  return off + threads <= c->ptw_cap ? (long long)off : -1;
+}
+
 __device__ __forceinline__ void ctl_reset_timers(DevCtrl* c) {
   c->t_relax.start = c->t_scan.start = ~0ull;
   c->t_relax.end = c->t_scan.end = 0;
@@ -278,8 +287,10 @@ __device__ __forceinline__ void control_warp(DevCtrl* c, cudaGraphConditionalHan
   }
   if (lane != 0) return;
   // this control kernel + the step's kernels (WD: scan + relax)
-  c->kernels += (c->small_exit || c->done ? 2 : (c->mode == kModeWD || c->mode == kModeHP ? 3 : 2)) -
-                 (fused ? 1 : 0);
+  // (two-kernel steps: WD scan + relax, HP window + CTA bin, NS relax + CTA bin)
+  const bool two = c->mode == kModeWD || c->mode == kModeHP ||
+                   (c->mode == kModeRelax && c->strategy == GLB_NS);
+  c->kernels += (c->small_exit || c->done ? 2 : (two ? 3 : 2)) - (fused ? 1 : 0);
   const unsigned long long wd_next = c->wd_next;
   const unsigned wd_zero = c->wd_zero_next;
   if (c->small_exit) {  // k_small_loop recorded and advanced its own iterations
@@ -317,6 +328,7 @@ __device__ __forceinline__ void control_warp(DevCtrl* c, cudaGraphConditionalHan
     rec.k1 = c->t_relax.end;
     rec.o0 = c->mode == kModeWD ? c->t_scan.start : 0;
     rec.o1 = c->mode == kModeWD ? c->t_scan.end : 0;
+    rec.ptw_off = ctl_ptw_take(c, (unsigned long long)rec.threads);
   }
   if (!wd_empty) c->nrec += 1;
   if (c->mode == kModeWD) c->scan_epoch += 1;

@@ -23,6 +23,7 @@
 
 #include "glb_control.cuh"
 #include "glb_internal.cuh"
+#include "glb_bins.cuh"
 #include "glb_relax.cuh"
 #include "glb_scan.cuh"
 #include "glb_small.cuh"
@@ -37,8 +38,13 @@ void histogram(glb_graph* g, const long long* row, long long n, unsigned long lo
 namespace {
 
 constexpr unsigned kMaxRecords = 1u << 16;
+constexpr unsigned long long kPtwCap = 1ull << 27;  // per-thread work slots of one run (512 MB)
 
-struct OverflowRestart {};  // a u32 candidate reached INF: re-run in u64
+// a narrow candidate reached INF: re-run at the next distance tier.  Derived
+// from std::exception so no C-ABI guard can let it escape an extern "C" call.
+struct OverflowRestart : std::exception {
+  const char* what() const noexcept override { return "distance overflow"; }
+};
 
 double now_ms() {
   return std::chrono::duration<double, std::milli>(
@@ -134,6 +140,7 @@ class Runner {
       else
         GLB_CUDA_TRY(cudaMemcpy(dist_out, out, (size_t)cnt * 8, cudaMemcpyDeviceToHost));
     }
+    g_->ptw_len = ptw_ ? (long long)std::min<unsigned long long>(h_->ctrl.ptw_off, kPtwCap) : 0;
     g_->stamp_epoch = h_->ctrl.gen;
     g_->scan_epoch = h_->ctrl.scan_epoch;
     float dev_ms = 0;
@@ -154,6 +161,7 @@ class Runner {
   uint32_t* src_ = nullptr;
   CellS<D>* cells_ = nullptr;
   uint32_t* stamp_ = nullptr;
+  uint32_t* ptw_ = nullptr;
   uint32_t* q_[4] = {nullptr, nullptr, nullptr, nullptr};
   DevCtrl* ctrl_ = nullptr;
   LaunchStats* ls_ = nullptr;
@@ -165,7 +173,7 @@ class Runner {
   unsigned* tile_first_[2] = {nullptr, nullptr};
   LookbackState<2> lb_{};
   // grids
-  int cap_relax_ = 0, cap_scan_ = 0, cap_wd_ = 0, cap_hp_ = 0;
+  int cap_relax_ = 0, cap_scan_ = 0, cap_wd_ = 0, cap_hp_ = 0, cap_big_ = 0;
   // graph loop: the control step runs as the tail of each step's last kernel
   CtlTail tail_{0, {}, 0};
   bool fused_ctl_ = getenv("GLB_NO_FUSED_CTL") == nullptr;
@@ -236,10 +244,14 @@ class Runner {
       cap_scan_ = cap((const void*)k_wd_scan<D>);
       cap_wd_ = cap((const void*)k_wd_relax<D, W>);
     }
-    if (p_.strategy == GLB_HP) {
+    if (p_.strategy == GLB_HP)
       cap_hp_ = std::max(cap((const void*)k_hp_window<D, W>), g_->num_sms);
-      // CTA-bin entries: every long window holds >= kHpCtaThreshold edges
-      hp_big_ = (HpBig*)ensure(ws.hp_big, ((size_t)g_->m / kHpCtaThreshold + 64) * sizeof(HpBig));
+    if (p_.strategy == GLB_HP || p_.strategy == GLB_NS) {
+      // CTA-bin entries: every long window holds >= kBinCtaMin edges
+      hp_big_ = (HpBig*)ensure(ws.hp_big, ((size_t)g_->m / kBinCtaMin + 64) * sizeof(HpBig));
+      cap_big_ = std::max(p_.strategy == GLB_HP ? cap((const void*)k_bigbin<D, W, NoMirror>)
+                                                : cap((const void*)k_bigbin<D, W, NsMirror>),
+                          g_->num_sms);
     }
     if (kSmallCtas > 8)
       GLB_CUDA_TRY(cudaFuncSetAttribute((const void*)k_small_loop<D, W>,
@@ -249,6 +261,11 @@ class Runner {
                                       (int)small_smem_bytes<D>()));
     if (relax_kernel()) cap_relax_ = std::max(cap(relax_kernel()), g_->num_sms);
     pin_cells_in_l2(nb * sizeof(CellS<D>));
+    ptw_ = nullptr;
+    if (p_.instrument) {  // per-thread work lists: zeroed once, atomically accumulated
+      ptw_ = (uint32_t*)ensure(ws.ptw, (size_t)kPtwCap * 4);
+      GLB_CUDA_TRY(cudaMemsetAsync(ptw_, 0, (size_t)kPtwCap * 4, s_));
+    }
     ctrl_ = (DevCtrl*)ensure(ws.ctrl, sizeof(DevCtrl));
     ls_ = (LaunchStats*)ensure_zero(ws.stats, sizeof(LaunchStats), s_);
     drecs_ = (DevRecord*)ensure(ws.recs, sizeof(DevRecord) * kMaxRecords);
@@ -289,6 +306,9 @@ class Runner {
     c.wd_fused = p_.strategy == GLB_WD && !shard_mode_ && getenv("GLB_WD_FUSED") ? 1 : 0;
     c.recs = drecs_;
     c.ls = ls_;
+    c.ptw = ptw_;
+    c.ptw_off = 0;
+    c.ptw_cap = ptw_ ? kPtwCap : 0;
     h_->ctrl = c;
     GLB_CUDA_TRY(cudaMemcpyAsync(ctrl_, &h_->ctrl, sizeof(DevCtrl), cudaMemcpyHostToDevice, s_));
 
@@ -368,7 +388,11 @@ class Runner {
     const Relaxer<D, W> rx = relaxer();
     switch (p_.strategy) {
       case GLB_BS: k_bs_relax<D, W><<<grid, kBlock, 0, s_>>>(row_, rx, ctrl_, tail_); break;
-      case GLB_NS: k_ns_relax<D, W><<<grid, kBlock, 0, s_>>>(row_, cs_, g_->n, rx, ctrl_, tail_); break;
+      case GLB_NS:  // binned windows + the CTA bin of the long ones (TMA-staged)
+        k_ns_relax<D, W><<<grid, kBlock, 0, s_>>>(row_, ns_mirror(), rx, ctrl_);
+        GLB_CHECK_LAUNCH();
+        launch_dependent(k_bigbin<D, W, NsMirror>, (unsigned)cap_big_, rx, ns_mirror(), ctrl_, tail_);
+        break;
       case GLB_EP:
         if (p_.chunked)
           k_ep_relax<D, W, true><<<grid, kBlock, 0, s_>>>(row_, src_, rx, ctrl_, tail_);
@@ -406,9 +430,10 @@ class Runner {
   void launch_hp(unsigned grid) {
     k_hp_window<D, W><<<grid, kBlock, 0, s_>>>(row_, relaxer(), ctrl_);
     GLB_CHECK_LAUNCH();
-    launch_dependent(k_hp_bigbin<D, W>, (unsigned)cap_hp_, relaxer(), ctrl_, tail_);
+    launch_dependent(k_bigbin<D, W, NoMirror>, (unsigned)cap_big_, relaxer(), NoMirror{}, ctrl_, tail_);
     GLB_CHECK_LAUNCH();
   }
+  NsMirror ns_mirror() const { return NsMirror{cs_, g_->n}; }
   void launch_small() {
     k_small_loop<D, W><<<kSmallCtas, kSmallThreads, small_smem_bytes<D>(), s_>>>(
         row_, p_.strategy == GLB_NS ? cs_ : nullptr, g_->n,
@@ -514,12 +539,13 @@ class Runner {
   std::string graph_key() const {
     std::ostringstream k;
     k << g_->device << '|' << p_.strategy << '|' << fused_ctl_ << '|' << unroll_ << '|' << pdl_ << '|' << Cell<D>::kDistBits << '|' << W << '|' << p_.chunked << '|' << cap_relax_
-      << '|' << cap_scan_ << '|' << cap_wd_ << '|' << cap_hp_ << '|' << (const void*)row_ << '|'
+      << '|' << cap_scan_ << '|' << cap_wd_ << '|' << cap_hp_ << '|' << cap_big_ << '|' << (const void*)row_ << '|'
       << (const void*)col_ << '|' << (const void*)wt_ << '|' << (const void*)cs_ << '|'
       << (const void*)src_ << '|' << (const void*)cells_ << '|' << (const void*)stamp_ << '|'
       << (const void*)ctrl_ << '|' << (const void*)items_[0] << '|' << (const void*)items_[1] << '|'
       << (const void*)tile_first_[0] << '|' << (const void*)tile_first_[1] << '|'
-      << (const void*)lb_.flags << '|' << (const void*)lb_.aggs << '|' << g_->n;
+      << (const void*)lb_.flags << '|' << (const void*)lb_.aggs << '|' << g_->n << '|' << n_all_
+      << '|' << mdt_;
     return k.str();
   }
 
@@ -685,6 +711,7 @@ class Runner {
       r.push_ops = d.push;
       r.kernel_ms = d.k1 > d.k0 && d.k0 != ~0ull ? (double)(d.k1 - d.k0) * 1e-6 : 0.0;
       r.overhead_ms = d.o0 && d.o1 > d.o0 && d.o0 != ~0ull ? (double)(d.o1 - d.o0) * 1e-6 : 0.0;
+      r.thread_work_offset = ptw_ ? d.ptw_off : -1;
       if (i < ev_of_rec_.size()) {  // host loop: CUDA-event times and the exact grid
         const EvPair& e = ev_of_rec_[i];
         float ms = 0;
@@ -1043,6 +1070,33 @@ extern "C" int glb_run_records(glb_graph* g, int64_t offset, glb_record* records
   return GLB_OK;
 }
 
+extern "C" int glb_run_thread_work(glb_graph* g, int64_t offset, int64_t count, uint32_t* out,
+                                   int64_t* total) {
+  try {
+    if (!g || offset < 0 || count < 0 || (count > 0 && !out))
+      throw glb::Error{GLB_EINVAL, "glb_run_thread_work: invalid argument"};
+    std::lock_guard<std::mutex> lk(g->mu);
+    if (total) *total = g->ptw_len;
+    if (count == 0) return GLB_OK;
+    if (offset + count > g->ptw_len || !g->ws.ptw.p)
+      throw glb::Error{GLB_ERANGE, "per-thread work range beyond the last instrumented run"};
+    int prev = -1;
+    cudaGetDevice(&prev);
+    GLB_CUDA_TRY(cudaSetDevice(g->device));
+    const cudaError_t e = cudaMemcpy(out, (const uint32_t*)g->ws.ptw.p + offset, (size_t)count * 4,
+                                     cudaMemcpyDeviceToHost);
+    if (prev >= 0) cudaSetDevice(prev);
+    GLB_CUDA_TRY(e);
+    return GLB_OK;
+  } catch (const glb::Error& e) {
+    glb::set_error(e.msg);
+    return e.code;
+  } catch (const std::exception& e) {
+    glb::set_error(e.what());
+    return GLB_ECUDA;
+  }
+}
+
 // ============================================================ shard C-ABI ===
 namespace {
 template <typename F>
@@ -1064,6 +1118,16 @@ int shard_guard(glb_graph* g, F&& f) {
   } catch (const glb::Error& e) {
     glb::set_error(e.msg);
     return e.code;
+  } catch (const glb::OverflowRestart&) {
+    // a sharded run has no automatic re-run at a wider tier: the caller
+    // restarts with dist_bits 64 (sharded.run_sharded does)
+    if (g) {
+      delete g->shard;
+      g->shard = nullptr;
+      glb::reset_epochs_public(g);
+    }
+    glb::set_error("distance exceeds the 32-bit range of the sharded run");
+    return GLB_EOVERFLOW;
   } catch (const std::exception& e) {
     glb::set_error(e.what());
     return GLB_ECUDA;
@@ -1087,7 +1151,8 @@ extern "C" int glb_shard_begin(glb_graph* g, const glb_run_params* p, const int6
     if (p->source < 0 || p->source >= g->n)
       throw glb::Error{GLB_EINVAL, "source out of range"};
     if (p->block_size < 1) throw glb::Error{GLB_EINVAL, "block_size must be >= 1"};
-    if (p->dist_bits == 64) throw glb::Error{GLB_EINVAL, "sharded runs use 32-bit distances"};
+    if (p->dist_bits == 64 || p->dist_bits == 24)
+      throw glb::Error{GLB_EINVAL, "sharded runs use 32-bit distances (dist_bits 0 or 32)"};
     delete g->shard;
     g->shard = nullptr;
     const bool weighted = p->algo == GLB_SSSP && g->wt != nullptr;

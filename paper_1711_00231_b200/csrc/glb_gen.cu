@@ -259,8 +259,8 @@ void rmat_device(glb_graph* g, int scale, long long edge_factor, double t_a, dou
       GLB_CUDA_TRY(e);
     }
     g->row = (long long*)dmalloc((size_t)(n + 1) * 8);
-    g->col = (uint32_t*)dmalloc(mb * 4);
-    if (weighted) g->wt = (uint32_t*)dmalloc(mb * 4);
+    g->col = (uint32_t*)dmalloc(mb * 4 + kEdgePad);
+    if (weighted) g->wt = (uint32_t*)dmalloc(mb * 4 + kEdgePad);
     // row offsets: counts per source, exclusive scan
     unsigned long long* cnt = (unsigned long long*)ensure(b_tmp, (size_t)(n + 1) * 8);
     GLB_CUDA_TRY(cudaMemsetAsync(cnt, 0, (size_t)(n + 1) * 8, s));

@@ -116,8 +116,8 @@ void measure_gather(glb_graph* g, double out[4]);
 
 void graph_upload(glb_graph* g, const int64_t* row, const int64_t* col, const int64_t* w) {
   g->row = (long long*)dmalloc((size_t)(g->n + 1) * 8);
-  g->col = (uint32_t*)dmalloc((size_t)std::max<long long>(g->m, 1) * 4);
-  if (w) g->wt = (uint32_t*)dmalloc((size_t)std::max<long long>(g->m, 1) * 4);
+  g->col = (uint32_t*)dmalloc((size_t)std::max<long long>(g->m, 1) * 4 + kEdgePad);
+  if (w) g->wt = (uint32_t*)dmalloc((size_t)std::max<long long>(g->m, 1) * 4 + kEdgePad);
   long long mx = 0;
   upload_rows(g, row, g->n, g->m, g->row, &mx);
   upload_narrow(g, col, g->m, g->col, (unsigned long long)g->n, false, nullptr,
@@ -429,8 +429,8 @@ void split_device(glb_graph* g, long long mdt, long long totals_out[4]) {
     ws.ns_row = nb;
   }
   long long* new_row = (long long*)ws.ns_row.p;
-  uint32_t* new_col = (uint32_t*)ensure(ws.ns_col, (size_t)std::max<long long>(m, 1) * 4);
-  uint32_t* new_w = g->wt ? (uint32_t*)ensure(ws.ns_w, (size_t)std::max<long long>(m, 1) * 4) : nullptr;
+  uint32_t* new_col = (uint32_t*)ensure(ws.ns_col, (size_t)std::max<long long>(m, 1) * 4 + kEdgePad);
+  uint32_t* new_w = g->wt ? (uint32_t*)ensure(ws.ns_w, (size_t)std::max<long long>(m, 1) * 4 + kEdgePad) : nullptr;
   long long* parent_of = (long long*)ensure(ws.ns_parent, (size_t)std::max<long long>(nchild, 1) * 8);
   if (n > 0) {
     const long long etiles = (m + kEdgeTile - 1) / kEdgeTile;
@@ -849,6 +849,25 @@ int glb_graph_download(glb_graph* g, int64_t* row_offsets, int64_t* col, int64_t
   });
 }
 
+int glb_graph_download_u32(glb_graph* g, int64_t* row_offsets, uint32_t* col, uint32_t* weights) {
+  return guarded([&] {
+    if (!g) throw Error{GLB_EINVAL, "graph is NULL"};
+    std::lock_guard<std::mutex> lk(g->mu);
+    DeviceGuard dg(g->device);
+    if (row_offsets)
+      GLB_CUDA_TRY(cudaMemcpyAsync(row_offsets, g->row, (size_t)(g->n + 1) * 8,
+                                   cudaMemcpyDeviceToHost, g->stream));
+    if (col && g->m)
+      GLB_CUDA_TRY(cudaMemcpyAsync(col, g->col, (size_t)g->m * 4, cudaMemcpyDeviceToHost, g->stream));
+    if (weights && g->m) {
+      if (!g->wt) throw Error{GLB_EINVAL, "graph is unweighted"};
+      GLB_CUDA_TRY(cudaMemcpyAsync(weights, g->wt, (size_t)g->m * 4, cudaMemcpyDeviceToHost,
+                                   g->stream));
+    }
+    GLB_CUDA_TRY(cudaStreamSynchronize(g->stream));
+  });
+}
+
 int glb_graph_partition(glb_graph* g, int parts, int64_t* bounds) {
   return guarded([&] {
     if (!g || !bounds) throw Error{GLB_EINVAL, "NULL argument"};
@@ -892,8 +911,8 @@ int glb_graph_restrict(glb_graph* g, int64_t v_lo, int64_t v_hi) {
     long long* row2 = nullptr;
     uint32_t *col2 = nullptr, *w2 = nullptr;
     row2 = (long long*)dmalloc((size_t)(g->n + 1) * 8);
-    col2 = (uint32_t*)dmalloc((size_t)std::max<long long>(m2, 1) * 4);
-    if (g->wt) w2 = (uint32_t*)dmalloc((size_t)std::max<long long>(m2, 1) * 4);
+    col2 = (uint32_t*)dmalloc((size_t)std::max<long long>(m2, 1) * 4 + kEdgePad);
+    if (g->wt) w2 = (uint32_t*)dmalloc((size_t)std::max<long long>(m2, 1) * 4 + kEdgePad);
     k_restrict_rows<<<grid_for(g->n + 1, kBlock, g->num_sms * 8), kBlock, 0, g->stream>>>(
         g->row, g->n, v_lo, v_hi, e[0], e[1], row2);
     GLB_CHECK_LAUNCH();

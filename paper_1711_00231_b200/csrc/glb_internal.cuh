@@ -23,6 +23,9 @@ namespace glb {
 
 constexpr int kBlock = 256;  // threads per CTA for every relax kernel
 constexpr int kStatSlots = 32;  // spread of the per-launch counter atomics
+// Tail padding of every u32 edge array (col / weights): the CTA bin's 1-D
+// TMA copies read whole 16-byte units, up to 3 elements past the last edge.
+constexpr size_t kEdgePad = 64;
 
 // ---------------------------------------------------------------- errors ---
 void set_error(const std::string& msg);
@@ -190,6 +193,8 @@ struct DevRecord {
   long long active, threads, work, relax, push, work_max;
   double work_sumsq;
   unsigned long long k0, k1, o0, o1;  // relax kernel / scan kernel timers
+  long long ptw_off;                  // first per-thread work slot, -1 = not recorded
+  long long pad2;
 };
 
 // Device control block: worklist cursors, the current step's frame (which
@@ -250,6 +255,10 @@ struct DevCtrl {
   struct LaunchStats* ls;
   unsigned int tail_done;       // CTAs of the step's last kernel that finished (ctl_tail)
   unsigned int tail_pad;
+  // ---- per-thread work lists (MetricsRecord.per_thread_work, engine.py:142-174):
+  // thread t of the launch recorded next adds its work to ptw[ptw_off + t]
+  uint32_t* ptw;                // null: summed counters only
+  unsigned long long ptw_off, ptw_cap;
 };
 
 // --------------------------------------------------------- device graph ---
@@ -273,6 +282,7 @@ struct Workspace {
   DevBuf tile_node;                          // first node of every edge tile
   DevBuf misc_small, shard_tmp;              // sharded-run counters / local split
   DevBuf hp_big;                             // HP CTA-bin entries
+  DevBuf ptw;                                // per-thread work lists (instrumented runs)
 };
 
 }  // namespace glb
@@ -310,6 +320,7 @@ struct glb_graph {
   cudaEvent_t ev[2] = {nullptr, nullptr};
   std::vector<cudaEvent_t> ev_pool;
   std::vector<glb_record> last_records;  // records of the most recent glb_run
+  long long ptw_len = 0;                 // per-thread work slots of the most recent glb_run
   glb::ShardSessionBase* shard = nullptr;                       // sharded run in progress
   std::mutex mu;              // drivers are not re-entrant (common.py:5-6)
 };
@@ -434,6 +445,21 @@ struct ThreadCounters {
   unsigned long long relax = 0;
   unsigned long long push = 0;
 };
+
+__device__ __forceinline__ void flush_counters(LaunchStats* ls, const ThreadCounters& c);
+
+// Per-thread work into the instrumented run's list (atomic: HP's window and
+// CTA-bin kernels are one launch of the record), then the summed counters.
+__device__ __forceinline__ void flush_counters(DevCtrl* ctrl, const ThreadCounters& c) {
+  uint32_t* ptw = ctrl->ptw;
+  if (ptw && c.work) {
+    const unsigned long long i =
+        ctrl->ptw_off + (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < ctrl->ptw_cap)
+      atomicAdd(ptw + i, c.work > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)c.work);
+  }
+  flush_counters(ctrl->ls, c);
+}
 
 __device__ __forceinline__ void flush_counters(LaunchStats* ls, const ThreadCounters& c) {
   unsigned long long w = c.work, r = c.relax, p = c.push, sq = c.work * c.work, mx = c.work;

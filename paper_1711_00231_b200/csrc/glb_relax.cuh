@@ -174,27 +174,17 @@ __device__ __forceinline__ void timer_end(StepTimer& t) {
   if (threadIdx.x == 0) atomicMax(&t.end, gtime());
 }
 
-// Relax up to K edges (bit k of `valid`: e[k] out of a node at distance
-// dn[k] != INF).  Returns the mask of edges whose atomicMin strictly lowered
-// dist[v[k]] to cand[k] (atomic_relax_min, engine.py:120-139); the ones that
-// also won the stamp claim were pushed to the CTA queue.
-// STREAM: the K edges of a batch are lanes-consecutive across the warp, so
-// every col / weight line is consumed by one load instruction and can be
-// fetched evict-first; thread-serial walks (BS, NS) reuse a line over several
-// batches and keep the default policy.
-template <int K, bool STREAM = true, typename D, bool W>
-__device__ __forceinline__ unsigned relax_batch(const Relaxer<D, W>& rx, BlockQ& bq,
-                                                const long long (&e)[K], const D (&dn)[K],
-                                                unsigned valid, ThreadCounters& c,
-                                                uint32_t (&v)[K], D (&cand)[K]) {
-  uint32_t w[K];
-  const unsigned long long pol = STREAM ? l2_evict_first() : 0ull;
-#pragma unroll
-  for (int k = 0; k < K; ++k)
-    if (valid >> k & 1u) {
-      v[k] = STREAM ? ld_stream_pol(rx.col + e[k], pol) : __ldg(rx.col + e[k]);
-      w[k] = W ? (STREAM ? ld_stream_pol(rx.wt + e[k], pol) : __ldg(rx.wt + e[k])) : 1u;
-    }
+// Relax up to K loaded edges (bit k of `valid`: edge to v[k] of weight w[k]
+// out of a node at distance dn[k] != INF).  Returns the mask of edges whose
+// atomicMin strictly lowered dist[v[k]] to cand[k] (atomic_relax_min,
+// engine.py:120-139); the ones that also won the stamp claim were pushed to
+// the CTA queue.  All dist gathers are issued before any atomic, so a thread
+// keeps K loads in flight.
+template <int K, typename D, bool W>
+__device__ __forceinline__ unsigned relax_vals(const Relaxer<D, W>& rx, BlockQ& bq,
+                                               const uint32_t (&v)[K], const uint32_t (&w)[K],
+                                               const D (&dn)[K], unsigned valid, ThreadCounters& c,
+                                               D (&cand)[K]) {
   unsigned want = 0;
 #if GLB_PRECHECK
   D cur[K];
@@ -245,6 +235,30 @@ __device__ __forceinline__ unsigned relax_batch(const Relaxer<D, W>& rx, BlockQ&
       ++c.push;
     }
   return won;
+}
+
+// Relax up to K edges e[k] (col / weight loads, then relax_vals).
+// STREAM: the K edges of a batch are lanes-consecutive across the warp, so
+// every col / weight line is consumed by one load instruction and can be
+// fetched evict-first; thread-serial walks (BS, NS) reuse a line over several
+// batches and keep the default policy.
+template <int K, bool STREAM = true, typename D, bool W>
+__device__ __forceinline__ unsigned relax_batch(const Relaxer<D, W>& rx, BlockQ& bq,
+                                                const long long (&e)[K], const D (&dn)[K],
+                                                unsigned valid, ThreadCounters& c,
+                                                uint32_t (&v)[K], D (&cand)[K]) {
+  uint32_t w[K];
+  const unsigned long long pol = STREAM ? l2_evict_first() : 0ull;
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    v[k] = 0;
+    w[k] = 1u;
+    if (valid >> k & 1u) {
+      v[k] = STREAM ? ld_stream_pol(rx.col + e[k], pol) : __ldg(rx.col + e[k]);
+      if (W) w[k] = STREAM ? ld_stream_pol(rx.wt + e[k], pol) : __ldg(rx.wt + e[k]);
+    }
+  }
+  return relax_vals<K>(rx, bq, v, w, dn, valid, c, cand);
 }
 
 // Serial walk over [lo, hi) by one thread in batches of K.
@@ -315,73 +329,7 @@ __global__ void __launch_bounds__(kBlock) k_bs_relax(const long long* __restrict
     }
     bq_flush(bq, rx.qout, rx.nout);
   }
-  flush_counters(ctrl->ls, c);
-  timer_end(ctrl->t_relax);
-  ctl_tail(tail, ctrl);
-}
-
-// ============================================================ NS (K9) ===
-// children of original node v: n_orig + cs[v] .. n_orig + cs[v+1]
-template <typename D, bool W>
-__global__ void __launch_bounds__(kBlock) k_ns_relax(const long long* __restrict__ row,
-                                                     const long long* __restrict__ cs,
-                                                     long long n_orig, Relaxer<D, W> rx0,
-                                                     DevCtrl* ctrl, CtlTail tail) {
-  __shared__ uint32_t s_q[kQCap];
-  __shared__ BlockQ bq;
-  const unsigned n = ctrl->qcount[ctrl->in];
-  if (blockIdx.x * kBlock >= n) {  // idle CTA: no barriers, no atomics
-    ctl_tail(tail, ctrl);
-    return;
-  }
-  timer_begin(ctrl->t_relax);
-  bq_init(bq, s_q);
-  const Relaxer<D, W> rx = bind(rx0, ctrl);
-  const uint32_t* __restrict__ qin = ctrl->qptr[ctrl->in];
-  ThreadCounters c;
-  constexpr int K = 4;
-  for (unsigned base = blockIdx.x * kBlock; base < n; base += gridDim.x * kBlock) {
-    const unsigned i = base + threadIdx.x;
-    if (i < n) {
-      const uint32_t u = qin[i];
-      const D du = rx.dist(u);
-      if (du != DistTraits<D>::kInf) {
-        const long long lo = row[u], hi = row[u + 1];
-        for (long long b = lo; b < hi; b += K) {
-          long long e[K];
-          D d[K];
-          unsigned valid = 0;
-#pragma unroll
-          for (int k = 0; k < K; ++k) {
-            e[k] = b + k;
-            d[k] = du;
-            if (b + k < hi) valid |= 1u << k;
-          }
-          uint32_t v[K];
-          D cand[K];
-          unsigned won = relax_batch<K, false>(rx, bq, e, d, valid, c, v, cand);
-          // reflect each improved parent's value onto its children (splitting.py:154-160)
-#pragma unroll
-          for (int k = 0; k < K; ++k) {
-            if (!(won >> k & 1u) || v[k] >= n_orig) continue;
-            const long long k1 = cs[v[k] + 1];
-            for (long long ch = cs[v[k]]; ch < k1; ++ch) {
-              const uint32_t child = (uint32_t)(n_orig + ch);
-              ++c.relax;
-              bool first = false;
-              if (relax_cell<D>(rx.cells, child, cand[k], rx.gen, &first) &&
-                  rx.claim_push(child, first)) {
-                bq_push(bq, rx.qout, rx.nout, child);
-                ++c.push;
-              }
-            }
-          }
-        }
-      }
-    }
-    bq_flush(bq, rx.qout, rx.nout);
-  }
-  flush_counters(ctrl->ls, c);
+  flush_counters(ctrl, c);
   timer_end(ctrl->t_relax);
   ctl_tail(tail, ctrl);
 }
@@ -505,7 +453,7 @@ __global__ void __launch_bounds__(kBlock) k_ep_relax(const long long* __restrict
       __syncthreads();
     }
   }
-  flush_counters(ctrl->ls, c);
+  flush_counters(ctrl, c);
   timer_end(ctrl->t_relax);
   ctl_tail(tail, ctrl);
 }
@@ -959,177 +907,7 @@ __global__ void __launch_bounds__(kBlock, GLB_WD_MINB) k_wd_relax(
   c.work = n_work;
   c.relax = n_relax;
   c.push = n_push;
-  flush_counters(ctrl->ls, c);
-  timer_end(ctrl->t_relax);
-  ctl_tail(tail, ctrl);
-}
-
-// ============================================================ HP (K10) ===
-// Window [s*mdt, (s+1)*mdt) of every sublist node, binned by window length:
-// windows >= kHpCtaThreshold take the whole CTA; all shorter windows of the
-// CTA's 256 nodes are flattened by a block scan and relaxed cooperatively
-// (each thread finds its edge's node by binary search over the 256 window
-// offsets in shared memory), so lanes walk consecutive edges.
-constexpr long long kHpCtaThreshold = 2048;
-constexpr long long kHpPiece = 2048;  // edges per CTA-bin piece
-constexpr int kHpQbCache = 2048;      // CTA-bin windows whose piece index is cached in smem
-
-template <typename D, bool W>
-__global__ void __launch_bounds__(kBlock, GLB_RELAX_MINB) k_hp_window(const long long* __restrict__ row,
-                                                      Relaxer<D, W> rx0, DevCtrl* ctrl) {
-  pdl_trigger();
-  using BScan = cub::BlockScan<int, kBlock, cub::BLOCK_SCAN_WARP_SCANS>;
-  __shared__ uint32_t s_q[kQCap];
-  __shared__ BlockQ bq;
-  __shared__ typename BScan::TempStorage s_scan;
-  __shared__ int s_off[kBlock];
-  __shared__ long long s_edge[kBlock];
-  __shared__ D s_dnv[kBlock];
-  __shared__ long long s_lo, s_hi;
-  __shared__ D s_dn;
-  __shared__ int s_owner;
-  __shared__ long long s_chunk;
-  const long long n = ctrl->qcount[ctrl->in];
-  if (blockIdx.x * (long long)kBlock >= n) return;  // idle CTA
-  timer_begin(ctrl->t_relax);
-  bq_init(bq, s_q);
-  const Relaxer<D, W> rx = bind(rx0, ctrl);
-  const uint32_t* __restrict__ qin = ctrl->qptr[ctrl->in];
-  uint32_t* qnext = ctrl->qptr[ctrl->next];
-  unsigned int* nnext = &ctrl->qcount[ctrl->next];
-  const long long window = ctrl->window, mdt = ctrl->mdt;
-  ThreadCounters c;
-  // chunks of 256 sublist nodes handed out by ticket: CTAs that drew light
-  // chunks take more, so one heavy chunk no longer sets the launch time
-  while (true) {
-    if (threadIdx.x == 0) s_chunk = (long long)atomicAdd(&ctrl->relax_ticket, 1ull);
-    __syncthreads();
-    const long long base = s_chunk * kBlock;
-    if (base >= n) break;
-    const long long i = base + threadIdx.x;
-    long long lo = 0, hi = 0;
-    D dn = DistTraits<D>::kInf;
-    if (i < n) {
-      const uint32_t u = qin[i];
-      const long long r0 = row[u], r1 = row[u + 1];
-      const long long start = r0 + window;
-      if (start < r1) {
-        const long long end = start + mdt < r1 ? start + mdt : r1;
-        dn = rx.dist(u);
-        if (dn != DistTraits<D>::kInf) {
-          lo = start;
-          hi = end;
-        }
-        if (end < r1) {  // unfinished: carry into the next sublist
-          q_append(qnext, nnext, u);
-          ++c.push;
-        }
-      }
-    }
-    // CTA granularity for long windows: into the grid-wide CTA bin, relaxed
-    // in 2048-edge pieces by every CTA of the next launch (k_hp_bigbin)
-    if (hi - lo >= kHpCtaThreshold) {
-      const unsigned pieces = (unsigned)((hi - lo + kHpPiece - 1) / kHpPiece);
-      const unsigned long long r =
-          atomicAdd(&ctrl->hp_big_ctr, (1ull << 32) | (unsigned long long)pieces);
-      HpBig* b = ctrl->hp_big + (unsigned)(r >> 32);
-      b->dn = (unsigned long long)dn;
-      b->lo = lo;
-      b->hi = hi;
-      b->qbase = (unsigned)r;
-      lo = hi;
-    }
-    // fine-grained gather of the remaining windows
-    int len = (int)(hi - lo), off, total;
-    BScan(s_scan).ExclusiveSum(len, off, total);
-    s_off[threadIdx.x] = off;
-    s_edge[threadIdx.x] = lo - off;
-    s_dnv[threadIdx.x] = dn;
-    __syncthreads();
-    constexpr int K = 4;
-    for (int f0 = 0; f0 < total; f0 += K * kBlock) {
-      long long e[K];
-      D d[K];
-      unsigned valid = 0;
-#pragma unroll
-      for (int k = 0; k < K; ++k) {
-        const int f = f0 + k * kBlock + threadIdx.x;
-        if (f < total) {
-          int o = 0;  // last window whose offset <= f
-#pragma unroll
-          for (int step = kBlock / 2; step > 0; step >>= 1)
-            if (s_off[o + step] <= f) o += step;
-          e[k] = s_edge[o] + f;
-          d[k] = s_dnv[o];
-          valid |= 1u << k;
-        }
-      }
-      uint32_t v[K];
-      D cand[K];
-      relax_batch<K>(rx, bq, e, d, valid, c, v, cand);
-    }
-    bq_flush(bq, rx.qout, rx.nout);
-  }
-  flush_counters(ctrl->ls, c);
-  timer_end(ctrl->t_relax);
-}
-
-// The CTA bin of the window step: a second launch (so no CTA ever waits for
-// another to be scheduled) where every CTA claims 2048-edge pieces of the long
-// windows by ticket; a piece's window is found by binary search over the
-// windows' first pieces (cached in shared memory).
-template <typename D, bool W>
-__global__ void __launch_bounds__(kBlock, GLB_RELAX_MINB) k_hp_bigbin(Relaxer<D, W> rx0,
-                                                                      DevCtrl* ctrl, CtlTail tail) {
-  pdl_wait();
-  __shared__ uint32_t s_q[kQCap];
-  __shared__ BlockQ bq;
-  __shared__ long long s_lo, s_hi;
-  __shared__ D s_dn;
-  __shared__ int s_owner;
-  __shared__ unsigned s_qb[kHpQbCache];  // first piece of every CTA-bin window
-  const unsigned long long bc = ctrl->hp_big_ctr;
-  const unsigned nbig = (unsigned)(bc >> 32), npieces = (unsigned)bc;
-  if (npieces == 0 || blockIdx.x >= npieces) {
-    ctl_tail(tail, ctrl);
-    return;
-  }
-  timer_begin(ctrl->t_relax);
-  bq_init(bq, s_q);
-  const Relaxer<D, W> rx = bind(rx0, ctrl);
-  ThreadCounters c;
-  const bool cached = nbig <= (unsigned)kHpQbCache;
-  if (cached)
-    for (unsigned i = threadIdx.x; i < nbig; i += kBlock) s_qb[i] = ctrl->hp_big[i].qbase;
-  __syncthreads();
-  while (true) {
-    if (threadIdx.x == 0) {
-      s_owner = -1;
-      const unsigned t = atomicAdd(&ctrl->hp_piece_next, 1u);
-      if (t < npieces) {
-        unsigned lo_i = 0, hi_i = nbig;  // last window with qbase <= t
-        while (hi_i - lo_i > 1) {
-          const unsigned mid = (lo_i + hi_i) >> 1;
-          const unsigned qb = cached ? s_qb[mid] : ctrl->hp_big[mid].qbase;
-          if (qb <= t)
-            lo_i = mid;
-          else
-            hi_i = mid;
-        }
-        const HpBig b = ctrl->hp_big[lo_i];
-        const long long off = (long long)(t - b.qbase) * kHpPiece;
-        s_lo = b.lo + off;
-        s_hi = b.lo + off + kHpPiece < b.hi ? b.lo + off + kHpPiece : b.hi;
-        s_dn = (D)b.dn;
-        s_owner = 1;
-      }
-    }
-    __syncthreads();
-    if (s_owner < 0) break;
-    relax_range_coop<4>(rx, bq, s_lo, s_hi, s_dn, threadIdx.x, kBlock, c);
-    bq_flush(bq, rx.qout, rx.nout);
-  }
-  flush_counters(ctrl->ls, c);
+  flush_counters(ctrl, c);
   timer_end(ctrl->t_relax);
   ctl_tail(tail, ctrl);
 }

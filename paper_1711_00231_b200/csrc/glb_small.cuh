@@ -420,6 +420,8 @@ __global__ void __cluster_dims__(kSmallCtas, 1, 1) __launch_bounds__(kSmallThrea
       }
     }
     // ---- counters of the iteration meet in CTA 0 (distributed shared memory)
+    if (ran && sc.ptw && c.work && sc.ptw_off + gt < sc.ptw_cap)
+      sc.ptw[sc.ptw_off + gt] = c.work > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)c.work;
     if (ran) {
       unsigned long long w = c.work, r = c.relax, p = c.push, sq = c.work * c.work, mx = c.work;
 #pragma unroll
@@ -465,6 +467,11 @@ __global__ void __cluster_dims__(kSmallCtas, 1, 1) __launch_bounds__(kSmallThrea
           rec.k0 = s_t0;
           rec.k1 = gtime();
           rec.o0 = rec.o1 = 0;
+        }
+        // every CTA advances its copy of the list cursor identically
+        if (!wd_empty && cc->nrec < cc->rec_cap) {
+          const long long off = ctl_ptw_take(cc, kSmallAll);
+          if (rank == 0) cc->recs[cc->nrec].ptw_off = off;
         }
         if (!wd_empty) cc->nrec += 1;
         if (cc->strategy == GLB_HP) {  // hierarchical.py:54-136

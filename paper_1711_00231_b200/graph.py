@@ -241,6 +241,18 @@ class DeviceCsrGraph:
     def release_device(self) -> None:
         _destroy_handles(self._handles)
 
+    def download_narrow(self):
+        """(row int64[n+1], col uint32[m], weights uint32[m] or None): the
+        device layout as is, half the host memory of ``to_host``."""
+        row = np.empty(self.num_nodes + 1, dtype=INDEX_DTYPE)
+        col = np.empty(self.num_edges, dtype=np.uint32)
+        w = np.empty(self.num_edges, dtype=np.uint32) if self._weighted else None
+        u32 = ctypes.POINTER(ctypes.c_uint32)
+        _lib.check(_lib.lib().glb_graph_download_u32(
+            self._handles[self._device], _lib.ptr64(row), col.ctypes.data_as(u32),
+            None if w is None else w.ctypes.data_as(u32)), "glb_graph_download_u32")
+        return row, col, w
+
     def to_host(self) -> CsrGraph:
         row = np.empty(self.num_nodes + 1, dtype=INDEX_DTYPE)
         col = np.empty(self.num_edges, dtype=INDEX_DTYPE)

@@ -36,10 +36,15 @@ class KernelConfig:
     (hierarchical.py:49).  ``virtual_threads``/``workers``/``deterministic_replay``/
     ``schedule_seed`` only steered the CPU emulation; they are validated and
     kept for compatibility, the device sizes its own grids.  ``loop`` picks the
-    host-driven loop ("host", one round trip per launch, exact per-launch
-    timing) or the device-driven CUDA graph ("graph").  ``dist_bits`` 0 runs
-    24-bit distances (one u32 cell per node), re-running at 32 and then 64
-    bits on overflow; 24 / 32 / 64 pin one width.
+    device-driven CUDA graph ("graph", the default: one launch per traversal)
+    or the host-driven loop ("host", one round trip per launch, CUDA-event
+    time per launch).  ``dist_bits`` 0 picks the distance tier (24-bit cells
+    for graphs whose 64-bit cells exceed twice the L2, else 32-bit), re-running
+    at the next width on overflow; 24 / 32 / 64 pin one width.
+    ``instrument`` records every launch's exact per-thread work list on the
+    device (``MetricsRecord.per_thread_work``, as the reference's harness
+    consumes it, bench.py:120-164); off, records carry the device's summed
+    counters (sum, sum of squares, max) only.
     """
 
     virtual_threads: int | None = None
@@ -48,9 +53,10 @@ class KernelConfig:
     deterministic_replay: bool = False
     schedule_seed: int | None = None
     device: int | None = None
-    loop: str = "host"
+    loop: str = "graph"
     dist_bits: int = 0
     record_timing: bool = True
+    instrument: bool = True
 
     def __post_init__(self):
         if self.virtual_threads is not None and self.virtual_threads < 1:
@@ -134,14 +140,15 @@ class DistArray:
         return f"DistArray({self._a!r})"
 
 
-@dataclass
+@dataclass(eq=False)
 class MetricsRecord:
     """Counters of one kernel invocation (engine.py:142-174).
 
-    ``per_thread_work`` is not shipped from the device; ``work_total``,
-    ``work_max`` and ``work_sumsq`` summarise it exactly over ``n_threads``
-    launched threads, and the reference's accessors are computed from them.
-    Wall times are seconds of CUDA-event time on the library stream.
+    ``per_thread_work`` is the exact per-thread list of an instrumented run
+    (an int64 numpy array, one entry per launched thread) or None; either way
+    ``total_work``, ``max_work`` and ``work_sumsq`` hold the device's summed
+    counters over ``n_threads`` threads and the accessors use them.  Wall
+    times are seconds of device time on the library stream.
     """
 
     iteration: int
@@ -158,20 +165,26 @@ class MetricsRecord:
     max_work: int = 0
     work_sumsq: float = 0.0
 
+    def _list(self):
+        # a plain list given by the caller wins; device runs carry counters too
+        w = self.per_thread_work
+        if w is None or (self.n_threads and isinstance(w, np.ndarray)):
+            return None
+        return w
+
     @property
     def threads(self) -> int:
-        if self.per_thread_work is not None:
-            return len(self.per_thread_work)
-        return self.n_threads
+        w = self._list()
+        return len(w) if w is not None else self.n_threads
 
     def work_total(self) -> int:
-        if self.per_thread_work is not None:
-            return sum(self.per_thread_work)
-        return self.total_work
+        w = self._list()
+        return sum(w) if w is not None else self.total_work
 
     def work_max(self) -> int:
-        if self.per_thread_work is not None:
-            return max(self.per_thread_work) if self.per_thread_work else 0
+        w = self._list()
+        if w is not None:
+            return max(w) if len(w) else 0
         return self.max_work
 
     def work_avg(self) -> float:
@@ -182,9 +195,10 @@ class MetricsRecord:
         t = self.threads
         if t == 0:
             return 0.0
-        if self.per_thread_work is not None:
+        w = self._list()
+        if w is not None:
             avg = self.work_total() / t
-            return sqrt(sum((w - avg) ** 2 for w in self.per_thread_work) / t)
+            return sqrt(sum((x - avg) ** 2 for x in w) / t)
         avg = self.total_work / t
         var = self.work_sumsq / t - avg * avg
         return sqrt(var) if var > 0 else 0.0

@@ -94,13 +94,31 @@ def _records(h, stats: _lib.RunStats, buf) -> list[MetricsRecord]:
         got = ctypes.c_int64()
         _lib.check(_lib.lib().glb_run_records(h, len(raw), more, len(more), ctypes.byref(got)))
         raw.extend(more[: got.value])
+    # exact per-thread work lists of an instrumented run: one download of the
+    # run's list, each record a view of its slice
+    ptw = None
+    total = ctypes.c_int64()
+    if any(r.thread_work_offset >= 0 for r in raw):
+        _lib.check(_lib.lib().glb_run_thread_work(h, 0, 0, None, ctypes.byref(total)))
+        if total.value:
+            flat = np.empty(total.value, dtype=np.uint32)
+            _lib.check(_lib.lib().glb_run_thread_work(
+                h, 0, total.value, flat.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32)), None))
+            ptw = flat.astype(np.int64)
     out = []
     for r in raw:
+        lst = None
+        if ptw is not None and r.thread_work_offset >= 0 and r.thread_work_offset + r.threads <= ptw.size:
+            lst = ptw[r.thread_work_offset: r.thread_work_offset + r.threads]
+        wmax, wsq = r.work_max, r.work_sumsq
+        if lst is not None:  # HP's two kernels add into one list entry per thread
+            wmax = int(lst.max(initial=0))
+            wsq = float(np.dot(lst.astype(np.float64), lst.astype(np.float64)))
         out.append(MetricsRecord(
             iteration=r.iteration,
             strategy=_TAG_OF.get(r.tag, str(r.tag)),
             active_items=r.active_items,
-            per_thread_work=None,
+            per_thread_work=lst,
             atomic_relax_ops=r.relax_ops,
             atomic_push_ops=r.push_ops,
             kernel_wall_time=r.kernel_ms / 1e3,
@@ -108,8 +126,8 @@ def _records(h, stats: _lib.RunStats, buf) -> list[MetricsRecord]:
             sub_iteration=None if r.sub_iteration < 0 else r.sub_iteration,
             n_threads=r.threads,
             total_work=r.work_total,
-            max_work=r.work_max,
-            work_sumsq=r.work_sumsq,
+            max_work=wmax,
+            work_sumsq=wsq,
         ))
     return out
 
@@ -138,6 +156,7 @@ def _device_run(tag: str, g: CsrGraph, source: int, op: RelaxOp, cfg: KernelConf
     p.dist_bits = cfg.dist_bits
     p.loop_mode = _lib.GLB_LOOP_GRAPH if cfg.loop == "graph" else _lib.GLB_LOOP_HOST
     p.record_timing = 1 if cfg.record_timing else 0
+    p.instrument = 1 if (cfg.instrument and want_records) else 0
     dist = np.empty(g.num_nodes, dtype=INDEX_DTYPE)
     stats = _lib.RunStats()
     cap = 4096 if want_records else 0

@@ -1,6 +1,6 @@
 """Generate the golden vectors by importing the REFERENCE graphlb in place.
 
-    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py [--big]
+    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py [--big [C1 C2 C3 C4]]
 
 Runs only in the build container (the GPU box has no /root/reference).  The
 outputs are committed; tests/test_oracle_golden.py pins oracle/ against them
@@ -12,8 +12,9 @@ and the GPU parity tests compare the device results with them.
   kats.json        SPEC.md known-answer vectors evaluated on the reference
   split.npz        reference split_graph arrays for corpus graphs
   scan.npz         reference inclusive_scan / find_offsets on random inputs
-  big.json         (--big) digests of reference oracle distances at C1 and
-                   C2 (RMAT s16 / s22), plus N_r / E_r
+  big.json         (--big) digests of reference oracle distances at C1, C2
+                   (RMAT s16 / s22), C3 (4096^2 grid) and C4 (skewed RMAT
+                   s22), plus the graph digests, N_r / E_r
 """
 
 from __future__ import annotations
@@ -202,12 +203,33 @@ def make_scan():
     print("scan.npz", len(arrays))
 
 
-def make_big():
-    out = {}
-    for name, spec in (("C1", dict(kind="rmat", scale=16, edge_factor=16, seed=1, max_weight=255)),
-                       ("C2", dict(kind="rmat", scale=22, edge_factor=16, seed=1, max_weight=255))):
+BIG_SPECS = {
+    "C1": dict(kind="rmat", scale=16, edge_factor=16, seed=1, max_weight=255),
+    "C2": dict(kind="rmat", scale=22, edge_factor=16, seed=1, max_weight=255),
+    # C3: the grid is not a reference generator; its arrays come from
+    # paper_1711_00231_b200.grid_graph and the REFERENCE oracle runs on them
+    "C3": dict(kind="grid", k=4096, seed=1, max_weight=255),
+    "C4": dict(kind="rmat", scale=22, edge_factor=16, seed=1, max_weight=255,
+               params=(0.7, 0.15, 0.10, 0.05)),
+}
+
+
+def _build_big(spec):
+    if spec["kind"] == "grid":
+        import paper_1711_00231_b200 as pkg
+
+        h = pkg.grid_graph(spec["k"], seed=spec["seed"], max_weight=spec["max_weight"])
+        return ref.CsrGraph(h.num_nodes, h.num_edges, h.row_offsets, h.col_indices, h.weights)
+    return gs.build(ref, spec)
+
+
+def make_big(names):
+    path = HERE / "big.json"
+    out = json.loads(path.read_text()) if path.exists() else {}
+    for name in names:
+        spec = BIG_SPECS[name]
         t0 = time.time()
-        g = gs.build(ref, spec)
+        g = _build_big(spec)
         rec = {"spec": spec, "graph_digest": gs.digest(g), "n": g.num_nodes, "m": g.num_edges,
                "gen_s": time.time() - t0}
         deg = g.outdegrees()
@@ -223,12 +245,13 @@ def make_big():
         out[name] = rec
         print(name, rec, flush=True)
         del g
-    (HERE / "big.json").write_text(json.dumps(out, indent=1, sort_keys=True))
+        path.write_text(json.dumps(out, indent=1, sort_keys=True))
 
 
 if __name__ == "__main__":
     if "--big" in sys.argv:
-        make_big()
+        names = [a for a in sys.argv[1:] if a in BIG_SPECS] or list(BIG_SPECS)
+        make_big(names)
     else:
         make_generators()
         make_kats()

@@ -97,3 +97,59 @@ def test_oracle_scan_and_offsets(oracle, golden):
 
 def test_oracle_coo(oracle, golden):
     assert oracle.coo_src([0, 2, 2]).tolist() == golden["kats"]["coo_small"]["src"]
+
+
+# ------------------------------------------------ narrow-layout oracle (C3-C5)
+def _narrow(oracle, g):
+    return oracle.NarrowGraph(g.row_offsets, g.col_indices.astype(np.uint32),
+                              None if g.weights is None else g.weights.astype(np.uint32))
+
+
+def test_oracle_rmat_generator_matches_reference_digests(oracle, golden):
+    """The C restatement of generate_rmat + from_edges (numpy PCG64 stream,
+    Lemire-bounded weights, stable grouping by source) reproduces the
+    reference's graphs byte for byte."""
+    d = golden["generators"]
+    specs = dict(d["extra_specs"])
+    specs.update({k: v for k, v in gs.CORPUS.items() if v["kind"] == "rmat"})
+    for gid, spec in specs.items():
+        if spec["kind"] != "rmat":
+            continue
+        g = oracle.rmat_narrow(spec["scale"], spec["edge_factor"],
+                               tuple(spec.get("params", pkg.DEFAULT_RMAT_PARAMS)), spec["seed"],
+                               spec.get("weighted", True), spec.get("max_weight", 100), threads=3)
+        assert gs.digest(g) == d["digests"][gid], gid
+    for w in (1, 3, 7, 1000, 65535):  # rejection thresholds; W=1 draws nothing
+        a = pkg.generate_rmat(11, 8, seed=5, max_weight=w)
+        assert gs.digest(oracle.rmat_narrow(11, 8, seed=5, max_weight=w)) == gs.digest(a), w
+
+
+def test_oracle_narrow_traversals_match_reference_corpus(oracle, golden):
+    for gid, spec in gs.CORPUS.items():
+        g = gs.build(pkg, spec)
+        ng = _narrow(oracle, g)
+        for src in gs.sources_for(g.num_nodes):
+            for algo in ("bfs", "sssp"):
+                exp = golden["corpus"][f"{gid}|{src}|{algo}"]
+                if algo == "bfs":
+                    assert np.array_equal(oracle.bfs_narrow(ng, src, parallel=False), exp), gid
+                    assert np.array_equal(oracle.bfs_narrow(ng, src, threads=4), exp), gid
+                else:
+                    d, _, _, done = oracle.bs_run_narrow(ng, src, ng.weights is not None, threads=4)
+                    assert done and np.array_equal(d, exp), gid
+
+
+def test_oracle_narrow_c2_matches_reference_digests(oracle, golden):
+    """C2 (RMAT s22) end to end in the narrow oracle: graph, BFS levels and
+    SSSP distances equal the reference's (big.json, made by the reference)."""
+    big = golden["big"]
+    if not big:
+        pytest.skip("big.json not generated")
+    c2 = big["C2"]
+    g = oracle.rmat_narrow(22, 16, seed=1, max_weight=255)
+    assert gs.digest(g) == c2["graph_digest"]
+    assert gs.dist_digest(oracle.narrow_distances(g, 0, "bfs")) == c2["bfs_digest"]
+    assert gs.dist_digest(oracle.narrow_distances(g, 0, "sssp")) == c2["sssp_digest"]
+    # a time-bounded run_bs sample stops early with partial work counted
+    _, it, ops, done = oracle.bs_run_narrow(g, 0, True, max_seconds=1e-6)
+    assert not done and it >= 1 and ops >= 1
