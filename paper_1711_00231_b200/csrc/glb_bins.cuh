@@ -2,20 +2,22 @@
 // hierarchical processing (HP, hierarchical.py:95-120) and node splitting
 // (NS, splitting.py:141-162).
 //
-// A step hands every thread of a CTA chunk (256 worklist items, claimed by
+// A step hands every lane of a warp chunk (32 worklist items, claimed by
 // ticket) one edge window [lo, lo + len) relaxed from distance dn -- HP: the
 // sub-iteration window [s*mdt, (s+1)*mdt) of a sublist node; NS: the whole
 // out-range of a split-graph node.  Windows are binned by length:
 //
-//   thread bin  len <= 32       the window stays with its lane; the 32 lanes'
-//                               windows are packed warp-wide (exclusive warp
-//                               scan of the lengths) and walked 32 edges per
-//                               load instruction, each edge's owner lane found
-//                               by a 5-step shuffle search -- one thread's
-//                               window, the warp's load slots;
-//   warp bin    32 < len < 2048 appended to the CTA's shared-memory queue
-//                               (warp-aggregated); warps claim entries and walk
-//                               them with lanes on consecutive edges;
+//   thread bin  len <= 32       one lane's window;
+//   warp bin    32 < len < 2048 a window its warp walks lane-consecutively;
+//                               both bins stay with the warp that drew the
+//                               items (32 per warp ticket): the warp walks the
+//                               concatenation of its lanes' windows (exclusive
+//                               warp scan of the lengths; an edge's owner lane
+//                               by a 5-step shuffle search), 32 consecutive
+//                               edges per load instruction and K per lane in
+//                               flight, so a thread-bin window never idles 31
+//                               lanes and a warp-bin window never idles the
+//                               tail of its last pass;
 //   CTA bin     len >= 2048     appended to the grid-wide bin (one 64-bit
 //                               atomic reserves the entry and its 2048-edge
 //                               pieces); the step's second kernel (k_bigbin,
@@ -47,21 +49,64 @@ constexpr int kBinQbCache = 1024;        // CTA-bin windows whose first piece is
 constexpr int kBinBuf = (int)kBinPiece + 4;  // a piece plus the 16-byte alignment slack
 constexpr int kBinK = 4;                 // edges in flight per lane
 
+// -------------------------------------------------------------- sinks ---
+// Warp-private push buffer in shared memory, flushed with one global
+// reservation per kBinWarpQ entries: the warps of a CTA never wait for each
+// other (all 32 lanes call push / flush together).
+constexpr int kBinWarps = kBlock / 32;
+constexpr int kBinWarpQ = 256;
+struct WarpSink {
+  uint32_t* buf;
+  unsigned n;
+  uint32_t* qout;
+  unsigned int* nout;
+  __device__ __forceinline__ void flush() {
+    __syncwarp();
+    unsigned base = 0;
+    if (lane_id() == 0 && n) base = atomicAdd(nout, n);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    for (unsigned i = lane_id(); i < n; i += 32) qout[base + i] = buf[i];
+    __syncwarp();
+    n = 0;
+  }
+  template <int K>
+  __device__ __forceinline__ void push(unsigned first, const uint32_t (&v)[K], ThreadCounters& c) {
+    constexpr unsigned FULL = 0xffffffffu;
+    const unsigned mine = __popc(first), lane = lane_id();
+    unsigned incl = mine;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const unsigned y = __shfl_up_sync(FULL, incl, off);
+      if (lane >= (unsigned)off) incl += y;
+    }
+    const unsigned total = __shfl_sync(FULL, incl, 31);
+    if (!total) return;
+    if (n + total > (unsigned)kBinWarpQ) flush();
+    unsigned pos = n + incl - mine;
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+      if (first >> k & 1u) buf[pos++] = v[k];
+    n += total;
+    c.push += mine;
+  }
+};
+
 // -------------------------------------------------------------- mirrors ---
 struct NoMirror {
   template <int K, typename D, bool W>
-  __device__ __forceinline__ void operator()(const Relaxer<D, W>&, BlockQ&, unsigned,
+  __device__ __forceinline__ void operator()(const Relaxer<D, W>&, unsigned,
                                              const uint32_t (&)[K], const D (&)[K],
                                              ThreadCounters&) const {}
 };
 
 // splitting.py:154-160: a strict improvement of original node v is written
-// onto its children n_orig + cs[v] .. n_orig + cs[v+1] (contiguous ids).
+// onto its children n_orig + cs[v] .. n_orig + cs[v+1] (contiguous ids);
+// pushes go straight to the out list (warp-aggregated, divergence-safe).
 struct NsMirror {
   const long long* __restrict__ cs;
   long long n_orig;
   template <int K, typename D, bool W>
-  __device__ __forceinline__ void operator()(const Relaxer<D, W>& rx, BlockQ& bq, unsigned won,
+  __device__ __forceinline__ void operator()(const Relaxer<D, W>& rx, unsigned won,
                                              const uint32_t (&v)[K], const D (&cand)[K],
                                              ThreadCounters& c) const {
 #pragma unroll
@@ -73,7 +118,7 @@ struct NsMirror {
         ++c.relax;
         bool first = false;
         if (relax_cell<D>(rx.cells, child, cand[k], rx.gen, &first) && rx.claim_push(child, first)) {
-          bq_push(bq, rx.qout, rx.nout, child);
+          q_append(rx.qout, rx.nout, child);
           ++c.push;
         }
       }
@@ -120,22 +165,6 @@ __device__ __forceinline__ void fence_proxy_async() {
 }
 
 // ------------------------------------------------------- binned windows ---
-template <typename D>
-struct WinEntry {  // a warp-bin window
-  long long lo;
-  D dn;
-  unsigned len;
-};
-
-template <typename D>
-struct BinSmem {
-  uint32_t q[kQCap];            // CTA push queue items
-  WinEntry<D> wq[kBlock];       // warp bin of the chunk
-  BlockQ bq;
-  unsigned wq_n, wq_next;
-  long long chunk;
-};
-
 // Reserve a CTA-bin entry with its pieces (grid-wide; k_bigbin relaxes it).
 template <typename D>
 __device__ __forceinline__ void cta_bin_push(DevCtrl* ctrl, long long lo, long long len, D dn) {
@@ -148,11 +177,11 @@ __device__ __forceinline__ void cta_bin_push(DevCtrl* ctrl, long long lo, long l
   b->qbase = (unsigned)r;
 }
 
-// One chunk: every thread of the CTA brings its window (len 0 = none).
+// The windows of a warp's 32 lanes (len 0 = none; all lanes call it).
 template <typename D, bool W, class M>
-__device__ __forceinline__ void bins_chunk(const Relaxer<D, W>& rx, BinSmem<D>& sm, long long lo,
-                                           long long len, D dn, const M& mirror, DevCtrl* ctrl,
-                                           ThreadCounters& c) {
+__device__ __forceinline__ void warp_windows(const Relaxer<D, W>& rx, WarpSink& sink, long long lo,
+                                             long long len, D dn, const M& mirror, DevCtrl* ctrl,
+                                             ThreadCounters& c) {
   constexpr unsigned FULL = 0xffffffffu;
   constexpr int K = kBinK;
   const unsigned lane = lane_id();
@@ -160,99 +189,53 @@ __device__ __forceinline__ void bins_chunk(const Relaxer<D, W>& rx, BinSmem<D>& 
     cta_bin_push<D>(ctrl, lo, len, dn);
     len = 0;
   }
-  // ---- warp bin: into the CTA queue, one smem atomic per warp
-  const bool wb = len > (long long)kBinThreadMax;
-  const unsigned wmask = __ballot_sync(FULL, wb);
-  if (wmask) {
-    unsigned base = 0;
-    if (lane == (unsigned)(__ffs(wmask) - 1)) base = atomicAdd(&sm.wq_n, (unsigned)__popc(wmask));
-    base = __shfl_sync(FULL, base, __ffs(wmask) - 1);
-    if (wb) {
-      WinEntry<D>& q = sm.wq[base + __popc(wmask & ((1u << lane) - 1u))];
-      q.lo = lo;
-      q.dn = dn;
-      q.len = (unsigned)len;
-    }
+  const unsigned tl = (unsigned)len;
+  unsigned incl = tl;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const unsigned y = __shfl_up_sync(FULL, incl, off);
+    if (lane >= (unsigned)off) incl += y;
   }
-  // ---- thread bin: the lanes' windows packed warp-wide
-  {
-    const unsigned tl = wb ? 0u : (unsigned)len;
-    unsigned incl = tl;
+  const unsigned total = __shfl_sync(FULL, incl, 31);
+  const unsigned pre = incl - tl;
+  const uint32_t base32 = (uint32_t)lo - pre;  // edge of flat slot f: base32 + f (edge ids < 2^32)
+  const unsigned long long pol = l2_evict_first();
+  for (unsigned f0 = 0; f0 < total; f0 += 32u * K) {
+    uint32_t v[K], w[K];
+    D d[K];
+    unsigned valid = 0;
 #pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-      const unsigned y = __shfl_up_sync(FULL, incl, off);
-      if (lane >= (unsigned)off) incl += y;
-    }
-    const unsigned total = __shfl_sync(FULL, incl, 31);
-    const unsigned pre = incl - tl;
-    const uint32_t base32 = (uint32_t)lo - pre;  // edge of flat slot f: base32 + f (edge ids < 2^32)
-    for (unsigned f0 = 0; f0 < total; f0 += 32u * K) {
-      long long e[K];
-      D d[K];
-      unsigned valid = 0;
+    for (int k = 0; k < K; ++k) {
+      const unsigned f = f0 + (unsigned)k * 32u + lane;
+      int o = 0;  // last lane whose window starts at or before f
 #pragma unroll
-      for (int k = 0; k < K; ++k) {
-        const unsigned f = f0 + (unsigned)k * 32u + lane;
-        int o = 0;  // last lane whose window starts at or before f
-#pragma unroll
-        for (int step = 16; step >= 1; step >>= 1) {
-          const unsigned p = __shfl_sync(FULL, pre, o + step);
-          if (p <= f) o += step;
-        }
-        e[k] = (long long)(uint32_t)(__shfl_sync(FULL, base32, o) + f);
-        d[k] = shfl_dist(dn, o);
-        if (f < total) valid |= 1u << k;
+      for (int step = 16; step >= 1; step >>= 1) {
+        const unsigned p = __shfl_sync(FULL, pre, o + step);
+        if (p <= f) o += step;
       }
-      uint32_t v[K];
-      D cand[K];
-      const unsigned won = relax_batch<K>(rx, sm.bq, e, d, valid, c, v, cand);
-      mirror(rx, sm.bq, won, v, cand, c);
-    }
-  }
-  __syncthreads();  // the chunk's warp bin is complete
-  // ---- warp bin: one warp per window, lanes on consecutive edges
-  const unsigned nw = sm.wq_n;
-  while (true) {
-    unsigned idx = 0;
-    if (lane == 0) idx = atomicAdd(&sm.wq_next, 1u);
-    idx = __shfl_sync(FULL, idx, 0);
-    if (idx >= nw) break;
-    const WinEntry<D> q = sm.wq[idx];
-    const long long hi = q.lo + q.len;
-    for (long long b = q.lo; b < hi; b += 32ll * K) {
-      long long e[K];
-      D d[K];
-      unsigned valid = 0;
-#pragma unroll
-      for (int k = 0; k < K; ++k) {
-        e[k] = b + (long long)k * 32 + lane;
-        d[k] = q.dn;
-        if (e[k] < hi) valid |= 1u << k;
+      const uint32_t e = __shfl_sync(FULL, base32, o) + f;
+      d[k] = shfl_dist(dn, o);
+      v[k] = 0;
+      w[k] = 1u;
+      if (f < total) {
+        valid |= 1u << k;
+        v[k] = ld_stream_pol(rx.col + e, pol);
+        if (W) w[k] = ld_stream_pol(rx.wt + e, pol);
       }
-      uint32_t v[K];
-      D cand[K];
-      const unsigned won = relax_batch<K>(rx, sm.bq, e, d, valid, c, v, cand);
-      mirror(rx, sm.bq, won, v, cand, c);
     }
+    D cand[K];
+    const unsigned won = relax_vals<K>(rx, sink, v, w, d, valid, c, cand);
+    mirror(rx, won, v, cand, c);
   }
-  bq_flush(sm.bq, rx.qout, rx.nout);  // barriers on both sides
-  if (threadIdx.x == 0) sm.wq_n = sm.wq_next = 0;
 }
 
-template <typename D>
-__device__ __forceinline__ void bins_init(BinSmem<D>& sm) {
-  if (threadIdx.x == 0) sm.wq_n = sm.wq_next = 0;
-  bq_init(sm.bq, sm.q);  // has the barrier
-}
-
-// Claim the next 256-item chunk of the step (dynamic: CTAs that drew light
-// chunks take more).  Returns the chunk's first item, or -1 when done.
-template <typename D>
-__device__ __forceinline__ long long bins_next_chunk(BinSmem<D>& sm, DevCtrl* ctrl, long long n) {
-  if (threadIdx.x == 0) sm.chunk = (long long)atomicAdd(&ctrl->relax_ticket, 1ull) * kBlock;
-  __syncthreads();
-  const long long base = sm.chunk;
-  return base < n ? base : -1;
+// Claim the next 32 items of the step for this warp (dynamic: warps that
+// drew light items take more).  Returns the first item, or -1 when done.
+__device__ __forceinline__ long long warp_next_chunk(DevCtrl* ctrl, long long n) {
+  unsigned long long t = 0;
+  if (lane_id() == 0) t = atomicAdd(&ctrl->relax_ticket, 32ull);
+  t = __shfl_sync(0xffffffffu, t, 0);
+  return (long long)t < n ? (long long)t : -1;
 }
 
 // ============================================================ HP (K10) ===
@@ -260,21 +243,21 @@ __device__ __forceinline__ long long bins_next_chunk(BinSmem<D>& sm, DevCtrl* ct
 // (hierarchical.py:95-120); unfinished nodes are carried to the next sublist.
 template <typename D, bool W>
 __global__ void __launch_bounds__(kBlock, GLB_BIN_MINB) k_hp_window(const long long* __restrict__ row,
-                                                         Relaxer<D, W> rx0, DevCtrl* ctrl) {
+                                                                    Relaxer<D, W> rx0, DevCtrl* ctrl) {
   pdl_trigger();
-  __shared__ BinSmem<D> sm;
+  __shared__ uint32_t s_wq[kBinWarps][kBinWarpQ];
   const long long n = ctrl->qcount[ctrl->in];
   if (blockIdx.x * (long long)kBlock >= n) return;  // idle CTA
   timer_begin(ctrl->t_relax);
-  bins_init(sm);
   const Relaxer<D, W> rx = bind(rx0, ctrl);
+  WarpSink sink{s_wq[threadIdx.x >> 5], 0u, rx.qout, rx.nout};
   const uint32_t* __restrict__ qin = ctrl->qptr[ctrl->in];
   uint32_t* qnext = ctrl->qptr[ctrl->next];
   unsigned int* nnext = &ctrl->qcount[ctrl->next];
   const long long window = ctrl->window, mdt = ctrl->mdt;
   ThreadCounters c;
-  for (long long base; (base = bins_next_chunk(sm, ctrl, n)) >= 0;) {
-    const long long i = base + threadIdx.x;
+  for (long long base; (base = warp_next_chunk(ctrl, n)) >= 0;) {
+    const long long i = base + lane_id();
     long long lo = 0, len = 0;
     D dn = DistTraits<D>::kInf;
     if (i < n) {
@@ -294,8 +277,9 @@ __global__ void __launch_bounds__(kBlock, GLB_BIN_MINB) k_hp_window(const long l
         }
       }
     }
-    bins_chunk(rx, sm, lo, len, dn, NoMirror{}, ctrl, c);
+    warp_windows(rx, sink, lo, len, dn, NoMirror{}, ctrl, c);
   }
+  sink.flush();
   flush_counters(ctrl, c);
   timer_end(ctrl->t_relax);
 }
@@ -305,19 +289,19 @@ __global__ void __launch_bounds__(kBlock, GLB_BIN_MINB) k_hp_window(const long l
 // node's range binned like an HP window, plus child mirroring.
 template <typename D, bool W>
 __global__ void __launch_bounds__(kBlock, GLB_BIN_MINB) k_ns_relax(const long long* __restrict__ row,
-                                                        NsMirror mirror, Relaxer<D, W> rx0,
-                                                        DevCtrl* ctrl) {
+                                                                   NsMirror mirror, Relaxer<D, W> rx0,
+                                                                   DevCtrl* ctrl) {
   pdl_trigger();
-  __shared__ BinSmem<D> sm;
+  __shared__ uint32_t s_wq[kBinWarps][kBinWarpQ];
   const long long n = ctrl->qcount[ctrl->in];
   if (blockIdx.x * (long long)kBlock >= n) return;  // idle CTA
   timer_begin(ctrl->t_relax);
-  bins_init(sm);
   const Relaxer<D, W> rx = bind(rx0, ctrl);
+  WarpSink sink{s_wq[threadIdx.x >> 5], 0u, rx.qout, rx.nout};
   const uint32_t* __restrict__ qin = ctrl->qptr[ctrl->in];
   ThreadCounters c;
-  for (long long base; (base = bins_next_chunk(sm, ctrl, n)) >= 0;) {
-    const long long i = base + threadIdx.x;
+  for (long long base; (base = warp_next_chunk(ctrl, n)) >= 0;) {
+    const long long i = base + lane_id();
     long long lo = 0, len = 0;
     D dn = DistTraits<D>::kInf;
     if (i < n) {
@@ -328,8 +312,9 @@ __global__ void __launch_bounds__(kBlock, GLB_BIN_MINB) k_ns_relax(const long lo
         len = row[u + 1] - lo;
       }
     }
-    bins_chunk(rx, sm, lo, len, dn, mirror, ctrl, c);
+    warp_windows(rx, sink, lo, len, dn, mirror, ctrl, c);
   }
+  sink.flush();
   flush_counters(ctrl, c);
   timer_end(ctrl->t_relax);
 }
@@ -436,7 +421,7 @@ __global__ void __launch_bounds__(kBlock) k_bigbin(Relaxer<D, W> rx0, M mirror, 
       }
       D cand[K];
       const unsigned won = relax_vals<K>(rx, bq, v, w, d, valid, c, cand);
-      mirror(rx, bq, won, v, cand, c);
+      mirror(rx, won, v, cand, c);
     }
     bq_flush(bq, rx.qout, rx.nout);  // barriers: piece b is consumed, s_pc[b^1] is visible
   }

@@ -185,6 +185,7 @@ constexpr int kSmallItemsCtl = 8192;
 #endif
 constexpr long long kSmallEdgesCtl = GLB_SMALL_EDGES;  // WD: active edges one cluster iteration takes
 constexpr long long kSmallMaxWindow = 64;   // HP: thread-per-node windows the cluster walks
+constexpr long long kSmallNsMaxDeg = 1024;  // NS: split-node degree (mdt) a cluster thread walks
 constexpr unsigned kSmallListCtl = 32768;    // BS / NS / EP / HP-window worklists (no item table)
 __device__ __forceinline__ bool small_eligible(const DevCtrl* c) {
   if (!c->small_ok || c->done || c->shard_mode) return false;
@@ -192,9 +193,10 @@ __device__ __forceinline__ bool small_eligible(const DevCtrl* c) {
   if (c->qcount[c->in] > (table ? (unsigned)kSmallItemsCtl : kSmallListCtl)) return false;
   switch (c->strategy) {
     case GLB_BS:
-    case GLB_NS:
     case GLB_EP:
       return c->mode == kModeRelax;
+    case GLB_NS:  // thread-per-node in the cluster: only while split nodes are short
+      return c->mode == kModeRelax && c->mdt <= kSmallNsMaxDeg;
     case GLB_WD:
       return c->mode == kModeWD || (c->mode == kModeWDF && c->wd_total <= kSmallEdgesCtl);
     case GLB_HP:  // WD-fallback steps, and window sub-iterations of short windows

@@ -174,14 +174,31 @@ __device__ __forceinline__ void timer_end(StepTimer& t) {
   if (threadIdx.x == 0) atomicMax(&t.end, gtime());
 }
 
+// Push sinks of improved destinations.  CtaSink: the CTA queue (any thread,
+// divergent callers allowed; flushed by bq_flush at CTA barriers).
+struct CtaSink {
+  BlockQ& bq;
+  uint32_t* qout;
+  unsigned int* nout;
+  template <int K>
+  __device__ __forceinline__ void push(unsigned first, const uint32_t (&v)[K], ThreadCounters& c) {
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+      if (first >> k & 1u) {
+        bq_push(bq, qout, nout, v[k]);
+        ++c.push;
+      }
+  }
+};
+
 // Relax up to K loaded edges (bit k of `valid`: edge to v[k] of weight w[k]
 // out of a node at distance dn[k] != INF).  Returns the mask of edges whose
 // atomicMin strictly lowered dist[v[k]] to cand[k] (atomic_relax_min,
-// engine.py:120-139); the ones that also won the stamp claim were pushed to
-// the CTA queue.  All dist gathers are issued before any atomic, so a thread
-// keeps K loads in flight.
-template <int K, typename D, bool W>
-__device__ __forceinline__ unsigned relax_vals(const Relaxer<D, W>& rx, BlockQ& bq,
+// engine.py:120-139); the ones that also won the push claim go to the sink.
+// All dist gathers are issued before any atomic, so a thread keeps K loads in
+// flight.
+template <int K, typename D, bool W, class S>
+__device__ __forceinline__ unsigned relax_vals(const Relaxer<D, W>& rx, S& sink,
                                                const uint32_t (&v)[K], const uint32_t (&w)[K],
                                                const D (&dn)[K], unsigned valid, ThreadCounters& c,
                                                D (&cand)[K]) {
@@ -228,13 +245,17 @@ __device__ __forceinline__ unsigned relax_vals(const Relaxer<D, W>& rx, BlockQ& 
     for (int k = 0; k < K; ++k)
       if ((won >> k & 1u) && prev[k] != rx.gen) first |= 1u << k;
   }
-#pragma unroll
-  for (int k = 0; k < K; ++k)
-    if (first >> k & 1u) {
-      bq_push(bq, rx.qout, rx.nout, v[k]);
-      ++c.push;
-    }
+  sink.template push<K>(first, v, c);
   return won;
+}
+
+template <int K, typename D, bool W>
+__device__ __forceinline__ unsigned relax_vals(const Relaxer<D, W>& rx, BlockQ& bq,
+                                               const uint32_t (&v)[K], const uint32_t (&w)[K],
+                                               const D (&dn)[K], unsigned valid, ThreadCounters& c,
+                                               D (&cand)[K]) {
+  CtaSink sink{bq, rx.qout, rx.nout};
+  return relax_vals<K>(rx, sink, v, w, dn, valid, c, cand);
 }
 
 // Relax up to K edges e[k] (col / weight loads, then relax_vals).
