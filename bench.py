@@ -67,6 +67,9 @@ def parse():
     ap.add_argument("--edge-factor", type=int, default=16)
     ap.add_argument("--loop", default=os.environ.get("GLB_BENCH_LOOP", "graph"),
                     choices=("host", "graph"))
+    ap.add_argument("--transport", default=os.environ.get("GLB_BENCH_TRANSPORT", "peer"),
+                    choices=("peer", "torch"),
+                    help="N>1 exchange: in-library P2P over NVLink (peer) or torch.distributed")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-seconds", type=float, default=20.0,
                     help="bound of one CPU-baseline sample (full traversals below it)")
@@ -451,7 +454,7 @@ def ours_sharded(args, world, rank, local):
     g.num_edges = m_own
     sg = sharded.ShardGraph(g, bounds, rank, dev)
     gen_s = time.time() - t0
-    transport = sharded.DistTransport(torch)
+    transport = sharded.DistTransport(torch) if args.transport == "torch" else "peer"
     cfg = pkg.KernelConfig(record_timing=True, instrument=False)
     op = pkg.RelaxOp(args.algo)
 
@@ -488,10 +491,12 @@ def ours_sharded(args, world, rank, local):
     e0.record()
     iters = 0
     k_ms = 0.0
+    xinfo = None
     for _ in range(args.steps):
         _, inf = step()
         iters = inf["bsp_iterations"]
         k_ms += inf["kernel_ms"]
+        xinfo = inf.get("exchange")
     e1.record()
     torch.cuda.synchronize()
     dist.barrier()
@@ -523,8 +528,12 @@ def ours_sharded(args, world, rank, local):
             _lib.check(_lib.lib().glb_graph_create(_lib.ptr64(hrow), _lib.ptr64(hcol), _lib.ptr64(hw),
                                                    g.num_nodes, m_own, dev, ctypes.byref(h)))
             dg = pkg.DeviceCsrGraph(h.value, g.num_nodes, m_own, True, dev)
-            d2, _ = sharded.run_sharded(tag, sharded.ShardGraph(dg, bounds, rank, dev), 0, op, cfg,
-                                        transport)
+            sg2 = sharded.ShardGraph(dg, bounds, rank, dev)
+            d2, _ = sharded.run_sharded(tag, sg2, 0, op, cfg,
+                                        sharded.DistTransport(torch) if args.transport == "torch"
+                                        else "peer")
+            if sg2.peer is not None:
+                sg2.peer.close()
             dg.release_device()
             torch.cuda.synchronize()
             if i:
@@ -562,11 +571,14 @@ def ours_sharded(args, world, rank, local):
                 "workload": workload_name(args, world),
                 "strategy": tag, "nodes": g.num_nodes, "edges": int(row[-1]),
                 "parallelism": f"shard{world}", "backend": backend,
+                "transport": ("peer: P2P stores into the owners' HBM (CUDA IPC over NVLink), "
+                              "release/acquire mailboxes, one host read per iteration"
+                              if args.transport == "peer" else f"torch.distributed {backend}"),
                 "ranks_per_gpu": max(1, world // max(ndev, 1)),
                 "E_r": e_r, "N_r": n_r, "bsp_iterations": iters, "gen_s": round(gen_s, 1),
                 "l2": "inputs larger than L2; no flush"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
-            "gpu_launches": int(launches), "parity_vs_single_gpu": parity,
+            "gpu_launches": int(launches), "exchange": xinfo, "parity_vs_single_gpu": parity,
             "parity_certificate": cert,
         }
         print(json.dumps(line), flush=True)
@@ -640,6 +652,10 @@ def self_launch(args) -> int:
 
 
 if __name__ == "__main__":
+    if os.environ.get("GLB_BENCH_WATCHDOG_S"):  # debugging: dump every thread's stack, then exit
+        import faulthandler
+
+        faulthandler.dump_traceback_later(float(os.environ["GLB_BENCH_WATCHDOG_S"]), exit=True)
     a = parse()
     world = int(os.environ.get("WORLD_SIZE", "0"))
     if a.impl == "reference":

@@ -5,8 +5,10 @@
  * Every entry point is `extern "C"`, takes plain pointers and sizes, and returns
  * an int status (GLB_OK == 0).  On failure a thread-local message is available
  * from glb_last_error().  Host arrays are always the reference's int64 layout
- * (graphlb/csr.py:16-21 INDEX_DTYPE = np.int64); the library narrows them on the
- * device and owns all device memory.
+ * (graphlb/csr.py:16-21 INDEX_DTYPE = np.int64); the library's host workers
+ * narrow them to 32 bits (8 bits for small weights) on the way into pinned
+ * staging buffers, so PCIe carries the narrow layout, and the library owns all
+ * device memory.
  *
  * Reference interfaces each entry point replaces (paths under
  * /root/reference/pkg/src/graphlb/):
@@ -190,8 +192,9 @@ int glb_run_records(glb_graph* g, int64_t offset, glb_record* records,
 int glb_run_thread_work(glb_graph* g, int64_t offset, int64_t count, uint32_t* out,
                         int64_t* total);
 
-/* ---- sharded runs: 1-D vertex partition across ranks ----
- * Every rank holds the graph over the GLOBAL id space with only its own rows
+/* ---- sharded runs, host-staged exchange: 1-D vertex partition across ranks ----
+ * The portable step-by-step form of the peer run below, for transports the
+ * caller drives (torch.distributed NCCL / gloo).  Every rank holds the graph over the GLOBAL id space with only its own rows
  * (glb_graph_restrict) and runs BS / WD / HP locally; per iteration:
  *   glb_shard_local  -> run to the iteration boundary, split the improved
  *                       vertices by owner: send_buf (device, u64 entries
@@ -210,6 +213,60 @@ int glb_shard_local(glb_graph* g, int64_t* send_counts, void* send_buf,
 int glb_shard_apply(glb_graph* g, const void* recv_buf, int64_t nrecv);
 int glb_shard_advance(glb_graph* g, int64_t* frontier);
 int glb_shard_finish(glb_graph* g, int64_t* dist_owned, glb_run_stats* stats);
+
+/* ---- sharded runs over peer memory (the product path) ----
+ * The whole BSP loop of a 1-D vertex partition runs inside the library.  Each
+ * rank owns an exchange region in its HBM (per-sender inbox segments and
+ * mailbox slots, double-buffered by iteration parity); ranks write each
+ * other's regions directly with P2P stores over NVLink / NVSwitch -- regions
+ * of other processes are mapped with CUDA IPC, ranks of one process use plain
+ * device pointers.  One iteration: local relaxation to the iteration boundary
+ * (the strategy's loop graph), remote improvements scattered straight into
+ * the owners' inboxes, mailbox publish (release), wait for every peer
+ * (acquire), relaxation of the received entries, advance; one control-block
+ * read-back per iteration carries the global termination and overflow
+ * verdicts.  Distance tiers 24 -> 32 -> 64 bits as glb_run, switched on
+ * every rank at the same iteration.  Replaces the reference's host loop
+ * (node_based.py:33-80, workload.py:175-189, hierarchical.py:54-136) across
+ * ranks; strategies BS, WD and HP (others: GLB_EINVAL).
+ *
+ *   glb_peer_create   exchange region for rank `rank` of `parts` on g's device
+ *                     (g: the rank's restricted shard, glb_graph_restrict)
+ *   glb_peer_handle   GLB_PEER_HANDLE_BYTES IPC handle of the region
+ *   glb_peer_connect  map every other rank's region from the gathered handles
+ *                     (parts * GLB_PEER_HANDLE_BYTES, rank order)
+ *   glb_peer_connect_local  connect ranks living in this process
+ *   glb_peer_run      one rank's whole run (blocking; every rank calls it with
+ *                     the same params); int64 distances of the owned range
+ *   glb_peer_run_local      every rank of this process, interleaved on one
+ *                     host thread (virtual ranks on one GPU, or one process
+ *                     driving several GPUs)
+ * A peer that never publishes makes the others fail with GLB_ECUDA after
+ * GLB_PEER_TIMEOUT_S seconds (default 120) instead of hanging. */
+#define GLB_PEER_HANDLE_BYTES 64
+#define GLB_PEER_IPC 1    /* regions of other processes mapped via CUDA IPC */
+#define GLB_PEER_LOCAL 2  /* all ranks in this process */
+typedef struct glb_peer glb_peer;
+typedef struct glb_peer_stats {
+  int64_t bsp_iterations;  /* exchange rounds (== global iterations) */
+  int64_t sent_entries;    /* (dist, v) updates this rank wrote into peers' inboxes */
+  int64_t recv_entries;    /* updates it received */
+  int32_t entry_bytes;     /* 8 (<= 32-bit distances) or 16 */
+  int32_t parts;
+  int32_t rank;
+  int32_t transport;       /* GLB_PEER_IPC / GLB_PEER_LOCAL */
+  double exchange_ms;      /* device time of scatter .. advance, summed over iterations */
+  double wait_ms;          /* of which polling for peers */
+} glb_peer_stats;
+int glb_peer_create(glb_graph* g, const int64_t* bounds, int parts, int rank, glb_peer** out);
+int glb_peer_handle(glb_peer* p, void* handle_out);
+int glb_peer_connect(glb_peer* p, const void* handles);
+int glb_peer_connect_local(glb_peer* const* peers, int parts);
+int glb_peer_run(glb_peer* p, const glb_run_params* params, int64_t* dist_owned,
+                 glb_run_stats* stats, glb_peer_stats* xstats);
+int glb_peer_run_local(glb_peer* const* peers, int parts, const glb_run_params* params,
+                       int64_t* const* dist_owned, glb_run_stats* stats, glb_peer_stats* xstats);
+int glb_peer_destroy(glb_peer* p);
 
 /* ---- graph files (io.py) ---- */
 /* read_csr_bin (io.py:141-170) straight into HBM: the "CSRG" v1 cache is

@@ -64,6 +64,17 @@ class Record(ctypes.Structure):
     ]
 
 
+class PeerStats(ctypes.Structure):
+    _fields_ = [
+        ("bsp_iterations", _i64), ("sent_entries", _i64), ("recv_entries", _i64),
+        ("entry_bytes", _i32), ("parts", _i32), ("rank", _i32), ("transport", _i32),
+        ("exchange_ms", _f64), ("wait_ms", _f64),
+    ]
+
+
+GLB_PEER_HANDLE_BYTES = 64
+GLB_PEER_IPC, GLB_PEER_LOCAL = 1, 2
+
 # name -> (restype, argtypes); the exported surface of include/graphlb_b200.h
 SIGNATURES = {
     "glb_last_error": (ctypes.c_char_p, []),
@@ -89,6 +100,17 @@ SIGNATURES = {
     "glb_shard_apply": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, _i64]),
     "glb_shard_advance": (ctypes.c_int, [ctypes.c_void_p, _p64]),
     "glb_shard_finish": (ctypes.c_int, [ctypes.c_void_p, _p64, ctypes.POINTER(RunStats)]),
+    "glb_peer_create": (ctypes.c_int, [ctypes.c_void_p, _p64, ctypes.c_int, ctypes.c_int,
+                                       ctypes.POINTER(ctypes.c_void_p)]),
+    "glb_peer_handle": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p]),
+    "glb_peer_connect": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p]),
+    "glb_peer_connect_local": (ctypes.c_int, [ctypes.POINTER(ctypes.c_void_p), ctypes.c_int]),
+    "glb_peer_run": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(RunParams), _p64,
+                                    ctypes.POINTER(RunStats), ctypes.POINTER(PeerStats)]),
+    "glb_peer_run_local": (ctypes.c_int, [ctypes.POINTER(ctypes.c_void_p), ctypes.c_int,
+                                          ctypes.POINTER(RunParams), ctypes.POINTER(_p64),
+                                          ctypes.POINTER(RunStats), ctypes.POINTER(PeerStats)]),
+    "glb_peer_destroy": (ctypes.c_int, [ctypes.c_void_p]),
     "glb_graph_info": (ctypes.c_int, [ctypes.c_void_p, _p64, _p64,
                                       ctypes.POINTER(ctypes.c_int),
                                       ctypes.POINTER(ctypes.c_int)]),

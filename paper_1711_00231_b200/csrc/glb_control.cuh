@@ -429,6 +429,18 @@ __global__ void k_shard_advance(DevCtrl* c) {
     c->sub = -1;
     c->window = 0;
   }
+  ctl_check_renorm(c);  // 24-bit tier: retag before every 128th generation
+}
+
+// Re-enter the loop graph of a sharded run after the exchange (the state
+// k_shard_advance left), instead of k_control_init's fresh start.
+__global__ void k_control_resume(DevCtrl* c, cudaGraphConditionalHandle h_loop, ModeHandles h_mode,
+                                 int graph_mode) {
+  if (threadIdx.x != 0) return;
+  c->kernels += 1;
+  c->tail_done = 0;
+  c->use_small = small_eligible(c);
+  ctl_set_conditionals(c, h_loop, h_mode, graph_mode);
 }
 
 }  // namespace glb

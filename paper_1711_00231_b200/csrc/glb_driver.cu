@@ -18,6 +18,7 @@
 #include <cstring>
 #include <sstream>
 #include <unordered_map>
+#include <memory>
 #include <mutex>
 #include <vector>
 
@@ -27,6 +28,7 @@
 #include "glb_relax.cuh"
 #include "glb_scan.cuh"
 #include "glb_small.cuh"
+#include "glb_peer.cuh"
 
 namespace glb {
 
@@ -183,6 +185,7 @@ class Runner {
   double setup_ms_ = 0;
   long long seed_count_ = 0;
   bool shard_mode_ = false;
+  bool resume_graph_ = false;  // the loop graph starts with k_control_resume
   // host-loop per-record event timing
   struct EvPair {
     cudaEvent_t k0, k1, o0, o1;
@@ -545,7 +548,7 @@ class Runner {
       << (const void*)ctrl_ << '|' << (const void*)items_[0] << '|' << (const void*)items_[1] << '|'
       << (const void*)tile_first_[0] << '|' << (const void*)tile_first_[1] << '|'
       << (const void*)lb_.flags << '|' << (const void*)lb_.aggs << '|' << g_->n << '|' << n_all_
-      << '|' << mdt_;
+      << '|' << mdt_ << '|' << resume_graph_;
     return k.str();
   }
 
@@ -578,7 +581,10 @@ class Runner {
       for (int u = 0; u < unroll; ++u)
         GLB_CUDA_TRY(cudaGraphConditionalHandleCreate(&h_mode.h[u], graph, 0, 0));
       capture_into(graph, nullptr, 0);
-      k_control_init<<<1, 32, 0, s_>>>(ctrl_, h_loop, h_mode, 1);
+      if (resume_graph_)  // sharded run: re-enter after the exchange
+        k_control_resume<<<1, 32, 0, s_>>>(ctrl_, h_loop, h_mode, 1);
+      else
+        k_control_init<<<1, 32, 0, s_>>>(ctrl_, h_loop, h_mode, 1);
       GLB_CHECK_LAUNCH();
       end_capture();
       cudaGraphNode_t init = only_node(graph);
@@ -663,7 +669,8 @@ class Runner {
   // into them (device, strategy, widths, grids and every buffer pointer).
   // With the caching allocator a new graph of the same shape usually gets the
   // same buffers back, so create -> run -> destroy cycles reuse the exec.
-  void loop_graph() {
+  void loop_graph() { GLB_CUDA_TRY(cudaGraphLaunch(graph_exec(), s_)); }
+  cudaGraphExec_t graph_exec() {
     const std::string key = graph_key();
     cudaGraphExec_t exec = nullptr;
     {
@@ -676,7 +683,7 @@ class Runner {
       std::lock_guard<std::mutex> lk(exec_cache_mu());
       exec_cache().emplace(key, exec);
     }
-    GLB_CUDA_TRY(cudaGraphLaunch(exec, s_));
+    return exec;
   }
   static std::mutex& exec_cache_mu() {
     static std::mutex* m = new std::mutex();
@@ -916,6 +923,190 @@ class ShardSession : public ShardSessionBase, public Runner<uint32_t, W> {
   unsigned long long* counts_ = nullptr;
   uint32_t* tmp_ = nullptr;
 };
+
+// ===================================================== peer-memory run ===
+// The whole sharded BSP loop inside the library (glb_peer_run): local
+// relaxation to the iteration boundary as the loop graph (one launch), then
+// the peer exchange of glb_peer.cuh, then one control-block read-back that
+// carries the global termination and overflow verdicts -- the only host
+// synchronisation of an iteration.
+class PeerRunBase {
+ public:
+  virtual ~PeerRunBase() {}
+  virtual void issue(unsigned long long seq) = 0;
+  virtual int complete() = 0;  // 0 continue, 1 globally done, 2 global overflow
+  virtual void finish(int64_t* dist_owned, glb_run_stats* st, glb_peer_stats* xs) = 0;
+};
+
+__global__ void k_peer_begin(PeerTable* t, uint32_t* tmp) {
+  if (threadIdx.x != 0) return;
+  t->tmp = tmp;
+  for (int o = 0; o < kPeerMaxParts; ++o) t->cursor[o] = 0;
+  t->my_work = t->sent = t->recv = t->wait_ns = 0;
+}
+
+__global__ void k_peer_reset_cursors(PeerTable* t) {
+  if (threadIdx.x < kPeerMaxParts) t->cursor[threadIdx.x] = 0;
+}
+
+template <typename D, bool W>
+class PeerRun : public PeerRunBase, public Runner<D, W> {
+  using R = Runner<D, W>;
+
+ public:
+  PeerRun(glb_peer* pr, const glb_run_params& p, std::vector<glb_record>& recs)
+      : R(pr->g, params_, recs), params_(p), pr_(pr) {
+    params_.loop_mode = GLB_LOOP_GRAPH;
+    this->shard_mode_ = true;
+    this->resume_graph_ = true;
+    // The control step runs as its own kernel here, not as the last-CTA tail
+    // of each step: with several processes time-sliced on one GPU (ranks
+    // sharing a device) the fused tail was observed to stall the WD loop
+    // graph (tools/peer_mp_probe.py: hangs with the tail, completes with
+    // GLB_NO_FUSED_CTL), and the extra ~3 us per step is small next to the
+    // exchange.
+    this->fused_ctl_ = false;
+    std::memset(&stats_, 0, sizeof(stats_));
+    stats_.split_fraction = -1.0;
+    lo_ = pr->bounds[pr->rank];
+    hi_ = pr->bounds[pr->rank + 1];
+    R::prepare(&stats_);
+    cudaStream_t s = this->s_;
+    if (p.source < lo_ || p.source >= hi_)  // not ours: start with an empty frontier
+      GLB_CUDA_TRY(cudaMemsetAsync(&this->ctrl_->qcount[0], 0, 4, s));
+    k_control_init<<<1, 32, 0, s>>>(this->ctrl_, 0, ModeHandles{}, 0);
+    GLB_CHECK_LAUNCH();
+    uint32_t* tmp = (uint32_t*)ensure(this->g_->ws.shard_tmp,
+                                      (size_t)std::max<long long>(this->g_->n, 1) * 4);
+    k_peer_begin<<<1, 32, 0, s>>>(pr->table, tmp);
+    GLB_CHECK_LAUNCH();
+    GLB_CUDA_TRY(cudaEventCreate(&ev_[0]));
+    GLB_CUDA_TRY(cudaEventCreate(&ev_[1]));
+    grid_ = (unsigned)this->g_->num_sms * 4;
+    // Build, instantiate and upload the loop graph now, before any rank's
+    // mailbox poll occupies the device: ranks sharing a GPU must never need
+    // a module load or a graph upload while a peer's k_peer_wait spins.
+    exec_ = R::graph_exec();
+    GLB_CUDA_TRY(cudaGraphUpload(exec_, s));
+    GLB_CUDA_TRY(cudaStreamSynchronize(s));
+  }
+  ~PeerRun() override {
+    for (cudaEvent_t e : ev_)
+      if (e) cudaEventDestroy(e);
+  }
+
+  void issue(unsigned long long seq) override {
+    const int parity = (int)(seq & 1ull);
+    cudaStream_t s = this->s_;
+    GLB_CUDA_TRY(cudaGraphLaunch(exec_, s));  // local relaxation, paused at the iteration boundary
+    GLB_CHECK_LAUNCH();
+    GLB_CUDA_TRY(cudaEventRecord(ev_[0], s));
+    PeerTable* t = pr_->table;
+    k_peer_scatter<D><<<grid_, kBlock, 0, s>>>(this->ctrl_, t, this->cells_, parity);
+    GLB_CHECK_LAUNCH();
+    k_peer_publish<<<1, 64, 0, s>>>(this->ctrl_, t, seq, parity);
+    GLB_CHECK_LAUNCH();
+    k_peer_wait<<<1, 32, 0, s>>>(this->ctrl_, t, seq, parity);
+    GLB_CHECK_LAUNCH();
+    k_peer_reset_cursors<<<1, kPeerMaxParts, 0, s>>>(t);
+    GLB_CHECK_LAUNCH();
+    k_peer_apply<D><<<grid_, kBlock, 0, s>>>(this->ctrl_, t, this->cells_, this->stamp_, parity);
+    GLB_CHECK_LAUNCH();
+    k_shard_advance<<<1, 32, 0, s>>>(this->ctrl_);
+    GLB_CHECK_LAUNCH();
+    GLB_CUDA_TRY(cudaEventRecord(ev_[1], s));
+    GLB_CUDA_TRY(cudaMemcpyAsync(&this->h_->ctrl, this->ctrl_, sizeof(DevCtrl),
+                                 cudaMemcpyDeviceToHost, s));
+  }
+
+  int complete() override {
+    GLB_CUDA_TRY(cudaStreamSynchronize(this->s_));
+    const DevCtrl& hc = this->h_->ctrl;
+    if ((hc.bad_input & 0xFFFF0000u) == kPeerTimeoutFlag) {
+      pr_->poisoned = true;
+      throw Error{GLB_ECUDA, "peer exchange: rank " + std::to_string(hc.bad_input & 0xFFFFu) +
+                                 " did not publish iteration " + std::to_string(bsp_ + 1) +
+                                 " within the timeout (GLB_PEER_TIMEOUT_S)"};
+    }
+    float ms = 0;
+    if (cudaEventElapsedTime(&ms, ev_[0], ev_[1]) == cudaSuccess) xms_ += ms;
+    cudaGetLastError();
+    ++bsp_;
+    if (hc.overflow) return 2;
+    return hc.aux[1] == 0 ? 1 : 0;
+  }
+
+  void finish(int64_t* dist_owned, glb_run_stats* st, glb_peer_stats* xs) override {
+    R::finish_run(dist_owned, &stats_, lo_, hi_);
+    *st = stats_;
+    if (xs) {
+      PeerTable ht;
+      GLB_CUDA_TRY(cudaMemcpy(&ht, pr_->table, sizeof(PeerTable), cudaMemcpyDeviceToHost));
+      std::memset(xs, 0, sizeof(*xs));
+      xs->bsp_iterations = bsp_;
+      xs->sent_entries = (int64_t)ht.sent;
+      xs->recv_entries = (int64_t)ht.recv;
+      xs->entry_bytes = (int32_t)PeerEntry<D>::kBytes;
+      xs->parts = pr_->parts;
+      xs->rank = pr_->rank;
+      xs->transport = pr_->transport;
+      xs->exchange_ms = xms_;
+      xs->wait_ms = (double)ht.wait_ns * 1e-6;
+    }
+  }
+
+ private:
+  glb_run_params params_;
+  glb_peer* pr_;
+  glb_run_stats stats_;
+  long long lo_ = 0, hi_ = 0;
+  cudaEvent_t ev_[2] = {nullptr, nullptr};
+  cudaGraphExec_t exec_ = nullptr;  // cached process-wide (Runner::graph_exec)
+  unsigned grid_ = 148;
+  long long bsp_ = 0;
+  double xms_ = 0;
+};
+
+}  // namespace
+
+// Load every exchange kernel into the context up front (lazy module loading
+// would otherwise load them at first launch -- possibly while another rank's
+// mailbox poll is spinning on the same GPU).
+void preload_peer_kernels() {
+  static std::mutex mu;
+  static std::vector<int> done;
+  int dev = -1;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  if (std::find(done.begin(), done.end(), dev) != done.end()) return;
+  done.push_back(dev);
+  {
+    cudaFuncAttributes a;
+    const void* ks[] = {
+        (const void*)k_peer_scatter<dist24_t>, (const void*)k_peer_scatter<uint32_t>,
+        (const void*)k_peer_scatter<unsigned long long>, (const void*)k_peer_apply<dist24_t>,
+        (const void*)k_peer_apply<uint32_t>, (const void*)k_peer_apply<unsigned long long>,
+        (const void*)k_peer_publish, (const void*)k_peer_wait, (const void*)k_peer_begin,
+        (const void*)k_peer_reset_cursors, (const void*)k_shard_advance,
+        (const void*)k_control_init, (const void*)k_control_resume};
+    for (const void* k : ks) cudaFuncGetAttributes(&a, k);
+    cudaGetLastError();
+  }
+}
+
+namespace {
+std::unique_ptr<PeerRunBase> make_peer_run(int bits, glb_peer* pr, const glb_run_params& p,
+                                           std::vector<glb_record>& recs) {
+  const bool w = p.algo == GLB_SSSP && pr->g->wt != nullptr;
+  if (bits == 24)
+    return w ? std::unique_ptr<PeerRunBase>(new PeerRun<dist24_t, true>(pr, p, recs))
+             : std::unique_ptr<PeerRunBase>(new PeerRun<dist24_t, false>(pr, p, recs));
+  if (bits == 32)
+    return w ? std::unique_ptr<PeerRunBase>(new PeerRun<uint32_t, true>(pr, p, recs))
+             : std::unique_ptr<PeerRunBase>(new PeerRun<uint32_t, false>(pr, p, recs));
+  return w ? std::unique_ptr<PeerRunBase>(new PeerRun<unsigned long long, true>(pr, p, recs))
+           : std::unique_ptr<PeerRunBase>(new PeerRun<unsigned long long, false>(pr, p, recs));
+}
 
 template <typename D>
 void run_typed(glb_graph* g, const glb_run_params& p, int64_t* dist_out, glb_run_stats* st,
@@ -1206,5 +1397,281 @@ extern "C" int glb_shard_finish(glb_graph* g, int64_t* dist_owned, glb_run_stats
     if (stats) *stats = st;
     delete g->shard;
     g->shard = nullptr;
+  });
+}
+
+// ============================================================= peer C-ABI ===
+namespace {
+template <typename F>
+int peer_guard(F&& f) {
+  try {
+    f();
+    return GLB_OK;
+  } catch (const glb::Error& e) {
+    glb::set_error(e.msg);
+    return e.code;
+  } catch (const std::exception& e) {
+    glb::set_error(e.what());
+    return GLB_ECUDA;
+  }
+}
+
+struct DeviceScope {  // make `dev` current, restore the caller's device
+  int prev = -1;
+  explicit DeviceScope(int dev) {
+    cudaGetDevice(&prev);
+    GLB_CUDA_TRY(cudaSetDevice(dev));
+  }
+  ~DeviceScope() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+unsigned long long peer_timeout_ns() {
+  const char* e = getenv("GLB_PEER_TIMEOUT_S");
+  const double s = e ? atof(e) : 120.0;
+  return (unsigned long long)((s > 0 ? s : 120.0) * 1e9);
+}
+
+void peer_write_table(glb_peer* p) {
+  glb::PeerTable ht;
+  std::memset(&ht, 0, sizeof(ht));
+  for (int r = 0; r < p->parts; ++r) {
+    ht.base[r] = p->base[r];
+    ht.seg[r] = p->bounds[r + 1] - p->bounds[r];
+  }
+  for (int r = 0; r <= p->parts; ++r) ht.bounds[r] = p->bounds[r];
+  ht.parts = p->parts;
+  ht.me = p->rank;
+  ht.timeout_ns = peer_timeout_ns();
+  GLB_CUDA_TRY(cudaMemcpy(p->table, &ht, sizeof(ht), cudaMemcpyHostToDevice));
+}
+
+void peer_check_params(glb_peer* p, const glb_run_params* q) {
+  if (!p || !q) throw glb::Error{GLB_EINVAL, "peer/params is NULL"};
+  if (!p->connected) throw glb::Error{GLB_EINVAL, "peer is not connected"};
+  if (p->poisoned)
+    throw glb::Error{GLB_ECUDA, "peer exchange lost lockstep (an earlier run timed out); recreate it"};
+  if (q->strategy != GLB_BS && q->strategy != GLB_WD && q->strategy != GLB_HP)
+    throw glb::Error{GLB_EINVAL, "sharded runs support the BS, WD and HP strategies"};
+  if (q->algo != GLB_BFS && q->algo != GLB_SSSP) throw glb::Error{GLB_EINVAL, "unknown algo"};
+  if (q->source < 0 || q->source >= p->g->n) throw glb::Error{GLB_EINVAL, "source out of range"};
+  if (q->block_size < 1) throw glb::Error{GLB_EINVAL, "block_size must be >= 1"};
+  if (q->dist_bits != 0 && q->dist_bits != 24 && q->dist_bits != 32 && q->dist_bits != 64)
+    throw glb::Error{GLB_EINVAL, "dist_bits must be 0, 24, 32 or 64"};
+}
+
+// Run every rank in `ps` (one host thread): each iteration is issued on all
+// ranks before any is waited for, so ranks sharing a GPU cannot deadlock.
+// All ranks see the same global verdict after every iteration, so a tier
+// change (overflow) happens on all of them at once.
+void peer_run_all(glb_peer* const* ps, int n, const glb_run_params& q, int64_t* const* dist,
+                  glb_run_stats* st, glb_peer_stats* xs) {
+  glb_peer* p0 = ps[0];
+  const bool sssp = q.algo == GLB_SSSP;
+  const bool huge = p0->g->n * 8LL > 2LL * p0->g->l2_bytes;
+  const int first = q.dist_bits ? q.dist_bits : (!p0->narrow_overflow[sssp] && huge ? 24 : 32);
+  for (int bits = first;; bits = bits == 24 ? 32 : 64) {
+    std::vector<std::vector<glb_record>> recs(n);
+    std::vector<std::unique_ptr<glb::PeerRunBase>> runs(n);
+    int verdict = 0;
+    try {
+      for (int r = 0; r < n; ++r) {
+        DeviceScope ds(ps[r]->g->device);
+        runs[r] = glb::make_peer_run(bits, ps[r], q, recs[r]);
+      }
+      while (verdict == 0) {
+        for (int r = 0; r < n; ++r) {
+          DeviceScope ds(ps[r]->g->device);
+          runs[r]->issue(++ps[r]->seq);
+        }
+        int v0 = -1;
+        for (int r = 0; r < n; ++r) {
+          DeviceScope ds(ps[r]->g->device);
+          const int v = runs[r]->complete();
+          if (v0 >= 0 && v != v0) {
+            for (int k = 0; k < n; ++k) ps[k]->poisoned = true;
+            throw glb::Error{GLB_ECUDA, "peer exchange: ranks disagree on the global verdict"};
+          }
+          v0 = v;
+        }
+        verdict = v0;
+      }
+      if (verdict == 1) {
+        for (int r = 0; r < n; ++r) {
+          DeviceScope ds(ps[r]->g->device);
+          runs[r]->finish(dist ? dist[r] : nullptr, &st[r], xs ? &xs[r] : nullptr);
+          st[r].n_records = (int64_t)recs[r].size();
+          ps[r]->g->last_records.swap(recs[r]);
+        }
+        return;
+      }
+    } catch (...) {
+      runs.clear();
+      for (int r = 0; r < n; ++r) {
+        DeviceScope ds(ps[r]->g->device);
+        glb::reset_epochs_public(ps[r]->g);
+      }
+      throw;
+    }
+    runs.clear();  // verdict 2: distance overflow somewhere -> next tier everywhere
+    for (int r = 0; r < n; ++r) {
+      DeviceScope ds(ps[r]->g->device);
+      glb::reset_epochs_public(ps[r]->g);
+    }
+    if (bits == 64) throw glb::Error{GLB_EOVERFLOW, "distance exceeds the 63-bit range"};
+    if (q.dist_bits)
+      throw glb::Error{GLB_EOVERFLOW, "distance exceeds the " + std::to_string(bits) + "-bit range"};
+    if (bits == 24)
+      for (int r = 0; r < n; ++r) ps[r]->narrow_overflow[sssp] = true;
+  }
+}
+}  // namespace
+
+extern "C" int glb_peer_create(glb_graph* g, const int64_t* bounds, int parts, int rank,
+                               glb_peer** out) {
+  return peer_guard([&] {
+    if (!g || !bounds || !out) throw glb::Error{GLB_EINVAL, "graph/bounds/out is NULL"};
+    if (parts < 1 || parts > glb::kPeerMaxParts || rank < 0 || rank >= parts)
+      throw glb::Error{GLB_EINVAL, "parts must be in [1, 64] and 0 <= rank < parts"};
+    if (bounds[0] != 0 || bounds[parts] != g->n)
+      throw glb::Error{GLB_EINVAL, "bounds must start at 0 and end at num_nodes"};
+    for (int i = 0; i < parts; ++i)
+      if (bounds[i + 1] < bounds[i]) throw glb::Error{GLB_EINVAL, "bounds must be nondecreasing"};
+    DeviceScope ds(g->device);
+    std::unique_ptr<glb_peer> p(new glb_peer());
+    p->g = g;
+    p->parts = parts;
+    p->rank = rank;
+    for (int i = 0; i <= parts; ++i) p->bounds[i] = bounds[i];
+    const long long seg = std::max<long long>(bounds[rank + 1] - bounds[rank], 1);
+    p->region_bytes = glb::kPeerHdrBytes + 2 * (size_t)parts * (size_t)seg * glb::kPeerEntryMax;
+    GLB_CUDA_TRY(cudaMalloc((void**)&p->region, p->region_bytes));
+    GLB_CUDA_TRY(cudaMemset(p->region, 0, glb::kPeerHdrBytes));
+    cudaError_t e = cudaMalloc((void**)&p->table, sizeof(glb::PeerTable));
+    if (e != cudaSuccess) {
+      cudaFree(p->region);
+      GLB_CUDA_TRY(e);
+    }
+    p->base[rank] = p->region;
+    glb::preload_peer_kernels();
+    *out = p.release();
+  });
+}
+
+extern "C" int glb_peer_handle(glb_peer* p, void* handle_out) {
+  return peer_guard([&] {
+    if (!p || !handle_out) throw glb::Error{GLB_EINVAL, "peer/handle is NULL"};
+    static_assert(sizeof(cudaIpcMemHandle_t) == GLB_PEER_HANDLE_BYTES, "IPC handle size");
+    DeviceScope ds(p->g->device);
+    cudaIpcMemHandle_t h;
+    GLB_CUDA_TRY(cudaIpcGetMemHandle(&h, p->region));
+    std::memcpy(handle_out, &h, sizeof(h));
+  });
+}
+
+extern "C" int glb_peer_connect(glb_peer* p, const void* handles) {
+  return peer_guard([&] {
+    if (!p || !handles) throw glb::Error{GLB_EINVAL, "peer/handles is NULL"};
+    if (p->connected) throw glb::Error{GLB_EINVAL, "peer is already connected"};
+    DeviceScope ds(p->g->device);
+    const char* hb = (const char*)handles;
+    for (int r = 0; r < p->parts; ++r) {
+      if (r == p->rank) continue;
+      cudaIpcMemHandle_t h;
+      std::memcpy(&h, hb + (size_t)r * GLB_PEER_HANDLE_BYTES, sizeof(h));
+      void* ptr = nullptr;
+      const cudaError_t e = cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess);
+      if (e != cudaSuccess) {
+        for (int k = 0; k < r; ++k)
+          if (p->ipc_opened[k]) {
+            cudaIpcCloseMemHandle(p->base[k]);
+            p->ipc_opened[k] = false;
+            p->base[k] = nullptr;
+          }
+        throw glb::Error{GLB_ECUDA, "cudaIpcOpenMemHandle(rank " + std::to_string(r) +
+                                        "): " + cudaGetErrorString(e)};
+      }
+      p->base[r] = (char*)ptr;
+      p->ipc_opened[r] = true;
+    }
+    peer_write_table(p);
+    p->transport = GLB_PEER_IPC;
+    p->connected = true;
+  });
+}
+
+extern "C" int glb_peer_connect_local(glb_peer* const* peers, int parts) {
+  return peer_guard([&] {
+    if (!peers || parts < 1) throw glb::Error{GLB_EINVAL, "peers is NULL"};
+    for (int r = 0; r < parts; ++r) {
+      if (!peers[r]) throw glb::Error{GLB_EINVAL, "NULL peer"};
+      if (peers[r]->parts != parts || peers[r]->rank != r)
+        throw glb::Error{GLB_EINVAL, "peers must be ranks 0..parts-1 of one partition"};
+      if (peers[r]->connected) throw glb::Error{GLB_EINVAL, "peer is already connected"};
+      for (int i = 0; i <= parts; ++i)
+        if (peers[r]->bounds[i] != peers[0]->bounds[i])
+          throw glb::Error{GLB_EINVAL, "peers were created with different bounds"};
+    }
+    for (int r = 0; r < parts; ++r) {
+      glb_peer* p = peers[r];
+      DeviceScope ds(p->g->device);
+      for (int k = 0; k < parts; ++k) {
+        p->base[k] = peers[k]->region;
+        const int dk = peers[k]->g->device;
+        if (dk != p->g->device) {  // direct loads/stores into the other GPU's HBM
+          const cudaError_t e = cudaDeviceEnablePeerAccess(dk, 0);
+          if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) GLB_CUDA_TRY(e);
+          cudaGetLastError();
+        }
+      }
+      peer_write_table(p);
+      p->transport = GLB_PEER_LOCAL;
+      p->connected = true;
+    }
+  });
+}
+
+extern "C" int glb_peer_run(glb_peer* p, const glb_run_params* params, int64_t* dist_owned,
+                            glb_run_stats* stats, glb_peer_stats* xstats) {
+  return peer_guard([&] {
+    peer_check_params(p, params);
+    if (!stats) throw glb::Error{GLB_EINVAL, "stats is NULL"};
+    std::lock_guard<std::mutex> lk(p->g->mu);
+    glb_peer* ps[1] = {p};
+    int64_t* ds[1] = {dist_owned};
+    peer_run_all(ps, 1, *params, ds, stats, xstats);
+  });
+}
+
+extern "C" int glb_peer_run_local(glb_peer* const* peers, int parts, const glb_run_params* params,
+                                  int64_t* const* dist_owned, glb_run_stats* stats,
+                                  glb_peer_stats* xstats) {
+  return peer_guard([&] {
+    if (!peers || parts < 1 || !stats) throw glb::Error{GLB_EINVAL, "peers/stats is NULL"};
+    std::vector<std::unique_lock<std::mutex>> locks;
+    for (int r = 0; r < parts; ++r) {
+      peer_check_params(peers[r], params);
+      if (peers[r]->parts != parts || peers[r]->rank != r || peers[r]->transport != GLB_PEER_LOCAL)
+        throw glb::Error{GLB_EINVAL, "glb_peer_run_local needs all ranks of a local connection"};
+      for (int k = 0; k < r; ++k)
+        if (peers[k]->g == peers[r]->g) throw glb::Error{GLB_EINVAL, "ranks share a graph handle"};
+      locks.emplace_back(peers[r]->g->mu);
+    }
+    peer_run_all(peers, parts, *params, dist_owned, stats, xstats);
+  });
+}
+
+extern "C" int glb_peer_destroy(glb_peer* p) {
+  return peer_guard([&] {
+    if (!p) return;
+    DeviceScope ds(p->g->device);
+    cudaStreamSynchronize(p->g->stream);
+    for (int r = 0; r < p->parts; ++r)
+      if (p->ipc_opened[r]) cudaIpcCloseMemHandle(p->base[r]);
+    cudaFree(p->table);
+    cudaFree(p->region);
+    cudaGetLastError();
+    delete p;
   });
 }

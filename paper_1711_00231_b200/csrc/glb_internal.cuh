@@ -299,6 +299,29 @@ struct ShardSessionBase {
 };
 }  // namespace glb
 
+namespace glb {
+struct PeerTable;
+}
+
+// One rank of a peer-memory sharded run (glb_peer_* C-ABI, glb_driver.cu):
+// the exchange region in this rank's HBM and every peer's region as mapped
+// in this process.
+struct glb_peer {
+  glb_graph* g = nullptr;        // this rank's shard (not owned)
+  int parts = 0, rank = 0;
+  long long bounds[65] = {};
+  char* region = nullptr;        // own exchange region (cudaMalloc: IPC-exportable)
+  size_t region_bytes = 0;
+  char* base[64] = {};           // every rank's region in this process's address space
+  bool ipc_opened[64] = {};      // base[r] came from cudaIpcOpenMemHandle
+  glb::PeerTable* table = nullptr;  // device table of the exchange kernels
+  unsigned long long seq = 0;    // iterations exchanged so far (lockstep on every rank)
+  int transport = 0;             // GLB_PEER_IPC / GLB_PEER_LOCAL once connected
+  bool connected = false;
+  bool poisoned = false;         // a timed-out exchange: the ranks are out of lockstep
+  bool narrow_overflow[2] = {false, false};
+};
+
 struct glb_graph {
   int device = 0;
   int64_t n = 0, m = 0;

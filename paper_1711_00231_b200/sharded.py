@@ -3,7 +3,22 @@
 Each rank owns a contiguous, edge-balanced vertex range [lo, hi) and holds the
 graph over the GLOBAL id space with only its own rows (``glb_graph_restrict``),
 so the single-GPU strategy kernels (BS, WD, HP) run unchanged on the owned
-frontier.  Per iteration (bulk-synchronous, as the reference's host loop):
+frontier.
+
+Two transports run the same bulk-synchronous iteration:
+
+* ``"peer"`` (default, the product path): the whole loop runs inside the
+  library (``glb_peer_run``).  Ranks write remote improvements straight into
+  each other's HBM over NVLink / NVSwitch (CUDA IPC between processes, plain
+  device pointers between ranks of one process), synchronise through
+  release/acquire mailboxes in that memory, and the host reads one control
+  block per iteration.  ``PeerExchange`` sets it up (IPC handles gathered
+  with torch.distributed).
+* ``"torch"``: the step-by-step ``glb_shard_*`` protocol below, exchanged
+  with torch.distributed collectives (NCCL between GPUs, gloo staged through
+  the host); kept as the portable form and for CPU tests of the protocol.
+
+Per iteration of the ``"torch"`` form:
 
 1. ``local``   -- the rank relaxes its frontier to the iteration boundary;
                   candidates for remote vertices are min-combined on the
@@ -46,6 +61,7 @@ class ShardGraph:
     bounds: np.ndarray  # int64[parts + 1], edge-balanced vertex ranges
     rank: int
     device: int
+    peer: "PeerExchange | None" = None  # connected peer transport (cached by run_sharded)
 
     @property
     def parts(self) -> int:
@@ -183,6 +199,119 @@ class CudaShard:
         return out, {f: getattr(st, f) for f, _ in _lib.RunStats._fields_}
 
 
+# -------------------------------------------------------- peer transport
+class PeerExchange:
+    """One rank's exchange region (glb_peer_*), connected to its peers."""
+
+    def __init__(self, sg: ShardGraph):
+        self.sg = sg
+        h = ctypes.c_void_p()
+        _lib.check(_lib.lib().glb_peer_create(sg.graph.device_graph(), _lib.ptr64(sg.bounds),
+                                              sg.parts, sg.rank, ctypes.byref(h)),
+                   "glb_peer_create")
+        self.h = h.value
+
+    def handle(self) -> bytes:
+        buf = ctypes.create_string_buffer(_lib.GLB_PEER_HANDLE_BYTES)
+        _lib.check(_lib.lib().glb_peer_handle(self.h, buf), "glb_peer_handle")
+        return buf.raw
+
+    def connect(self, handles: list[bytes]) -> None:
+        """Map every other rank's region (handles in rank order)."""
+        if len(handles) != self.sg.parts:
+            raise ValueError("one handle per rank")
+        blob = b"".join(handles)
+        _lib.check(_lib.lib().glb_peer_connect(self.h, blob), "glb_peer_connect")
+
+    @staticmethod
+    def connect_local(peers: list["PeerExchange"]) -> None:
+        arr = (ctypes.c_void_p * len(peers))(*[p.h for p in peers])
+        _lib.check(_lib.lib().glb_peer_connect_local(arr, len(peers)), "glb_peer_connect_local")
+
+    @classmethod
+    def over(cls, sg: ShardGraph, group=None) -> "PeerExchange":
+        """Create this rank's region and connect it to every rank of the
+        torch.distributed group (IPC handles all-gathered)."""
+        import torch.distributed as dist
+
+        px = cls(sg)
+        handles: list = [None] * sg.parts
+        dist.all_gather_object(handles, px.handle(), group=group)
+        px.connect(handles)
+        dist.barrier(group=group)
+        return px
+
+    def run(self, tag: str, source: int, op: RelaxOp, cfg: KernelConfig | None = None):
+        """This rank's part of a sharded run: int64 distances of [lo, hi) and
+        stats (run stats + exchange stats under ``"exchange"``)."""
+        cfg = cfg or KernelConfig()
+        p = _shard_params(tag, source, op, cfg)
+        out = np.empty(self.sg.hi - self.sg.lo, dtype=np.int64)
+        st = _lib.RunStats()
+        xs = _lib.PeerStats()
+        _lib.check(_lib.lib().glb_peer_run(self.h, ctypes.byref(p), _lib.ptr64(out),
+                                           ctypes.byref(st), ctypes.byref(xs)), "glb_peer_run")
+        return out, _stats(st, xs)
+
+    def close(self) -> None:
+        if self.h:
+            _lib.lib().glb_peer_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _shard_params(tag: str, source: int, op: RelaxOp, cfg: KernelConfig):
+    if tag.upper() not in SHARD_TAGS:
+        raise ValueError(f"sharded runs support {SHARD_TAGS}, not {tag!r}")
+    p = _lib.RunParams()
+    p.strategy = _ID_OF[tag.upper()]
+    p.algo = _lib.GLB_BFS if op.kind == "bfs" else _lib.GLB_SSSP
+    p.source = source
+    p.bins = 10
+    p.chunked = 1
+    p.max_cells = 1 << 62
+    p.block_size = cfg.block_size
+    p.hp_fallback = 1
+    p.dist_bits = cfg.dist_bits
+    p.loop_mode = _lib.GLB_LOOP_GRAPH
+    p.record_timing = 1 if cfg.record_timing else 0
+    return p
+
+
+def _stats(st, xs=None) -> dict:
+    d = {f: getattr(st, f) for f, _ in _lib.RunStats._fields_}
+    if xs is not None:
+        d["exchange"] = {f: getattr(xs, f) for f, _ in _lib.PeerStats._fields_}
+        d["bsp_iterations"] = xs.bsp_iterations
+    return d
+
+
+def run_virtual_peer(tag: str, shards: list[ShardGraph], source: int, op: RelaxOp,
+                     cfg: KernelConfig | None = None, peers: list[PeerExchange] | None = None):
+    """Every rank in this process over the peer transport (glb_peer_run_local):
+    virtual ranks sharing one GPU, or one process driving several GPUs.
+    Returns the full int64 distance array and the per-rank stats."""
+    cfg = cfg or KernelConfig()
+    if peers is None:
+        peers = [PeerExchange(sg) for sg in shards]
+        PeerExchange.connect_local(peers)
+    parts = len(shards)
+    p = _shard_params(tag, source, op, cfg)
+    outs = [np.empty(sg.hi - sg.lo, dtype=np.int64) for sg in shards]
+    arr = (ctypes.c_void_p * parts)(*[px.h for px in peers])
+    dptr = (_lib._p64 * parts)(*[_lib.ptr64(o) for o in outs])
+    st = (_lib.RunStats * parts)()
+    xs = (_lib.PeerStats * parts)()
+    _lib.check(_lib.lib().glb_peer_run_local(arr, parts, ctypes.byref(p), dptr, st, xs),
+               "glb_peer_run_local")
+    return np.concatenate(outs), [_stats(st[r], xs[r]) for r in range(parts)]
+
+
 # --------------------------------------------------------------- transports
 class DistTransport:
     """All-to-all of the owner buckets + all-reduce of frontiers through
@@ -246,13 +375,24 @@ def bsp_loop(shard, transport, device, max_iterations: int | None = None) -> int
 
 
 def run_sharded(tag: str, sg: ShardGraph, source: int, op: RelaxOp,
-                cfg: KernelConfig | None = None, transport=None):
+                cfg: KernelConfig | None = None, transport=None, group=None):
     """This rank's part of a sharded run (one process per GPU).  Returns the
-    int64 distances of the owned range [sg.lo, sg.hi) and device stats."""
+    int64 distances of the owned range [sg.lo, sg.hi) and device stats.
+
+    transport: ``"peer"`` (default; a PeerExchange is created once per shard
+    and cached on it), a connected ``PeerExchange``, ``"torch"`` or a
+    DistTransport-like object for the step-by-step protocol."""
     import torch
 
     cfg = cfg or KernelConfig()
-    transport = transport or DistTransport(torch)
+    if transport is None or transport == "peer" or isinstance(transport, PeerExchange):
+        px = transport if isinstance(transport, PeerExchange) else getattr(sg, "peer", None)
+        if px is None:
+            px = PeerExchange.over(sg, group)
+            sg.peer = px
+        return px.run(tag, source, op, cfg)
+    if transport == "torch":
+        transport = DistTransport(torch, group)
     shard = CudaShard(sg, tag, source, op, cfg, torch)
     it = bsp_loop(shard, transport, shard.dev)
     dist, info = shard.finish()
@@ -261,9 +401,14 @@ def run_sharded(tag: str, sg: ShardGraph, source: int, op: RelaxOp,
 
 
 def run_virtual(tag: str, shards: list[ShardGraph], source: int, op: RelaxOp,
-                cfg: KernelConfig | None = None):
-    """All ranks in one process (e.g. several virtual ranks on one GPU): the
-    exchange is device-side slicing.  Returns the full int64 distance array."""
+                cfg: KernelConfig | None = None, transport: str = "peer"):
+    """All ranks in one process (e.g. several virtual ranks on one GPU).
+    Returns the full int64 distance array and the BSP iteration count.
+    ``"peer"``: glb_peer_run_local; ``"torch"``: the step-by-step protocol
+    with device-side slicing as the exchange."""
+    if transport == "peer":
+        d, stats = run_virtual_peer(tag, shards, source, op, cfg)
+        return d, stats[0]["bsp_iterations"]
     import torch
 
     cfg = cfg or KernelConfig()
