@@ -229,11 +229,25 @@ __device__ __forceinline__ void warp_windows(const Relaxer<D, W>& rx, WarpSink& 
   }
 }
 
-// Claim the next 32 items of the step for this warp (dynamic: warps that
-// drew light items take more).  Returns the first item, or -1 when done.
-__device__ __forceinline__ long long warp_next_chunk(DevCtrl* ctrl, long long n) {
+// Items per warp claim: 32, or fewer when the list would not give every
+// warp of the grid a full chunk -- then a warp's edges come from fewer,
+// longer windows and its lanes still walk 32 consecutive edges per load
+// (HP sub-iterations s >= 1 hold a few thousand windows of ~mdt edges; with
+// 32 per warp they ran as long serial chains on a fraction of the warps).
+__device__ __forceinline__ int bin_chunk(long long n) {
+  const long long warps = (long long)gridDim.x * kBinWarps;
+  if (n >= 32 * warps) return 32;
+  const long long c = n / warps;
+  int p = 1;
+  while (p * 2 <= c) p *= 2;
+  return p;
+}
+
+// Claim the next `chunk` items of the step for this warp (dynamic: warps
+// that drew light items take more).  Returns the first item, or -1 when done.
+__device__ __forceinline__ long long warp_next_chunk(DevCtrl* ctrl, long long n, int chunk) {
   unsigned long long t = 0;
-  if (lane_id() == 0) t = atomicAdd(&ctrl->relax_ticket, 32ull);
+  if (lane_id() == 0) t = atomicAdd(&ctrl->relax_ticket, (unsigned long long)chunk);
   t = __shfl_sync(0xffffffffu, t, 0);
   return (long long)t < n ? (long long)t : -1;
 }
@@ -243,11 +257,16 @@ __device__ __forceinline__ long long warp_next_chunk(DevCtrl* ctrl, long long n)
 // (hierarchical.py:95-120); unfinished nodes are carried to the next sublist.
 template <typename D, bool W>
 __global__ void __launch_bounds__(kBlock, GLB_BIN_MINB) k_hp_window(const long long* __restrict__ row,
-                                                                    Relaxer<D, W> rx0, DevCtrl* ctrl) {
+                                                                    Relaxer<D, W> rx0, DevCtrl* ctrl,
+                                                                    CtlTail tail) {
   pdl_trigger();
   __shared__ uint32_t s_wq[kBinWarps][kBinWarpQ];
   const long long n = ctrl->qcount[ctrl->in];
-  if (blockIdx.x * (long long)kBlock >= n) return;  // idle CTA
+  const int chunk = bin_chunk(n);
+  if (blockIdx.x * (long long)kBinWarps * chunk >= n) {  // idle CTA
+    ctl_tail(tail, ctrl);
+    return;
+  }
   timer_begin(ctrl->t_relax);
   const Relaxer<D, W> rx = bind(rx0, ctrl);
   WarpSink sink{s_wq[threadIdx.x >> 5], 0u, rx.qout, rx.nout};
@@ -256,8 +275,8 @@ __global__ void __launch_bounds__(kBlock, GLB_BIN_MINB) k_hp_window(const long l
   unsigned int* nnext = &ctrl->qcount[ctrl->next];
   const long long window = ctrl->window, mdt = ctrl->mdt;
   ThreadCounters c;
-  for (long long base; (base = warp_next_chunk(ctrl, n)) >= 0;) {
-    const long long i = base + lane_id();
+  for (long long base; (base = warp_next_chunk(ctrl, n, chunk)) >= 0;) {
+    const long long i = lane_id() < (unsigned)chunk ? base + lane_id() : n;
     long long lo = 0, len = 0;
     D dn = DistTraits<D>::kInf;
     if (i < n) {
@@ -282,6 +301,7 @@ __global__ void __launch_bounds__(kBlock, GLB_BIN_MINB) k_hp_window(const long l
   sink.flush();
   flush_counters(ctrl, c);
   timer_end(ctrl->t_relax);
+  ctl_tail(tail, ctrl);  // on only when no window can reach the CTA bin (no k_bigbin)
 }
 
 // ============================================================ NS (K9) ===
@@ -290,18 +310,22 @@ __global__ void __launch_bounds__(kBlock, GLB_BIN_MINB) k_hp_window(const long l
 template <typename D, bool W>
 __global__ void __launch_bounds__(kBlock, GLB_BIN_MINB) k_ns_relax(const long long* __restrict__ row,
                                                                    NsMirror mirror, Relaxer<D, W> rx0,
-                                                                   DevCtrl* ctrl) {
+                                                                   DevCtrl* ctrl, CtlTail tail) {
   pdl_trigger();
   __shared__ uint32_t s_wq[kBinWarps][kBinWarpQ];
   const long long n = ctrl->qcount[ctrl->in];
-  if (blockIdx.x * (long long)kBlock >= n) return;  // idle CTA
+  const int chunk = bin_chunk(n);
+  if (blockIdx.x * (long long)kBinWarps * chunk >= n) {  // idle CTA
+    ctl_tail(tail, ctrl);
+    return;
+  }
   timer_begin(ctrl->t_relax);
   const Relaxer<D, W> rx = bind(rx0, ctrl);
   WarpSink sink{s_wq[threadIdx.x >> 5], 0u, rx.qout, rx.nout};
   const uint32_t* __restrict__ qin = ctrl->qptr[ctrl->in];
   ThreadCounters c;
-  for (long long base; (base = warp_next_chunk(ctrl, n)) >= 0;) {
-    const long long i = base + lane_id();
+  for (long long base; (base = warp_next_chunk(ctrl, n, chunk)) >= 0;) {
+    const long long i = lane_id() < (unsigned)chunk ? base + lane_id() : n;
     long long lo = 0, len = 0;
     D dn = DistTraits<D>::kInf;
     if (i < n) {
@@ -317,6 +341,7 @@ __global__ void __launch_bounds__(kBlock, GLB_BIN_MINB) k_ns_relax(const long lo
   sink.flush();
   flush_counters(ctrl, c);
   timer_end(ctrl->t_relax);
+  ctl_tail(tail, ctrl);  // on only when no split node can reach the CTA bin (no k_bigbin)
 }
 
 // ======================================================== CTA bin (TMA) ===

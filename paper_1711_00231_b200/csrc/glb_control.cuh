@@ -185,6 +185,7 @@ constexpr int kSmallItemsCtl = 8192;
 #endif
 constexpr long long kSmallEdgesCtl = GLB_SMALL_EDGES;  // WD: active edges one cluster iteration takes
 constexpr long long kSmallMaxWindow = 64;   // HP: thread-per-node windows the cluster walks
+constexpr long long kSmallHpEdgesCtl = 16384;  // HP: window edges (items x mdt) of a cluster step
 constexpr long long kSmallNsMaxDeg = 1024;  // NS: split-node degree (mdt) a cluster thread walks
 constexpr unsigned kSmallListCtl = 32768;    // BS / NS / EP / HP-window worklists (no item table)
 __device__ __forceinline__ bool small_eligible(const DevCtrl* c) {
@@ -199,8 +200,12 @@ __device__ __forceinline__ bool small_eligible(const DevCtrl* c) {
       return c->mode == kModeRelax && c->mdt <= kSmallNsMaxDeg;
     case GLB_WD:
       return c->mode == kModeWD || (c->mode == kModeWDF && c->wd_total <= kSmallEdgesCtl);
-    case GLB_HP:  // WD-fallback steps, and window sub-iterations of short windows
-      return c->mode == kModeWD || (c->mode == kModeHP && c->mdt <= kSmallMaxWindow);
+    case GLB_HP:  // WD-fallback steps, and window sub-iterations of few, short windows
+      // (a cluster thread walks its window serially: thousands of mdt-long
+      // windows are a long chain per thread there, the grid kernel spreads them)
+      return c->mode == kModeWD ||
+             (c->mode == kModeHP && c->mdt <= kSmallMaxWindow &&
+              (long long)c->qcount[c->in] * c->mdt <= kSmallHpEdgesCtl);
     default:
       return false;
   }
@@ -290,8 +295,9 @@ __device__ __forceinline__ void control_warp(DevCtrl* c, cudaGraphConditionalHan
   if (lane != 0) return;
   // this control kernel + the step's kernels (WD: scan + relax)
   // (two-kernel steps: WD scan + relax, HP window + CTA bin, NS relax + CTA bin)
-  const bool two = c->mode == kModeWD || c->mode == kModeHP ||
-                   (c->mode == kModeRelax && c->strategy == GLB_NS);
+  const bool two = c->mode == kModeWD ||
+                   (c->bins_two && (c->mode == kModeHP ||
+                                    (c->mode == kModeRelax && c->strategy == GLB_NS)));
   c->kernels += (c->small_exit || c->done ? 2 : (two ? 3 : 2)) - (fused ? 1 : 0);
   const unsigned long long wd_next = c->wd_next;
   const unsigned wd_zero = c->wd_zero_next;

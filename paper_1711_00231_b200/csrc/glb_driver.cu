@@ -300,6 +300,7 @@ class Runner {
     // scan + relax (the pushes' row loads sit on the relax kernel's critical
     // path), so they are opt-in.
     c.hp_big = hp_big_;
+    c.bins_two = bins_two() ? 1 : 0;
     c.n_nodes = n_all_;
     // Dense-frontier scans (cells in id order) speed the relax kernel up per
     // edge but the id-ordered processing does ~10 % more re-relaxation on C2,
@@ -392,7 +393,11 @@ class Runner {
     switch (p_.strategy) {
       case GLB_BS: k_bs_relax<D, W><<<grid, kBlock, 0, s_>>>(row_, rx, ctrl_, tail_); break;
       case GLB_NS:  // binned windows + the CTA bin of the long ones (TMA-staged)
-        k_ns_relax<D, W><<<grid, kBlock, 0, s_>>>(row_, ns_mirror(), rx, ctrl_);
+        if (!bins_two()) {  // split nodes all shorter than a CTA-bin window: one kernel
+          k_ns_relax<D, W><<<grid, kBlock, 0, s_>>>(row_, ns_mirror(), rx, ctrl_, tail_);
+          break;
+        }
+        k_ns_relax<D, W><<<grid, kBlock, 0, s_>>>(row_, ns_mirror(), rx, ctrl_, CtlTail{0, {}, 0});
         GLB_CHECK_LAUNCH();
         launch_dependent(k_bigbin<D, W, NsMirror>, (unsigned)cap_big_, rx, ns_mirror(), ctrl_, tail_);
         break;
@@ -430,8 +435,16 @@ class Runner {
     cfg.numAttrs = 1;
     GLB_CUDA_TRY(cudaLaunchKernelEx(&cfg, kernel, args...));
   }
+  // HP / NS windows never reach the CTA bin when mdt < kBinCtaMin: the
+  // window kernel is then the step's only kernel (and runs the control tail)
+  bool bins_two() const { return mdt_ >= kBinCtaMin; }
   void launch_hp(unsigned grid) {
-    k_hp_window<D, W><<<grid, kBlock, 0, s_>>>(row_, relaxer(), ctrl_);
+    if (!bins_two()) {
+      k_hp_window<D, W><<<grid, kBlock, 0, s_>>>(row_, relaxer(), ctrl_, tail_);
+      GLB_CHECK_LAUNCH();
+      return;
+    }
+    k_hp_window<D, W><<<grid, kBlock, 0, s_>>>(row_, relaxer(), ctrl_, CtlTail{0, {}, 0});
     GLB_CHECK_LAUNCH();
     launch_dependent(k_bigbin<D, W, NoMirror>, (unsigned)cap_big_, relaxer(), NoMirror{}, ctrl_, tail_);
     GLB_CHECK_LAUNCH();
@@ -485,7 +498,8 @@ class Runner {
         }
         case kModeRelax: {
           const long long per = p_.strategy == GLB_EP ? 4LL * kBlock : kBlock;
-          const unsigned grid = grid_for(n_in, (int)per, cap_relax_);
+          const unsigned grid = p_.strategy == GLB_NS ? (unsigned)cap_relax_  // as HP windows
+                                                      : grid_for(n_in, (int)per, cap_relax_);
           ev.threads = (long long)grid * kBlock;
           if (timing) GLB_CUDA_TRY(cudaEventRecord(ev.k0, s_));
           launch_relax(grid);
@@ -516,8 +530,8 @@ class Runner {
         case kModeRenorm:
           launch_renorm();
           break;
-        case kModeHP: {
-          const unsigned grid = grid_for(n_in, kBlock, cap_hp_);
+        case kModeHP: {  // full grid: the window kernel sizes its warp chunks to the list
+          const unsigned grid = (unsigned)cap_hp_;
           ev.threads = (long long)grid * kBlock;
           if (timing) GLB_CUDA_TRY(cudaEventRecord(ev.k0, s_));
           launch_hp(grid);

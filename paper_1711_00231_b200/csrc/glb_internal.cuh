@@ -243,6 +243,7 @@ struct DevCtrl {
   struct HpBig* hp_big;         // bin entries of the current window step
   unsigned long long hp_big_ctr;  // (entries << 32) | pieces reserved, in one atomic
   unsigned int hp_piece_next;   // next piece ticket
+  int bins_two;                 // HP / NS steps launch k_bigbin after the window kernel
   // ---- HP super-iteration state (hierarchical.py:54-136)
   int sup_in, sup_out, cur, spare;
   long long s;

@@ -482,8 +482,12 @@ __global__ void __launch_bounds__(kBlock) k_ep_relax(const long long* __restrict
 // ====================================================== WD (K4 + K5/K6) ===
 constexpr int kWdIPT = 8;                     // frontier items per thread in the scan
 constexpr int kWdScanTile = kBlock * kWdIPT;  // 2048 items per scan tile
-constexpr int kWdEPL = 8;                     // edges per lane of a warp tile
+#ifndef GLB_WD_EPL
+#define GLB_WD_EPL 8
+#endif
+constexpr int kWdEPL = GLB_WD_EPL;            // edges per lane of a warp tile
 constexpr int kWdTile = 32 * kWdEPL;          // 256 edges per warp tile
+static_assert(kWdEPL % 4 == 0, "head flags are handled in int4 groups");
 constexpr int kWdWarpQ = 256;                 // per-warp push buffer (smem entries)
 
 // One compacted frontier item of a WD invocation (16 B, one 128-bit load):
@@ -777,8 +781,8 @@ __global__ void __launch_bounds__(kBlock, GLB_WD_MINB) k_wd_relax(
     // ---- head flags: item i of the tile writes i at its first edge
     {
       int4* o4 = reinterpret_cast<int4*>(own + lane * kWdEPL);
-      o4[0] = make_int4(0, 0, 0, 0);
-      o4[1] = make_int4(0, 0, 0, 0);
+#pragma unroll
+      for (int q = 0; q < kWdEPL / 4; ++q) o4[q] = make_int4(0, 0, 0, 0);
     }
     __syncwarp();
     // (the tile's last item may start exactly at the next tile: st == 256)
@@ -805,8 +809,15 @@ __global__ void __launch_bounds__(kBlock, GLB_WD_MINB) k_wd_relax(
     //      max-scan for the carry, scanned owners back to shared memory ...
     {
       int4* o4 = reinterpret_cast<int4*>(own + lane * kWdEPL);
-      const int4 a = o4[0], b = o4[1];
-      int o[kWdEPL] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+      int o[kWdEPL];
+#pragma unroll
+      for (int q = 0; q < kWdEPL / 4; ++q) {
+        const int4 a = o4[q];
+        o[4 * q] = a.x;
+        o[4 * q + 1] = a.y;
+        o[4 * q + 2] = a.z;
+        o[4 * q + 3] = a.w;
+      }
 #pragma unroll
       for (int k = 1; k < kWdEPL; ++k) o[k] = o[k] > o[k - 1] ? o[k] : o[k - 1];
       int carry = o[kWdEPL - 1];
@@ -819,8 +830,8 @@ __global__ void __launch_bounds__(kBlock, GLB_WD_MINB) k_wd_relax(
       if (lane == 0) prev = 0;
 #pragma unroll
       for (int k = 0; k < kWdEPL; ++k) o[k] = o[k] > prev ? o[k] : prev;
-      o4[0] = make_int4(o[0], o[1], o[2], o[3]);
-      o4[1] = make_int4(o[4], o[5], o[6], o[7]);
+#pragma unroll
+      for (int q = 0; q < kWdEPL / 4; ++q) o4[q] = make_int4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
     }
     __syncwarp();
     // ... and read back so that lane l takes edges k*32 + l: each load
