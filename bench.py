@@ -153,16 +153,27 @@ class ClockSampler:
                 "samples": len(sm), "reasons": sorted(reasons)}
 
 
-def cpu_sample(ng, algo, seconds, threads=0):
-    """The pinned run_bs port on all host threads: full traversals while they
-    fit the bound, else one time-bounded traversal extrapolated by its share
-    of a full traversal's relaxations (measured once, untimed)."""
+# the reference's CPU algorithm per strategy: C ports of run_wd / run_bs
+PORTS = {"WD": ("wd_run_narrow", "run_wd", "workload.py:75-189"),
+         "BS": ("bs_run_narrow", "run_bs", "node_based.py:19-82")}
+
+
+def port_of(strategy):
+    """Same strategy as our arm where a port exists (WD, BS), else run_bs."""
+    return strategy.upper() if strategy.upper() in PORTS else "BS"
+
+
+def cpu_sample(ng, algo, seconds, threads=0, strategy="WD"):
+    """The pinned port of the strategy's driver on all host threads: full
+    traversals while they fit the bound, else one time-bounded traversal
+    extrapolated by its share of a full traversal's relaxations."""
     from oracle import oracle
 
     w = algo == "sssp"
     threads = threads or (os.cpu_count() or 1)
+    fn = getattr(oracle, PORTS[port_of(strategy)][0])
     t0 = time.perf_counter()
-    d, it, ops, done = oracle.bs_run_narrow(ng, 0, w, threads, max_seconds=seconds)
+    d, it, ops, done = fn(ng, 0, w, threads, max_seconds=seconds)
     t = time.perf_counter() - t0
     return d, it, ops, done, t, threads
 
@@ -382,14 +393,16 @@ def ours(args):
     # ---- CPU baseline: pinned C port of run_bs on the host cores
     cpu = None
     if not args.no_cpu:
-        d, it, ops, done, t, thr = cpu_sample(ng, args.algo, args.cpu_seconds)
+        port = port_of(args.strategy)
+        d, it, ops, done, t, thr = cpu_sample(ng, args.algo, args.cpu_seconds, strategy=port)
         rate = e_r / t / 1e9 if done else None
+        _, drv, cite = PORTS[port]
         cpu = {"value": round(rate, 5) if rate else round(ops / t / 1e9, 5), "unit": UNIT,
-               "cores": thr, "kind": "port",
-               "sample": (f"one full {args.algo.upper()} run_bs traversal of the benchmark graph "
+               "cores": thr, "kind": "port", "strategy": port,
+               "sample": (f"one full {args.algo.upper()} {drv} traversal of the benchmark graph "
                           f"({t:.2f} s, {it} iterations, {ops} relaxations), C port of "
-                          f"node_based.py:19-82 on {thr} threads" if done else
-                          f"run_bs stopped after {it} iterations / {t:.1f} s; value = examined "
+                          f"{cite} on {thr} threads" if done else
+                          f"{drv} stopped after {it} iterations / {t:.1f} s; value = examined "
                           f"edges per second")}
 
     line = {
@@ -554,7 +567,7 @@ def ours_sharded(args, world, rank, local):
 
         oracle.build()
         ng = oracle.NarrowGraph(*host_narrow)
-        _, it, ops, done, t, thr = cpu_sample(ng, args.algo, args.cpu_seconds)
+        _, it, ops, done, t, thr = cpu_sample(ng, args.algo, args.cpu_seconds, strategy=tag)
         cpu = {"value": round(e_r / t / 1e9 if done else ops / t / 1e9, 5), "unit": UNIT,
                "cores": thr, "kind": "port",
                "sample": (f"one full traversal of the same graph ({t:.1f} s)" if done else
@@ -589,9 +602,11 @@ def ours_sharded(args, world, rank, local):
 def reference(args):
     """The reference's algorithm on the host cores, without the CUDA library:
     graph by the pinned C restatement of generate_rmat, steps by the pinned C
-    port of run_bs (full traversals; at scale > 24 each step is a time-bounded
-    sample whose value extrapolates by its share of a full traversal's
-    relaxations, measured once untimed)."""
+    port of the SAME strategy's driver as our arm (run_wd for WD, run_bs for
+    BS; other strategies fall back to run_bs) -- full traversals; at scale >
+    24 each step is a time-bounded sample whose value extrapolates by its
+    share of a full traversal's relaxations, measured once untimed.  The other
+    port is timed once beside it (``ports``) for the best-vs-best view."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
@@ -604,21 +619,32 @@ def reference(args):
     gen_s = time.time() - t0
     w = args.algo == "sssp"
     bounded = args.scale > 24
-    d, it, ops_full, done = oracle.bs_run_narrow(ng, 0, w, threads)
+    port = port_of(args.strategy)
+    fn_name, drv, cite = PORTS[port]
+    run = getattr(oracle, fn_name)
+    d, it, ops_full, done = run(ng, 0, w, threads)
     e_r, n_r = reached_edges(ng.outdegrees(), d)
     vals = []
     for i in range(args.warmup + args.steps):
         t1 = time.perf_counter()
-        _, it, ops, done = oracle.bs_run_narrow(ng, 0, w, threads,
-                                                max_seconds=args.cpu_seconds if bounded else 0.0)
+        _, it, ops, done = run(ng, 0, w, threads, max_seconds=args.cpu_seconds if bounded else 0.0)
         t = time.perf_counter() - t1
         if i >= args.warmup:
             vals.append(e_r * (ops / ops_full) / t / 1e9)
     value = statistics.mean(vals)
     ms = e_r / (value * 1e9) * 1e3
+    ports = {port: round(value, 5)}
+    for other, (fo, _, _) in PORTS.items():  # one sample of the other port
+        if other == port:
+            continue
+        t1 = time.perf_counter()
+        _, _, ops, odone = getattr(oracle, fo)(ng, 0, w, threads, max_seconds=args.cpu_seconds)
+        t = time.perf_counter() - t1
+        # a full traversal: E_r / t; a bounded one: examined edges / t
+        ports[other] = round((e_r if odone else ops) / t / 1e9, 5)
     sample = (f"each step = one {'time-bounded (' + str(args.cpu_seconds) + ' s) ' if bounded else 'full '}"
-              f"{args.algo.upper()} node-based (run_bs) traversal of the benchmark graph, C port of "
-              f"node_based.py:19-82 on {threads} threads; graph from the C restatement of "
+              f"{args.algo.upper()} {drv} traversal of the benchmark graph, C port of "
+              f"{cite} on {threads} threads; graph from the C restatement of "
               f"generate_rmat (oracle_rmat_u32, {gen_s:.1f} s)")
     line = {
         "metric": METRIC, "value": round(value, 5), "unit": UNIT, "n_gpus": args.gpus,
@@ -626,11 +652,12 @@ def reference(args):
         "higher_is_better": True, "scaling": "weak" if args.gpus == 1 else "strong",
         "vs_baseline": None, "dtype": "int64",
         "data": "synthetic (RMAT from the pinned C restatement of graphlb.generate_rmat)",
-        "config": {"workload": workload_name(args, args.gpus), "strategy": "BS",
+        "config": {"workload": workload_name(args, args.gpus), "strategy": port,
                    "nodes": ng.num_nodes, "edges": ng.num_edges, "E_r": e_r, "N_r": n_r},
         "impl": "reference",
         "cpu_baseline": {"value": round(value, 5), "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": sample},
+                         "strategy": port, "sample": sample},
+        "ports": ports,
         "e2e": {"value": round(value, 5), "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }

@@ -546,3 +546,144 @@ int oracle_bs_run_u32(int64_t n, const int64_t* row, const uint32_t* col, const 
   if (completed) *completed = !st.stopped;
   return 0;
 }
+
+/* ========================================================== run_wd (port) */
+/* Workload decomposition (strategies/workload.py:75-159, run_wd loop
+ * workload.py:162-189) over the narrow layout: per iteration the frontier's
+ * out-degrees are prefix-summed (inclusive_scan, scan.py:19-65), every host
+ * thread takes an equal slice of ept = ceil(total / threads) edges, finds its
+ * first item by binary search over the prefix (find_offsets,
+ * workload.py:45-72) and walks the slice, reading the item's distance when it
+ * enters a node (workload.py:131,140).  Test / baseline infrastructure only. */
+typedef struct {
+  const int64_t* row;
+  const uint32_t *col, *w;
+  int64_t* dist;
+  uint32_t *in, *out;
+  int64_t* prefix;      /* inclusive prefix of the frontier's out-degrees */
+  int64_t* part;        /* per-thread partial sums of the scan */
+  unsigned char* flag;
+  int64_t n_in, n_out, ops, iterations, total;
+  double deadline;
+  int stopped, nth;
+  pthread_barrier_t bar;
+} wd32_t;
+
+static void* wd32_job(void* p, int tid, int nth) {
+  wd32_t* st = (wd32_t*)p;
+  int64_t ops = 0;
+  for (;;) {
+    pthread_barrier_wait(&st->bar);
+    const int64_t n_in = st->n_in;
+    if (n_in == 0 || st->stopped) break;
+    /* scan pass 1: this thread's chunk of the frontier */
+    const int64_t c0 = n_in * tid / nth, c1 = n_in * (tid + 1) / nth;
+    int64_t s = 0;
+    for (int64_t i = c0; i < c1; ++i) {
+      const uint32_t u = st->in[i];
+      s += st->row[u + 1] - st->row[u];
+    }
+    st->part[tid] = s;
+    if (pthread_barrier_wait(&st->bar) == PTHREAD_BARRIER_SERIAL_THREAD) {
+      int64_t run = 0;
+      for (int t = 0; t < nth; ++t) {
+        const int64_t x = st->part[t];
+        st->part[t] = run;
+        run += x;
+      }
+      st->total = run;
+    }
+    pthread_barrier_wait(&st->bar);
+    s = st->part[tid];
+    for (int64_t i = c0; i < c1; ++i) {
+      const uint32_t u = st->in[i];
+      s += st->row[u + 1] - st->row[u];
+      st->prefix[i] = s;
+    }
+    pthread_barrier_wait(&st->bar);
+    /* relax: an equal slice of edges per thread */
+    const int64_t total = st->total;
+    const int64_t ept = (total + nth - 1) / nth;
+    int64_t start = (int64_t)tid * ept, end = start + ept < total ? start + ept : total;
+    if (start < end) {
+      int64_t lo = 0, hi = n_in - 1; /* first item whose inclusive prefix > start */
+      while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (st->prefix[mid] > start)
+          hi = mid;
+        else
+          lo = mid + 1;
+      }
+      int64_t wi = lo;
+      int64_t f = start;
+      while (f < end) {
+        const uint32_t u = st->in[wi];
+        const int64_t pre0 = st->prefix[wi] - (st->row[u + 1] - st->row[u]);
+        const int64_t stop = st->prefix[wi] < end ? st->prefix[wi] : end;
+        const int64_t du = __atomic_load_n(&st->dist[u], __ATOMIC_RELAXED); /* dn at node entry */
+        for (; f < stop; ++f) {
+          const int64_t e = st->row[u] + (f - pre0);
+          const uint32_t v = st->col[e];
+          ++ops;
+          if (du != ORACLE_INF &&
+              relax_cas(&st->dist[v], du + (st->w ? (int64_t)st->w[e] : 1)) &&
+              !__atomic_exchange_n(&st->flag[v], 1, __ATOMIC_RELAXED)) {
+            const int64_t slot = __atomic_fetch_add(&st->n_out, 1, __ATOMIC_RELAXED);
+            st->out[slot] = v;
+          }
+        }
+        ++wi;
+      }
+    }
+    if (pthread_barrier_wait(&st->bar) == PTHREAD_BARRIER_SERIAL_THREAD) {
+      for (int64_t i = 0; i < st->n_out; ++i) st->flag[st->out[i]] = 0; /* clear() on swap */
+      uint32_t* t = st->in;
+      st->in = st->out;
+      st->out = t;
+      st->n_in = st->total ? st->n_out : 0; /* no edges left: done (workload.py:181-183) */
+      st->n_out = 0;
+      st->iterations++;
+      if (st->deadline > 0 && st->n_in && mono_s() > st->deadline) st->stopped = 1;
+    }
+  }
+  __atomic_fetch_add(&st->ops, ops, __ATOMIC_RELAXED);
+  return NULL;
+}
+
+/* run_wd over the narrow layout; arguments and results as oracle_bs_run_u32. */
+int oracle_wd_run_u32(int64_t n, const int64_t* row, const uint32_t* col, const uint32_t* w,
+                      int64_t source, int threads, double max_seconds, int64_t* dist,
+                      int64_t* iterations, int64_t* relax_ops, int* completed) {
+  if (source < 0 || source >= n) return -1;
+  int nth = nthreads_or_all(threads);
+  wd32_t st;
+  memset(&st, 0, sizeof(st));
+  st.row = row;
+  st.col = col;
+  st.w = w;
+  st.dist = dist;
+  st.nth = nth;
+  const size_t nb = (size_t)(n > 0 ? n : 1);
+  st.in = (uint32_t*)malloc(sizeof(uint32_t) * nb);
+  st.out = (uint32_t*)malloc(sizeof(uint32_t) * nb);
+  st.prefix = (int64_t*)malloc(sizeof(int64_t) * nb);
+  st.part = (int64_t*)malloc(sizeof(int64_t) * (size_t)nth);
+  st.flag = (unsigned char*)calloc(nb, 1);
+  if (!st.in || !st.out || !st.prefix || !st.part || !st.flag) {
+    free(st.in); free(st.out); free(st.prefix); free(st.part); free(st.flag);
+    return -2;
+  }
+  for (int64_t i = 0; i < n; ++i) dist[i] = ORACLE_INF;
+  dist[source] = 0;
+  st.in[0] = (uint32_t)source;
+  st.n_in = 1;
+  st.deadline = max_seconds > 0 ? mono_s() + max_seconds : 0;
+  pthread_barrier_init(&st.bar, NULL, (unsigned)nth);
+  parallel(wd32_job, &st, nth);
+  pthread_barrier_destroy(&st.bar);
+  free(st.in); free(st.out); free(st.prefix); free(st.part); free(st.flag);
+  if (iterations) *iterations = st.iterations;
+  if (relax_ops) *relax_ops = st.ops;
+  if (completed) *completed = !st.stopped;
+  return 0;
+}

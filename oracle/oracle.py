@@ -57,6 +57,7 @@ def lib() -> ctypes.CDLL:
         L.oracle_bfs_levels_u32.argtypes = [i64, _p64, u32p, i64, ctypes.c_int, _p64]
         L.oracle_bs_run_u32.argtypes = [i64, _p64, u32p, u32p, i64, ctypes.c_int, ctypes.c_double,
                                         _p64, _p64, _p64, ctypes.POINTER(ctypes.c_int)]
+        L.oracle_wd_run_u32.argtypes = L.oracle_bs_run_u32.argtypes
         _lib = L
     return _lib
 
@@ -260,6 +261,22 @@ def bs_run_narrow(g, source: int, weighted: bool, threads: int = 0, max_seconds:
         raise ValueError("bad source")
     if rc:
         raise MemoryError("oracle bs_run: allocation failed")
+    return out, it.value, ops.value, bool(done.value)
+
+
+def wd_run_narrow(g, source: int, weighted: bool, threads: int = 0, max_seconds: float = 0.0):
+    """run_wd (workload.py:75-189) port over the narrow layout, equal edge
+    slices per host thread; results as bs_run_narrow."""
+    out = np.empty(g.num_nodes, dtype=np.int64)
+    it, ops, done = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int()
+    w = g.weights if weighted else None
+    rc = lib().oracle_wd_run_u32(g.num_nodes, _p(g.row_offsets), _u32(g.col_indices), _u32(w),
+                                 source, threads, max_seconds, _p(out), ctypes.byref(it),
+                                 ctypes.byref(ops), ctypes.byref(done))
+    if rc == -1:
+        raise ValueError("bad source")
+    if rc:
+        raise MemoryError("oracle wd_run: allocation failed")
     return out, it.value, ops.value, bool(done.value)
 
 

@@ -137,6 +137,11 @@ def test_oracle_narrow_traversals_match_reference_corpus(oracle, golden):
                 else:
                     d, _, _, done = oracle.bs_run_narrow(ng, src, ng.weights is not None, threads=4)
                     assert done and np.array_equal(d, exp), gid
+                # the run_wd port (the reference arm of bench.py): both kinds
+                w = algo == "sssp" and ng.weights is not None
+                for th in (1, 3):
+                    d, _, _, done = oracle.wd_run_narrow(ng, src, w, threads=th)
+                    assert done and np.array_equal(d, exp), (gid, src, algo, th)
 
 
 def test_oracle_narrow_c2_matches_reference_digests(oracle, golden):
@@ -153,3 +158,5 @@ def test_oracle_narrow_c2_matches_reference_digests(oracle, golden):
     # a time-bounded run_bs sample stops early with partial work counted
     _, it, ops, done = oracle.bs_run_narrow(g, 0, True, max_seconds=1e-6)
     assert not done and it >= 1 and ops >= 1
+    d, _, _, done = oracle.wd_run_narrow(g, 0, True)
+    assert done and gs.dist_digest(d) == c2["sssp_digest"]
