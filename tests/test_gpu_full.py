@@ -91,9 +91,25 @@ def test_c5_rmat27_single_gpu(oracle):
     assert np.array_equal(ref.weights, w)
     del ref
     ng = oracle.NarrowGraph(row, col, w)
+    exps = {}
     for algo in ("bfs", "sssp"):
         exp = oracle.narrow_distances(ng, 0, algo)
+        exps[algo] = exp
         _check_all(g, exp, algo, tags=("BS", "WD", "NS", "HP"))
         r = pkg.run_ep(g, 0, pkg.RelaxOp(algo), pkg.KernelConfig(instrument=False))
         assert r.status == pkg.INFEASIBLE_MEMORY and r.dist is None
     g.release_device()
+    del g, row, col, w, ng
+    # C5 as north_star shards it: 1-D edge-balanced vertex partition, here two
+    # ranks sharing GPU 0 over the peer transport (the one-process-per-GPU
+    # code path minus CUDA IPC), against the same oracle arrays
+    from paper_1711_00231_b200 import sharded
+
+    shards = [sharded.shard_rmat(27, 16, 2, r, 0, seed=1) for r in range(2)]
+    for algo in ("bfs", "sssp"):
+        d, st = sharded.run_virtual_peer("WD", shards, 0, pkg.RelaxOp(algo),
+                                         pkg.KernelConfig(instrument=False))
+        assert np.array_equal(d, exps[algo]), algo
+        assert st[0]["dist_bits"] == 24  # u64 cells would exceed twice the L2
+    for sg in shards:
+        sg.graph.release_device()
