@@ -66,11 +66,19 @@ class Runner {
       : g_(g), p_(p), recs_(recs), s_(g->stream) {}
 
   void run(int64_t* dist_out, glb_run_stats* st) {
-    prepare(st);
-    if (p_.loop_mode == GLB_LOOP_GRAPH)
-      loop_graph();
-    else
-      loop_host();
+    {
+      NvtxRange r("glb setup (histogram/MDT, split, COO, init)");
+      prepare(st);
+    }
+    {
+      NvtxRange r(p_.loop_mode == GLB_LOOP_GRAPH ? "glb traversal (graph loop)"
+                                                  : "glb traversal (host loop)");
+      if (p_.loop_mode == GLB_LOOP_GRAPH)
+        loop_graph();
+      else
+        loop_host();
+    }
+    NvtxRange r("glb distances + records to host");
     finish_run(dist_out, st, 0, g_->n);
   }
 
@@ -1010,6 +1018,7 @@ class PeerRun : public PeerRunBase, public Runner<D, W> {
   }
 
   void issue(unsigned long long seq) override {
+    NvtxRange r("glb bsp iteration: local relaxation + peer exchange (issue)");
     const int parity = (int)(seq & 1ull);
     cudaStream_t s = this->s_;
     GLB_CUDA_TRY(cudaGraphLaunch(exec_, s));  // local relaxation, paused at the iteration boundary
@@ -1034,7 +1043,10 @@ class PeerRun : public PeerRunBase, public Runner<D, W> {
   }
 
   int complete() override {
-    GLB_CUDA_TRY(cudaStreamSynchronize(this->s_));
+    {
+      NvtxRange r("glb bsp iteration: wait for the global verdict");
+      GLB_CUDA_TRY(cudaStreamSynchronize(this->s_));
+    }
     const DevCtrl& hc = this->h_->ctrl;
     if ((hc.bad_input & 0xFFFF0000u) == kPeerTimeoutFlag) {
       pr_->poisoned = true;

@@ -730,6 +730,7 @@ int glb_device_count(int* count) {
 
 int glb_graph_create(const int64_t* row_offsets, const int64_t* col, const int64_t* weights_or_null,
                      int64_t n, int64_t m, int device, glb_graph** out) {
+  glb::NvtxRange nvtx_range("glb_graph_create (validate, narrow, upload)");
   return guarded([&] {
     if (!out) throw Error{GLB_EINVAL, "out is NULL"};
     *out = nullptr;
@@ -777,6 +778,7 @@ int glb_graph_create(const int64_t* row_offsets, const int64_t* col, const int64
 int glb_graph_create_rmat(int scale, int64_t edge_factor, double t_a, double t_ab, double t_abc,
                           const uint64_t* state_hi_lo, const uint64_t* inc_hi_lo, int weighted,
                           int64_t max_weight, int device, glb_graph** out) {
+  glb::NvtxRange nvtx_range("glb_graph_create_rmat (generate + CSR build in HBM)");
   return guarded([&] {
     if (!out || !state_hi_lo || !inc_hi_lo) throw Error{GLB_EINVAL, "NULL argument"};
     *out = nullptr;

@@ -11,6 +11,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 #include <stdint.h>
 
 #include <mutex>
@@ -26,6 +27,18 @@ constexpr int kStatSlots = 32;  // spread of the per-launch counter atomics
 // Tail padding of every u32 edge array (col / weights): the CTA bin's 1-D
 // TMA copies read whole 16-byte units, up to 3 elements past the last edge.
 constexpr size_t kEdgePad = 64;
+
+// NVTX range over a host-side phase (header-only NVTX v3: free unless a
+// profiler is attached).  Phases mirror the reference's perf_counter splits
+// (engine.py:221,269; node_based.py:21-29,75-78; workload.py:96-110):
+// upload, setup overhead, traversal loop, distances back, and per BSP
+// iteration of a sharded run the local relaxation and the peer exchange.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 // ---------------------------------------------------------------- errors ---
 void set_error(const std::string& msg);

@@ -29,9 +29,11 @@ ap.add_argument("--reps", type=int, default=5)
 ap.add_argument("--loop", default="graph")
 ap.add_argument("--skewed", action="store_true")
 ap.add_argument("--dist-bits", type=int, default=0)
+ap.add_argument("--grid", type=int, default=0, help="k x k grid (C3: 4096) instead of an R-MAT")
 a = ap.parse_args()
 params = (0.7, 0.15, 0.10, 0.05) if a.skewed else pkg.DEFAULT_RMAT_PARAMS
-g = pkg.generate_rmat(a.scale, 16, params=params, seed=1, max_weight=255)
+g = (pkg.grid_graph(a.grid, seed=1, max_weight=255) if a.grid else
+     pkg.generate_rmat(a.scale, 16, params=params, seed=1, max_weight=255))
 from oracle import oracle  # noqa: E402
 
 exp = oracle.oracle_distances(g, 0, a.algo)
