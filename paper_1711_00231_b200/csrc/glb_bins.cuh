@@ -43,9 +43,11 @@
 namespace glb {
 
 constexpr unsigned kBinThreadMax = 32;   // thread bin: windows of at most 32 edges
-constexpr long long kBinCtaMin = 2048;   // CTA bin: windows of at least 2048 edges
+#ifndef GLB_BIN_CTA_MIN
+#define GLB_BIN_CTA_MIN 512  // C4 A/B: 2048 -> 512 took HP BFS 1.36 -> 1.09 ms, NS 2.06 -> 1.69 ms
+#endif
+constexpr long long kBinCtaMin = GLB_BIN_CTA_MIN;  // CTA bin: windows of at least this many edges
 constexpr long long kBinPiece = 2048;    // edges per CTA-bin piece (one TMA stage)
-constexpr int kBinQbCache = 1024;        // CTA-bin windows whose first piece is cached in smem
 constexpr int kBinBuf = (int)kBinPiece + 4;  // a piece plus the 16-byte alignment slack
 constexpr int kBinK = 4;                 // edges in flight per lane
 
@@ -170,11 +172,14 @@ template <typename D>
 __device__ __forceinline__ void cta_bin_push(DevCtrl* ctrl, long long lo, long long len, D dn) {
   const unsigned pieces = (unsigned)((len + kBinPiece - 1) / kBinPiece);
   const unsigned long long r = atomicAdd(&ctrl->hp_big_ctr, (1ull << 32) | (unsigned long long)pieces);
-  HpBig* b = ctrl->hp_big + (unsigned)(r >> 32);
+  const unsigned e = (unsigned)(r >> 32);
+  HpBig* b = ctrl->hp_big + e;
   b->dn = (unsigned long long)dn;
   b->lo = lo;
   b->hi = lo + len;
   b->qbase = (unsigned)r;
+  // piece -> window table: k_bigbin finds a claimed piece's window in one read
+  for (unsigned k = 0; k < pieces; ++k) ctrl->hp_owner[(unsigned)r + k] = e;
 }
 
 // The windows of a warp's 32 lanes (len 0 = none; all lanes call it).
@@ -366,24 +371,20 @@ __global__ void __launch_bounds__(kBlock) k_bigbin(Relaxer<D, W> rx0, M mirror, 
   __shared__ BigPiece<D> s_pc[2];
   __shared__ uint32_t s_q[kQCap];
   __shared__ BlockQ bq;
-  __shared__ unsigned s_qb[kBinQbCache];
   const unsigned long long bc = ctrl->hp_big_ctr;
-  const unsigned nbig = (unsigned)(bc >> 32), npieces = (unsigned)bc;
+  const unsigned npieces = (unsigned)bc;  // (entries << 32 | pieces)
   if (npieces == 0 || blockIdx.x >= npieces) {
     ctl_tail(tail, ctrl);
     return;
   }
   timer_begin(ctrl->t_relax);
   const Relaxer<D, W> rx = bind(rx0, ctrl);
-  const bool cached = nbig <= (unsigned)kBinQbCache;
-  if (cached)
-    for (unsigned i = threadIdx.x; i < nbig; i += kBlock) s_qb[i] = ctrl->hp_big[i].qbase;
   if (threadIdx.x == 0) {
     mbar_init(&s_bar[0], 1);
     mbar_init(&s_bar[1], 1);
     mbar_fence_init();
   }
-  bq_init(bq, s_q);  // barrier: s_qb and the mbarriers are ready
+  bq_init(bq, s_q);  // barrier: the mbarriers are ready
   const unsigned long long pol = l2_evict_first();
   // thread 0: claim a piece into buffer b and start its copies
   auto claim = [&](int b) {
@@ -393,16 +394,7 @@ __global__ void __launch_bounds__(kBlock) k_bigbin(Relaxer<D, W> rx0, M mirror, 
       pc.valid = 0;
       return;
     }
-    unsigned lo_i = 0, hi_i = nbig;  // last window with qbase <= t
-    while (hi_i - lo_i > 1) {
-      const unsigned mid = (lo_i + hi_i) >> 1;
-      const unsigned qb = cached ? s_qb[mid] : ctrl->hp_big[mid].qbase;
-      if (qb <= t)
-        lo_i = mid;
-      else
-        hi_i = mid;
-    }
-    const HpBig w = ctrl->hp_big[lo_i];
+    const HpBig w = ctrl->hp_big[ctrl->hp_owner[t]];
     const long long lo = w.lo + (long long)(t - w.qbase) * kBinPiece;
     const long long hi = lo + kBinPiece < w.hi ? lo + kBinPiece : w.hi;
     const long long a_lo = lo & ~3ll;  // 16-byte aligned source (arrays carry a 64 B tail pad)

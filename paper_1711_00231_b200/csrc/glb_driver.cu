@@ -179,6 +179,7 @@ class Runner {
   HostMirror* h_ = nullptr;
   // WD workspace
   HpBig* hp_big_ = nullptr;
+  unsigned* hp_owner_ = nullptr;
   WdItem* items_[2] = {nullptr, nullptr};
   unsigned* tile_first_[2] = {nullptr, nullptr};
   LookbackState<2> lb_{};
@@ -259,7 +260,10 @@ class Runner {
       cap_hp_ = std::max(cap((const void*)k_hp_window<D, W>), g_->num_sms);
     if (p_.strategy == GLB_HP || p_.strategy == GLB_NS) {
       // CTA-bin entries: every long window holds >= kBinCtaMin edges
-      hp_big_ = (HpBig*)ensure(ws.hp_big, ((size_t)g_->m / kBinCtaMin + 64) * sizeof(HpBig));
+      const size_t entries = (size_t)g_->m / kBinCtaMin + 64;
+      const size_t pieces = entries + (size_t)g_->m / kBinPiece + 64;
+      hp_big_ = (HpBig*)ensure(ws.hp_big, entries * sizeof(HpBig) + pieces * 4);
+      hp_owner_ = reinterpret_cast<unsigned*>(hp_big_ + entries);
       cap_big_ = std::max(p_.strategy == GLB_HP ? cap((const void*)k_bigbin<D, W, NoMirror>)
                                                 : cap((const void*)k_bigbin<D, W, NsMirror>),
                           g_->num_sms);
@@ -308,6 +312,7 @@ class Runner {
     // scan + relax (the pushes' row loads sit on the relax kernel's critical
     // path), so they are opt-in.
     c.hp_big = hp_big_;
+    c.hp_owner = hp_owner_;
     c.bins_two = bins_two() ? 1 : 0;
     c.n_nodes = n_all_;
     // Dense-frontier scans (cells in id order) speed the relax kernel up per

@@ -254,6 +254,7 @@ struct DevCtrl {
   long long n_nodes;            // nodes of the traversed graph
   // ---- HP: windows >= kHpCtaThreshold edges form a grid-wide CTA bin
   struct HpBig* hp_big;         // bin entries of the current window step
+  unsigned int* hp_owner;       // CTA-bin piece -> entry
   unsigned long long hp_big_ctr;  // (entries << 32) | pieces reserved, in one atomic
   unsigned int hp_piece_next;   // next piece ticket
   int bins_two;                 // HP / NS steps launch k_bigbin after the window kernel
