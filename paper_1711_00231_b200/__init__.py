@@ -11,8 +11,9 @@ Not provided here (outside the hot path): the CPU launch emulation
 oracles (they live in oracle/ as test infrastructure); results are instead
 certified on the device (validate_distances).  The file loaders (io.py) are
 native and read the binary cache straight into HBM.  The benchmark harness,
-report writer and CLI are ``.bench``, ``.report`` and ``.cli``
-(``python -m paper_1711_00231_b200``).
+report writer and CLI are off the hot path and not rebuilt; the
+reference's own ``summarize_run`` accepts this package's records.  Sharded
+multi-GPU runs are ``.sharded``.
 """
 
 from .analysis import (
