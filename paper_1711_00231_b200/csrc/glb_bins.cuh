@@ -220,6 +220,12 @@ __device__ __forceinline__ void warp_windows(const Relaxer<D, W>& rx, WarpSink& 
       }
       const uint32_t e = __shfl_sync(FULL, base32, o) + f;
       d[k] = shfl_dist(dn, o);
+#if GLB_RELAX_BRANCHLESS
+      valid |= (unsigned)(f < total) << k;
+      const uint32_t ek = f < total ? e : 0u;  // invalid slots load edge 0 (always mapped)
+      v[k] = ld_stream_pol(rx.col + ek, pol);
+      w[k] = W ? ld_stream_pol(rx.wt + ek, pol) : 1u;
+#else
       v[k] = 0;
       w[k] = 1u;
       if (f < total) {
@@ -227,6 +233,7 @@ __device__ __forceinline__ void warp_windows(const Relaxer<D, W>& rx, WarpSink& 
         v[k] = ld_stream_pol(rx.col + e, pol);
         if (W) w[k] = ld_stream_pol(rx.wt + e, pol);
       }
+#endif
     }
     D cand[K];
     const unsigned won = relax_vals<K>(rx, sink, v, w, d, valid, c, cand);

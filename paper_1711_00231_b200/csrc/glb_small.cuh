@@ -38,6 +38,9 @@ namespace cg = cooperative_groups;
 #ifndef GLB_SMALL_CTAS
 #define GLB_SMALL_CTAS 8
 #endif
+#ifndef GLB_SMALL_BRANCHLESS
+#define GLB_SMALL_BRANCHLESS 1  // small_relax without divergent regions (C3 BFS BS 79.5 -> 75.1 ms)
+#endif
 constexpr int kSmallCtas = GLB_SMALL_CTAS;        // cluster size (8 = portable maximum, 16 opt-in)
 constexpr int kSmallThreads = 1024;               // threads per CTA
 constexpr int kSmallAll = kSmallCtas * kSmallThreads;
@@ -79,6 +82,32 @@ __device__ __forceinline__ unsigned small_relax(const Relaxer<D, W>& rx, unsigne
                                                 ThreadCounters& c, uint32_t (&v)[K],
                                                 D (&cand)[K], const SmallPush* fused = nullptr) {
   uint32_t w[K];
+  unsigned want = 0;
+#if GLB_SMALL_BRANCHLESS
+  // invalid slots load edge 0 / gather its head (always mapped): no divergent regions
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const uint32_t ek = (valid >> k & 1u) ? e[k] : 0u;
+    v[k] = __ldg(rx.col + ek);
+    w[k] = W ? __ldg(rx.wt + ek) : 1u;
+  }
+  D cur[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) cur[k] = dist_cg<D>(rx.cells, v[k]);
+  c.work += __popc(valid);
+  c.relax += __popc(valid);
+  bool ovf = false;
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const unsigned long long c64 = (unsigned long long)dn[k] + (unsigned long long)w[k];
+    const bool big = c64 >= (unsigned long long)DistTraits<D>::kInf;
+    cand[k] = (D)c64;
+    const bool vk = (valid >> k & 1u) != 0;
+    ovf |= vk && big;
+    want |= (unsigned)(vk && !big && cand[k] < cur[k]) << k;
+  }
+  if (ovf) atomicOr(rx.ovf, 1u);
+#else
 #pragma unroll
   for (int k = 0; k < K; ++k)
     if (valid >> k & 1u) {
@@ -89,7 +118,6 @@ __device__ __forceinline__ unsigned small_relax(const Relaxer<D, W>& rx, unsigne
 #pragma unroll
   for (int k = 0; k < K; ++k)
     if (valid >> k & 1u) cur[k] = dist_cg<D>(rx.cells, v[k]);
-  unsigned want = 0;
 #pragma unroll
   for (int k = 0; k < K; ++k)
     if (valid >> k & 1u) {
@@ -97,6 +125,7 @@ __device__ __forceinline__ unsigned small_relax(const Relaxer<D, W>& rx, unsigne
       ++c.relax;
       if (make_cand<D>(dn[k], w[k], cand[k], rx.ovf) && cand[k] < cur[k]) want |= 1u << k;
     }
+#endif
   unsigned won = 0, first = 0;
 #pragma unroll
   for (int k = 0; k < K; ++k)
