@@ -350,6 +350,7 @@ __device__ __forceinline__ void control_warp(DevCtrl* c, cudaGraphConditionalHan
         ctl_wd_fused_advance(c, wd_next, wd_zero);
       } else {
         ctl_simple_advance(c);
+        c->mode = kModeWD;  // a relax-only step on the cluster loop's item list pushed nodes
       }
       break;
     case GLB_HP:

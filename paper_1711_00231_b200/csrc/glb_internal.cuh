@@ -243,6 +243,7 @@ struct DevCtrl {
   void* wd_items_buf[2];        // WdItem lists (the step's input is [wd_cur])
   unsigned int* wd_tf_buf[2];   // tile_first of each list
   int wd_fused;                 // WD strategy outside sharded runs
+  int wd_fused_small;           // fused pushes inside the cluster loop only
   int wd_cur;
   unsigned long long wd_next;   // (items << 32) | edges appended to list [wd_cur ^ 1]
   unsigned int wd_zero_next;    // zero-degree nodes pushed (counted for the record only)

@@ -265,7 +265,7 @@ __global__ void __cluster_dims__(kSmallCtas, 1, 1) __launch_bounds__(kSmallThrea
     bool ran = true;
     SmallPush push;
     const SmallPush* fused = nullptr;
-    if (sc.wd_fused) {
+    if (sc.wd_fused || sc.wd_fused_small) {
       push.row = row;
       push.out = reinterpret_cast<WdItem*>(sc.wd_items_buf[sc.wd_cur ^ 1]);
       push.tf = sc.wd_tf_buf[sc.wd_cur ^ 1];
@@ -507,7 +507,7 @@ __global__ void __cluster_dims__(kSmallCtas, 1, 1) __launch_bounds__(kSmallThrea
           ctl_hp_after_step(cc);
         } else if (wd_empty) {
           cc->done = 1;
-        } else if (cc->wd_fused) {
+        } else if (cc->wd_fused || (cc->wd_fused_small && cc->strategy == GLB_WD)) {
           ctl_wd_fused_advance(cc, *(volatile unsigned long long*)(wdn0 + slot),
                                *(volatile unsigned*)(wdz0 + slot));
         } else {
