@@ -384,17 +384,18 @@ __global__ void __cluster_dims__(kSmallCtas, 1, 1) __launch_bounds__(kSmallThrea
         const uint32_t w = W ? __ldg(rx.wt + e) : 1u;
         ++c.work;
         const D du = dist_cg<D>(rx.cells, u);
+        const D dv = dist_cg<D>(rx.cells, v);  // in flight with du
         if (du == DistTraits<D>::kInf) continue;
         ++c.relax;
         D cand;
-        if (!make_cand<D>(du, w, cand, rx.ovf) || cand >= dist_cg<D>(rx.cells, v)) continue;
+        if (!make_cand<D>(du, w, cand, rx.ovf) || cand >= dv) continue;
+        const long long lo = row[v], hi = row[v + 1];  // the push's range, in flight with the atomic
         const CellS<D> old = atomicMin(rx.cells + v, Cell<D>::make(cand, rx.gen));
         if (cand >= Cell<D>::dist(old)) continue;
         const bool first = Cell<D>::kPacked ? Cell<D>::gen(old) != Cell<D>::tag(rx.gen)
                                             : atomicExch(rx.stamp + v, rx.gen) != rx.gen;
         if (!first) continue;
-        const long long lo = row[v];
-        const unsigned len = (unsigned)(row[v + 1] - lo);
+        const unsigned len = (unsigned)(hi - lo);
         if (len == 0) continue;
         if (ep_chunked) {
           ++c.push;
@@ -411,9 +412,9 @@ __global__ void __cluster_dims__(kSmallCtas, 1, 1) __launch_bounds__(kSmallThrea
       // ---- BS / NS: thread per worklist node (node i -> cluster thread i mod 8192)
       for (unsigned i = gt; i < n; i += kSmallAll) {
         const uint32_t u = __ldcg(qin + i);
+        const uint32_t lo = (uint32_t)row[u], hi = (uint32_t)row[u + 1];  // in flight with du
         const D du = dist_cg<D>(rx.cells, u);
         if (du == DistTraits<D>::kInf) continue;
-        const uint32_t lo = (uint32_t)row[u], hi = (uint32_t)row[u + 1];
         constexpr int K = 4;
         for (uint32_t b = lo; b < hi; b += K) {
           uint32_t e[K];
