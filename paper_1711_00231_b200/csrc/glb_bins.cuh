@@ -294,10 +294,11 @@ __global__ void __launch_bounds__(kBlock, GLB_BIN_MINB) k_hp_window(const long l
     if (i < n) {
       const uint32_t u = qin[i];
       const long long r0 = row[u], r1 = row[u + 1];
+      const D du = rx.dist(u);  // dn at window entry (hierarchical.py:108), in flight with the row
       const long long start = r0 + window;
       if (start < r1) {
         const long long end = start + mdt < r1 ? start + mdt : r1;
-        dn = rx.dist(u);  // dn at window entry (hierarchical.py:108)
+        dn = du;
         if (dn != DistTraits<D>::kInf) {
           lo = start;
           len = end - start;
@@ -342,10 +343,11 @@ __global__ void __launch_bounds__(kBlock, GLB_BIN_MINB) k_ns_relax(const long lo
     D dn = DistTraits<D>::kInf;
     if (i < n) {
       const uint32_t u = qin[i];
+      const long long r0 = row[u], r1 = row[u + 1];  // in flight with dn
       dn = rx.dist(u);
       if (dn != DistTraits<D>::kInf) {
-        lo = row[u];
-        len = row[u + 1] - lo;
+        lo = r0;
+        len = r1 - r0;
       }
     }
     warp_windows(rx, sink, lo, len, dn, mirror, ctrl, c);
