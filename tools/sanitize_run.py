@@ -62,4 +62,28 @@ for g in graphs[:3]:
     if not pkg.validate_distances(g, 0, "sssp", exp).matched:
         bad += 1
         print("CERTIFICATE rejected a correct array", g.num_nodes)
+# round 2: HP / NS CTA bin (TMA-staged pieces, piece -> window table) on a
+# hub-heavy graph, and the peer-memory sharded loop with virtual ranks
+from paper_1711_00231_b200 import sharded  # noqa: E402
+
+hub = pkg.generate_rmat(11 if QUICK else 13, 8, params=(0.7, 0.15, 0.10, 0.05), seed=1,
+                        max_weight=255)
+for algo in ("bfs", "sssp"):
+    exp = oracle.oracle_distances(hub, 0, algo)
+    for tag in ("HP", "NS", "WD"):
+        for mdt in (None, 600):  # 600: windows above the 512-edge CTA-bin threshold
+            r = pkg.run_strategy(tag, hub, 0, pkg.RelaxOp(algo), pkg.KernelConfig(loop="graph"),
+                                 mdt=mdt)
+            if not np.array_equal(r.dist.array, exp):
+                bad += 1
+                print("MISMATCH hub", algo, tag, mdt)
+for parts in ((2,) if QUICK else (2, 3)):
+    shards = [sharded.shard_graph(graphs[0], parts, r, 0) for r in range(parts)]
+    for algo in ("bfs", "sssp"):
+        exp = oracle.oracle_distances(graphs[0], 0, algo)
+        for tag in sharded.SHARD_TAGS:
+            d, _ = sharded.run_virtual_peer(tag, shards, 0, pkg.RelaxOp(algo))
+            if not np.array_equal(d, exp):
+                bad += 1
+                print("MISMATCH peer", parts, algo, tag)
 print("sanitize workload done, mismatches:", bad)
