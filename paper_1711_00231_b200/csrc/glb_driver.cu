@@ -151,6 +151,7 @@ class Runner {
         GLB_CUDA_TRY(cudaMemcpy(dist_out, out, (size_t)cnt * 8, cudaMemcpyDeviceToHost));
     }
     g_->ptw_len = ptw_ ? (long long)std::min<unsigned long long>(h_->ctrl.ptw_off, kPtwCap) : 0;
+    if (ptw_) g_->ptw_dirty = g_->ptw_len;
     g_->stamp_epoch = h_->ctrl.gen;
     g_->scan_epoch = h_->ctrl.scan_epoch;
     float dev_ms = 0;
@@ -278,8 +279,15 @@ class Runner {
     pin_cells_in_l2(nb * sizeof(CellS<D>));
     ptw_ = nullptr;
     if (p_.instrument) {  // per-thread work lists: zeroed once, atomically accumulated
+      // The list is accumulated with atomics, so it must start zeroed; only
+      // the prefix the previous instrumented run used is dirty (a fresh or
+      // recycled buffer is zeroed whole).
+      const void* before = ws.ptw.p;
       ptw_ = (uint32_t*)ensure(ws.ptw, (size_t)kPtwCap * 4);
-      GLB_CUDA_TRY(cudaMemsetAsync(ptw_, 0, (size_t)kPtwCap * 4, s_));
+      const long long dirty = (before != ws.ptw.p || g_->ptw_dirty < 0) ? (long long)kPtwCap
+                                                                         : g_->ptw_dirty;
+      if (dirty > 0) GLB_CUDA_TRY(cudaMemsetAsync(ptw_, 0, (size_t)dirty * 4, s_));
+      g_->ptw_dirty = -1;  // unknown until this run finishes
     }
     ctrl_ = (DevCtrl*)ensure(ws.ctrl, sizeof(DevCtrl));
     ls_ = (LaunchStats*)ensure_zero(ws.stats, sizeof(LaunchStats), s_);

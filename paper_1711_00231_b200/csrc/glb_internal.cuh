@@ -360,6 +360,7 @@ struct glb_graph {
   std::vector<cudaEvent_t> ev_pool;
   std::vector<glb_record> last_records;  // records of the most recent glb_run
   long long ptw_len = 0;                 // per-thread work slots of the most recent glb_run
+  long long ptw_dirty = -1;              // slots of the list buffer that may be nonzero (-1: all)
   glb::ShardSessionBase* shard = nullptr;                       // sharded run in progress
   std::mutex mu;              // drivers are not re-entrant (common.py:5-6)
 };
