@@ -49,7 +49,10 @@ constexpr unsigned kBinThreadMax = 32;   // thread bin: windows of at most 32 ed
 constexpr long long kBinCtaMin = GLB_BIN_CTA_MIN;  // CTA bin: windows of at least this many edges
 constexpr long long kBinPiece = 2048;    // edges per CTA-bin piece (one TMA stage)
 constexpr int kBinBuf = (int)kBinPiece + 4;  // a piece plus the 16-byte alignment slack
-constexpr int kBinK = 4;                 // edges in flight per lane
+#ifndef GLB_BIN_K
+#define GLB_BIN_K 4
+#endif
+constexpr int kBinK = GLB_BIN_K;         // edges in flight per lane
 
 // -------------------------------------------------------------- sinks ---
 // Warp-private push buffer in shared memory, flushed with one global
