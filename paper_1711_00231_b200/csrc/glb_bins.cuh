@@ -460,3 +460,69 @@ __global__ void __launch_bounds__(kBlock) k_bigbin(Relaxer<D, W> rx0, M mirror, 
 }
 
 }  // namespace glb
+
+namespace glb {
+// ====================================================== BS, warp sinks ===
+// Node-based relaxation (node_based.py:43-67), thread per worklist node and
+// all its out-edges, with pushes through a warp-private buffer instead of the
+// CTA queue: no CTA barrier between grid-stride rounds, so warps of a CTA
+// never wait for each other.  The batch loop runs to the warp's longest
+// node (what SIMT execution of the per-thread loop does anyway).
+template <typename D, bool W>
+__global__ void __launch_bounds__(kBlock) k_bs_warp(const long long* __restrict__ row,
+                                                    Relaxer<D, W> rx0, DevCtrl* ctrl,
+                                                    CtlTail tail) {
+  __shared__ uint32_t s_wq[kBinWarps][kBinWarpQ];
+  const unsigned n = ctrl->qcount[ctrl->in];
+  if (blockIdx.x * kBlock >= n) {  // idle CTA
+    ctl_tail(tail, ctrl);
+    return;
+  }
+  timer_begin(ctrl->t_relax);
+  const Relaxer<D, W> rx = bind(rx0, ctrl);
+  WarpSink sink{s_wq[threadIdx.x >> 5], 0u, rx.qout, rx.nout};
+  const uint32_t* __restrict__ qin = ctrl->qptr[ctrl->in];
+  ThreadCounters c;
+  constexpr int K = 4;
+  for (unsigned base = blockIdx.x * kBlock; base < n; base += gridDim.x * kBlock) {
+    const unsigned i = base + threadIdx.x;
+    long long lo = 0, hi = 0;
+    D du = DistTraits<D>::kInf;
+    if (i < n) {
+      const uint32_t u = qin[i];
+      du = rx.dist(u);
+      if (du != DistTraits<D>::kInf) {
+        lo = row[u];
+        hi = row[u + 1];
+      }
+    }
+    long long mx = hi - lo;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      const long long o = __shfl_xor_sync(0xffffffffu, mx, off);
+      mx = o > mx ? o : mx;
+    }
+    for (long long b = 0; b < mx; b += K) {
+      uint32_t v[K], w[K];
+      D d[K];
+      unsigned valid = 0;
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const long long e = lo + b + k;
+        const bool ok = e < hi;
+        valid |= (unsigned)ok << k;
+        const long long ek = ok ? e : 0ll;  // edge 0 is always mapped
+        v[k] = __ldg(rx.col + ek);
+        w[k] = W ? __ldg(rx.wt + ek) : 1u;
+        d[k] = du;
+      }
+      D cand[K];
+      relax_vals<K>(rx, sink, v, w, d, valid, c, cand);
+    }
+  }
+  sink.flush();
+  flush_counters(ctrl, c);
+  timer_end(ctrl->t_relax);
+  ctl_tail(tail, ctrl);
+}
+}  // namespace glb

@@ -190,6 +190,9 @@ class Runner {
   CtlTail tail_{0, {}, 0};
   bool fused_ctl_ = getenv("GLB_NO_FUSED_CTL") == nullptr;
   bool pdl_ = getenv("GLB_NO_PDL") == nullptr;
+  // BS pushes through warp buffers (k_bs_warp): C2 SSSP BS -10 %, BFS -17 %, but
+  // C3 SSSP +12 % (the CTA queue wins on degree-4 grids), so opt-in
+  bool bs_warp_ = getenv("GLB_BS_WARP") != nullptr;
   int unroll_ = getenv("GLB_GRAPH_UNROLL") ? std::max(1, std::min(kGraphUnroll, atoi(getenv("GLB_GRAPH_UNROLL"))))
                                            : kGraphUnroll;
   double setup_ms_ = 0;
@@ -217,7 +220,8 @@ class Runner {
 
   const void* relax_kernel() const {
     switch (p_.strategy) {
-      case GLB_BS: return (const void*)k_bs_relax<D, W>;
+      case GLB_BS:
+        return bs_warp_ ? (const void*)k_bs_warp<D, W> : (const void*)k_bs_relax<D, W>;
       case GLB_NS: return (const void*)k_ns_relax<D, W>;
       case GLB_EP:
         return p_.chunked ? (const void*)k_ep_relax<D, W, true> : (const void*)k_ep_relax<D, W, false>;
@@ -417,7 +421,12 @@ class Runner {
   void launch_relax(unsigned grid) {
     const Relaxer<D, W> rx = relaxer();
     switch (p_.strategy) {
-      case GLB_BS: k_bs_relax<D, W><<<grid, kBlock, 0, s_>>>(row_, rx, ctrl_, tail_); break;
+      case GLB_BS:
+        if (bs_warp_)
+          k_bs_warp<D, W><<<grid, kBlock, 0, s_>>>(row_, rx, ctrl_, tail_);
+        else
+          k_bs_relax<D, W><<<grid, kBlock, 0, s_>>>(row_, rx, ctrl_, tail_);
+        break;
       case GLB_NS:  // binned windows + the CTA bin of the long ones (TMA-staged)
         if (!bins_two()) {  // split nodes all shorter than a CTA-bin window: one kernel
           k_ns_relax<D, W><<<grid, kBlock, 0, s_>>>(row_, ns_mirror(), rx, ctrl_, tail_);
@@ -581,7 +590,7 @@ class Runner {
   // ----------------------------------------------------- graph loop ---
   std::string graph_key() const {
     std::ostringstream k;
-    k << g_->device << '|' << p_.strategy << '|' << fused_ctl_ << '|' << unroll_ << '|' << pdl_ << '|' << Cell<D>::kDistBits << '|' << W << '|' << p_.chunked << '|' << cap_relax_
+    k << g_->device << '|' << p_.strategy << '|' << bs_warp_ << '|' << fused_ctl_ << '|' << unroll_ << '|' << pdl_ << '|' << Cell<D>::kDistBits << '|' << W << '|' << p_.chunked << '|' << cap_relax_
       << '|' << cap_scan_ << '|' << cap_wd_ << '|' << cap_hp_ << '|' << cap_big_ << '|' << (const void*)row_ << '|'
       << (const void*)col_ << '|' << (const void*)wt_ << '|' << (const void*)cs_ << '|'
       << (const void*)src_ << '|' << (const void*)cells_ << '|' << (const void*)stamp_ << '|'

@@ -37,7 +37,9 @@ VARIANTS = {"default": {}, "grid_kernels": {"GLB_NO_SMALL": "1"},
             # graph-loop structure knobs: separate control kernel, one step per
             # WHILE iteration without programmatic dependent launch
             "grid_ctl_kernel": {"GLB_NO_SMALL": "1", "GLB_NO_FUSED_CTL": "1"},
-            "grid_unroll1_nopdl": {"GLB_NO_SMALL": "1", "GLB_GRAPH_UNROLL": "1", "GLB_NO_PDL": "1"}}
+            "grid_unroll1_nopdl": {"GLB_NO_SMALL": "1", "GLB_GRAPH_UNROLL": "1", "GLB_NO_PDL": "1"},
+            # BS with warp push buffers (k_bs_warp)
+            "grid_bs_warp": {"GLB_NO_SMALL": "1", "GLB_BS_WARP": "1"}}
 
 
 @pytest.mark.parametrize("variant", list(VARIANTS))
@@ -284,7 +286,7 @@ def test_records_and_counters():
     assert sd["EP"] < sd["BS"] and sd["WD"] < sd["BS"] and sd["NS"] < sd["BS"], sd
 
 
-@pytest.mark.parametrize("variant", ["grid_kernels", "wd_fused", "grid_dense"])
+@pytest.mark.parametrize("variant", ["grid_kernels", "wd_fused", "grid_dense", "grid_bs_warp"])
 def test_random_graphs_execution_variants(oracle, variant, monkeypatch):
     for k, v in VARIANTS[variant].items():
         monkeypatch.setenv(k, v)
