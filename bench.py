@@ -462,10 +462,11 @@ def ours_sharded(args, world, rank, local):
     host_narrow = None
     if rank == 0 and not args.no_cpu:
         host_narrow = g.download_narrow()
+    mdt = sharded.global_mdt(g)  # HP's window of the whole graph, before the cut
     _lib.check(_lib.lib().glb_graph_restrict(g.device_graph(), lo, hi), "glb_graph_restrict")
     m_own = int(row[hi] - row[lo])
     g.num_edges = m_own
-    sg = sharded.ShardGraph(g, bounds, rank, dev)
+    sg = sharded.ShardGraph(g, bounds, rank, dev, mdt=mdt)
     gen_s = time.time() - t0
     transport = sharded.DistTransport(torch) if args.transport == "torch" else "peer"
     cfg = pkg.KernelConfig(record_timing=True, instrument=False)
@@ -541,7 +542,7 @@ def ours_sharded(args, world, rank, local):
             _lib.check(_lib.lib().glb_graph_create(_lib.ptr64(hrow), _lib.ptr64(hcol), _lib.ptr64(hw),
                                                    g.num_nodes, m_own, dev, ctypes.byref(h)))
             dg = pkg.DeviceCsrGraph(h.value, g.num_nodes, m_own, True, dev)
-            sg2 = sharded.ShardGraph(dg, bounds, rank, dev)
+            sg2 = sharded.ShardGraph(dg, bounds, rank, dev, mdt=mdt)
             d2, _ = sharded.run_sharded(tag, sg2, 0, op, cfg,
                                         sharded.DistTransport(torch) if args.transport == "torch"
                                         else "peer")

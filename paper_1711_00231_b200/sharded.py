@@ -62,6 +62,7 @@ class ShardGraph:
     rank: int
     device: int
     peer: "PeerExchange | None" = None  # connected peer transport (cached by run_sharded)
+    mdt: int = 0  # HP's window of the WHOLE graph (0: each rank computes its own)
 
     @property
     def parts(self) -> int:
@@ -80,6 +81,15 @@ class ShardGraph:
         return self.graph.num_nodes
 
 
+def global_mdt(g, bins: int = 10) -> int:
+    """compute_mdt(build_histogram(g, bins)) of the full graph (degrees.py:45-76),
+    taken before a shard is restricted: every rank then runs HP with the
+    reference's window, not one derived from its own rows."""
+    from .analysis import build_histogram, compute_mdt
+
+    return compute_mdt(build_histogram(g, bins))
+
+
 def partition_bounds(g, parts: int) -> np.ndarray:
     """Edge-balanced contiguous vertex ranges of a device graph."""
     b = np.empty(parts + 1, dtype=np.int64)
@@ -96,12 +106,13 @@ def shard_rmat(scale: int, edge_factor: int, parts: int, rank: int, device: int,
     g = generate_rmat(scale, edge_factor, params=params, seed=seed, weighted=weighted,
                       max_weight=max_weight, device=device, download=False)
     bounds = partition_bounds(g, parts)
+    mdt = global_mdt(g)
     _lib.check(_lib.lib().glb_graph_restrict(g.device_graph(), int(bounds[rank]),
                                              int(bounds[rank + 1])), "glb_graph_restrict")
     m = ctypes.c_int64()
     _lib.check(_lib.lib().glb_graph_info(g.device_graph(), None, ctypes.byref(m), None, None))
     g.num_edges = int(m.value)
-    return ShardGraph(g, bounds, rank, device)
+    return ShardGraph(g, bounds, rank, device, mdt=mdt)
 
 
 def shard_graph(g, parts: int, rank: int, device: int) -> ShardGraph:
@@ -112,9 +123,10 @@ def shard_graph(g, parts: int, rank: int, device: int) -> ShardGraph:
                                            device, ctypes.byref(h)), "glb_graph_create")
     dg = DeviceCsrGraph(h.value, g.num_nodes, g.num_edges, g.weights is not None, device)
     bounds = partition_bounds(dg, parts)
+    mdt = global_mdt(dg)
     _lib.check(_lib.lib().glb_graph_restrict(h.value, int(bounds[rank]), int(bounds[rank + 1])),
                "glb_graph_restrict")
-    return ShardGraph(dg, bounds, rank, device)
+    return ShardGraph(dg, bounds, rank, device, mdt=mdt)
 
 
 def restrict_host(g, bounds: np.ndarray, rank: int):
@@ -132,16 +144,17 @@ def restrict_host(g, bounds: np.ndarray, rank: int):
     return np.ascontiguousarray(r, dtype=np.int64), col, w
 
 
-def shard_host_graph(g, bounds: np.ndarray, rank: int, device: int) -> ShardGraph:
+def shard_host_graph(g, bounds: np.ndarray, rank: int, device: int, mdt: int = 0) -> ShardGraph:
     """Upload only this rank's rows of a host CsrGraph (the sharded form of
-    glb_graph_create): 1/P of the edges cross PCIe on every rank."""
+    glb_graph_create): 1/P of the edges cross PCIe on every rank.  `mdt`: the
+    whole graph's HP window (global_mdt), 0 = per rank."""
     row, col, w = restrict_host(g, bounds, rank)
     h = ctypes.c_void_p()
     _lib.check(_lib.lib().glb_graph_create(_lib.ptr64(row), _lib.ptr64(col), _lib.ptr64(w),
                                            g.num_nodes, int(col.shape[0]), device, ctypes.byref(h)),
                "glb_graph_create")
     dg = DeviceCsrGraph(h.value, g.num_nodes, int(col.shape[0]), w is not None, device)
-    return ShardGraph(dg, np.asarray(bounds, dtype=np.int64), rank, device)
+    return ShardGraph(dg, np.asarray(bounds, dtype=np.int64), rank, device, mdt=mdt)
 
 
 # ----------------------------------------------------------------- backends
@@ -160,6 +173,7 @@ class CudaShard:
         p.algo = _lib.GLB_BFS if op.kind == "bfs" else _lib.GLB_SSSP
         p.source = source
         p.bins = 10
+        p.mdt = sg.mdt
         p.chunked = 1
         p.max_cells = 1 << 62
         p.block_size = cfg.block_size
@@ -245,7 +259,7 @@ class PeerExchange:
         """This rank's part of a sharded run: int64 distances of [lo, hi) and
         stats (run stats + exchange stats under ``"exchange"``)."""
         cfg = cfg or KernelConfig()
-        p = _shard_params(tag, source, op, cfg)
+        p = _shard_params(tag, source, op, cfg, self.sg.mdt)
         out = np.empty(self.sg.hi - self.sg.lo, dtype=np.int64)
         st = _lib.RunStats()
         xs = _lib.PeerStats()
@@ -265,7 +279,7 @@ class PeerExchange:
             pass
 
 
-def _shard_params(tag: str, source: int, op: RelaxOp, cfg: KernelConfig):
+def _shard_params(tag: str, source: int, op: RelaxOp, cfg: KernelConfig, mdt: int = 0):
     if tag.upper() not in SHARD_TAGS:
         raise ValueError(f"sharded runs support {SHARD_TAGS}, not {tag!r}")
     p = _lib.RunParams()
@@ -273,6 +287,7 @@ def _shard_params(tag: str, source: int, op: RelaxOp, cfg: KernelConfig):
     p.algo = _lib.GLB_BFS if op.kind == "bfs" else _lib.GLB_SSSP
     p.source = source
     p.bins = 10
+    p.mdt = mdt
     p.chunked = 1
     p.max_cells = 1 << 62
     p.block_size = cfg.block_size
@@ -301,7 +316,7 @@ def run_virtual_peer(tag: str, shards: list[ShardGraph], source: int, op: RelaxO
         peers = [PeerExchange(sg) for sg in shards]
         PeerExchange.connect_local(peers)
     parts = len(shards)
-    p = _shard_params(tag, source, op, cfg)
+    p = _shard_params(tag, source, op, cfg, shards[0].mdt)
     outs = [np.empty(sg.hi - sg.lo, dtype=np.int64) for sg in shards]
     arr = (ctypes.c_void_p * parts)(*[px.h for px in peers])
     dptr = (_lib._p64 * parts)(*[_lib.ptr64(o) for o in outs])

@@ -16,10 +16,11 @@ def main(out_dir: str) -> None:
     g = pkg.generate_rmat(14, 8, seed=3, max_weight=255, device=0, download=False)
     exp = {a: pkg.run_wd(g, 0, pkg.RelaxOp(a), pkg.KernelConfig()).dist.array for a in ("bfs", "sssp")}
     bounds = sharded.partition_bounds(g, world)
+    mdt = sharded.global_mdt(g)
     from paper_1711_00231_b200 import _lib
     _lib.check(_lib.lib().glb_graph_restrict(g.device_graph(), int(bounds[rank]),
                                              int(bounds[rank + 1])))
-    sg = sharded.ShardGraph(g, bounds, rank, 0)
+    sg = sharded.ShardGraph(g, bounds, rank, 0, mdt=mdt)
     res = []
     for algo in ("bfs", "sssp"):
         for tag in sharded.SHARD_TAGS:

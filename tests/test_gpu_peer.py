@@ -36,8 +36,10 @@ def need_gpu():
 def test_peer_virtual_ranks_match_golden(golden):
     for gid in ("rmat10_s1", "rmat10_skew", "grid24", "quirks", "rmat12_s4", "degrees"):
         g = gs.build(pkg, gs.CORPUS[gid])
+        full_mdt = pkg.compute_mdt(pkg.build_histogram(g, 10))
         for parts in (1, 2, 3, 5):
             shards = [sharded.shard_graph(g, parts, r, 0) for r in range(parts)]
+            assert all(sg.mdt == full_mdt for sg in shards)
             for algo in ("bfs", "sssp"):
                 exp = golden["corpus"][f"{gid}|0|{algo}"]
                 for tag in sharded.SHARD_TAGS:
@@ -48,6 +50,8 @@ def test_peer_virtual_ranks_match_golden(golden):
                     sent = sum(s["exchange"]["sent_entries"] for s in st)
                     recv = sum(s["exchange"]["recv_entries"] for s in st)
                     assert sent == recv, (sent, recv)
+                    if tag == "HP":  # every rank windows by the whole graph's MDT
+                        assert {s["mdt"] for s in st} == {shards[0].mdt}, (gid, parts)
 
 
 def test_peer_and_torch_transports_agree_on_rmat():

@@ -18,8 +18,9 @@ if rank == 0 and "ref" in sys.argv:
     ref = pkg.run_strategy("WD", g, 0, pkg.RelaxOp("sssp"), pkg.KernelConfig(instrument=False)).dist.array
     log("ref done")
 bounds = sharded.partition_bounds(g, world)
+mdt = sharded.global_mdt(g)
 _lib.check(_lib.lib().glb_graph_restrict(g.device_graph(), int(bounds[rank]), int(bounds[rank + 1])))
-sg = sharded.ShardGraph(g, bounds, rank, 0)
+sg = sharded.ShardGraph(g, bounds, rank, 0, mdt=mdt)
 px = sharded.PeerExchange.over(sg)
 log("connected")
 for algo in ("bfs", "sssp"):
