@@ -138,3 +138,29 @@ def test_peer_two_processes_over_cuda_ipc(tmp_path):
     assert rcs == [0, 0], rcs
     res = (tmp_path / "result.txt").read_text().split()
     assert res == ["ok"] * 6, res
+
+
+def test_peer_missing_rank_times_out_instead_of_hanging(monkeypatch):
+    """Rank 0 runs, rank 1 never does: rank 0's mailbox poll gives up after
+    GLB_PEER_TIMEOUT_S, the call fails with DeviceError, the peer refuses
+    further runs (lockstep lost) and the GPU stays usable."""
+    import time
+
+    monkeypatch.setenv("GLB_PEER_TIMEOUT_S", "2")
+    g = pkg.generate_rmat(10, 8, seed=1, max_weight=255)
+    shards = [sharded.shard_graph(g, 2, r, 0) for r in range(2)]
+    peers = [sharded.PeerExchange(sg) for sg in shards]
+    sharded.PeerExchange.connect_local(peers)
+    t0 = time.time()
+    with pytest.raises(_lib.DeviceError, match="did not publish"):
+        peers[0].run("WD", 0, pkg.RelaxOp("bfs"))
+    assert time.time() - t0 < 60
+    with pytest.raises(_lib.DeviceError, match="lockstep"):
+        peers[0].run("WD", 0, pkg.RelaxOp("bfs"))
+    for p in peers:
+        p.close()
+    # the device is healthy: a fresh run on the same GPU is bit-exact
+    r = pkg.run_wd(g, 0, pkg.RelaxOp("bfs"), pkg.KernelConfig())
+    h = pkg.generate_rmat(10, 8, seed=1, max_weight=255)
+    exp = pkg.run_bs(h, 0, pkg.RelaxOp("bfs"), pkg.KernelConfig()).dist.array
+    assert np.array_equal(r.dist.array, exp)
