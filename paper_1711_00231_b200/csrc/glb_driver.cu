@@ -29,6 +29,9 @@
 #include "glb_scan.cuh"
 #include "glb_small.cuh"
 #include "glb_peer.cuh"
+#ifdef GLB_EXP_SORT
+#include <cub/device/device_radix_sort.cuh>
+#endif
 
 namespace glb {
 
@@ -40,6 +43,7 @@ void histogram(glb_graph* g, const long long* row, long long n, unsigned long lo
 namespace {
 
 constexpr unsigned kMaxRecords = 1u << 16;
+constexpr unsigned kBmThrDefault = 32768;  // BS lists rebuilt in id order from this size
 constexpr unsigned long long kPtwCap = 1ull << 27;  // per-thread work slots of one run (512 MB)
 
 // a narrow candidate reached INF: re-run at the next distance tier.  Derived
@@ -144,6 +148,7 @@ class Runner {
     GLB_CUDA_TRY(cudaStreamSynchronize(s_));
     if (p_.loop_mode == GLB_LOOP_GRAPH) count_launches(h_->ctrl.kernels);
     if (h_->ctrl.overflow) throw OverflowRestart{};
+    if (h_->ctrl.bm_err) throw Error{GLB_ECUDA, "BS frontier bitmap out of step with its worklist"};
     if (cnt > 0 && dist_out) {
       if (kNarrow)
         download_dist_u32(s_, (const uint32_t*)out, cnt, dist_out);
@@ -193,6 +198,37 @@ class Runner {
   // BS pushes through warp buffers (k_bs_warp): C2 SSSP BS -10 %, BFS -17 %, but
   // C3 SSSP +12 % (the CTA queue wins on degree-4 grids), so opt-in
   bool bs_warp_ = getenv("GLB_BS_WARP") != nullptr;
+  // BS id-ordered frontiers (k_bm_compact) for relax steps of >= bm_thr_
+  // nodes (and >= 1/256 of the graph); GLB_BM_THR=t sets the threshold to t
+  // exactly, GLB_BM_THR=0 turns them off
+  unsigned bm_thr_ = getenv("GLB_BM_THR") ? (unsigned)atoll(getenv("GLB_BM_THR")) : kBmThrDefault;
+  uint32_t* bm_[2] = {nullptr, nullptr};
+  long long bm_vec_ = 0;
+  bool bm_on() const { return p_.strategy == GLB_BS && !bs_warp_ && !shard_mode_ && bm_thr_ > 0; }
+#ifdef GLB_EXP_SORT
+  long long sort_thr_ = getenv("GLB_SORT_THR") ? atoll(getenv("GLB_SORT_THR")) : 0;
+  uint32_t* sort_buf_ = nullptr;
+  void* sort_tmp_ = nullptr;
+  size_t sort_tmp_n_ = 0;
+  long long sort_cap_ = 0;
+  // experiment: sort the in-list (host loop only) before a relax step
+  void exp_sort(long long n_in, int bits) {
+    if (!sort_thr_ || n_in < sort_thr_) return;
+    uint32_t* q = h_->ctrl.qptr[h_->ctrl.in];
+    if (n_in > sort_cap_) {
+      if (sort_buf_) cudaFree(sort_buf_);
+      if (sort_tmp_) cudaFree(sort_tmp_);
+      sort_cap_ = n_in * 2;
+      GLB_CUDA_TRY(cudaMalloc(&sort_buf_, sort_cap_ * 4));
+      sort_tmp_n_ = 0;
+      cub::DeviceRadixSort::SortKeys(nullptr, sort_tmp_n_, q, sort_buf_, (int)sort_cap_, 0, bits, s_);
+      GLB_CUDA_TRY(cudaMalloc(&sort_tmp_, sort_tmp_n_));
+    }
+    size_t t = sort_tmp_n_;
+    GLB_CUDA_TRY(cub::DeviceRadixSort::SortKeys(sort_tmp_, t, q, sort_buf_, (int)n_in, 0, bits, s_));
+    GLB_CUDA_TRY(cudaMemcpyAsync(q, sort_buf_, n_in * 4, cudaMemcpyDeviceToDevice, s_));
+  }
+#endif
   int unroll_ = getenv("GLB_GRAPH_UNROLL") ? std::max(1, std::min(kGraphUnroll, atoi(getenv("GLB_GRAPH_UNROLL"))))
                                            : kGraphUnroll;
   double setup_ms_ = 0;
@@ -246,6 +282,14 @@ class Runner {
     } else {
       for (int i = 0; i < 4; ++i)
         q_[i] = (i < 2 || p_.strategy == GLB_HP) ? (uint32_t*)ensure(ws.q[i], nb * 4) : q_[1];
+    }
+    bm_[0] = bm_[1] = nullptr;
+    if (bm_on()) {  // two member bitmaps, 16-byte vectors, zeroed per run
+      bm_vec_ = ((long long)nb + 127) / 128;  // words / 4 (16-byte aligned halves)
+      char* b = (char*)ensure(ws.bm, (size_t)bm_vec_ * 32);
+      GLB_CUDA_TRY(cudaMemsetAsync(b, 0, (size_t)bm_vec_ * 32, s_));
+      bm_[0] = (uint32_t*)b;
+      bm_[1] = (uint32_t*)(b + (size_t)bm_vec_ * 16);
     }
     if (p_.strategy == GLB_WD || p_.strategy == GLB_HP) {
       items_[0] = (WdItem*)ensure(ws.wd_items[0], nb * sizeof(WdItem));
@@ -338,6 +382,14 @@ class Runner {
     // 117 -> 96 ms); grid steps keep scan + relax.
     c.wd_fused_small = p_.strategy == GLB_WD && !shard_mode_ && !c.wd_fused &&
                        !getenv("GLB_NO_WD_FUSED_SMALL") ? 1 : 0;
+    c.bm[0] = bm_[0];
+    c.bm[1] = bm_[1];
+    // a compaction reads the whole bitmap (n/8 bytes): worth it once the list
+    // holds >= 1/256 of the nodes (C3 SSSP: 65,536 of 16.8M) and >= 32K of them
+    c.bm_thr = !bm_on() ? 0u
+               : getenv("GLB_BM_THR") ? bm_thr_
+                                      : (unsigned)std::max<long long>(bm_thr_, n_all_ / 256);
+    c.bm_valid[0] = 1;  // the seed list's bit is set after the seed kernel
     c.recs = drecs_;
     c.ls = ls_;
     c.ptw = ptw_;
@@ -372,6 +424,8 @@ class Runner {
     k_seed<D><<<grid_for(std::max<long long>(seeds, 1), kBlock, g_->num_sms * 4), kBlock, 0, s_>>>(
         cells_, q_[0], &ctrl_->qcount[0], src, klo, khi, elo, ehi, edges);
     GLB_CHECK_LAUNCH();
+    if (bm_[0])  // the seed list's member bit
+      GLB_CUDA_TRY(cudaMemsetAsync((char*)bm_[0] + (src >> 3), 1 << (src & 7), 1, s_));
   }
 
   // Keep the distance cells -- the randomly accessed array -- resident in L2
@@ -422,10 +476,16 @@ class Runner {
     const Relaxer<D, W> rx = relaxer();
     switch (p_.strategy) {
       case GLB_BS:
-        if (bs_warp_)
+        if (bs_warp_) {
           k_bs_warp<D, W><<<grid, kBlock, 0, s_>>>(row_, rx, ctrl_, tail_);
-        else
-          k_bs_relax<D, W><<<grid, kBlock, 0, s_>>>(row_, rx, ctrl_, tail_);
+          break;
+        }
+        if (bm_[0]) {  // id-ordered in-list (no-op below the threshold)
+          k_bm_compact<<<grid_for(bm_vec_ * 4, kBmBlock, g_->num_sms * 8), kBmBlock, 0, s_>>>(ctrl_,
+                                                                                          bm_vec_ * 4);
+          GLB_CHECK_LAUNCH();
+        }
+        k_bs_relax<D, W><<<grid, kBlock, 0, s_>>>(row_, rx, ctrl_, tail_);
         break;
       case GLB_NS:  // binned windows + the CTA bin of the long ones (TMA-staged)
         if (!bins_two()) {  // split nodes all shorter than a CTA-bin window: one kernel
@@ -536,6 +596,13 @@ class Runner {
           const unsigned grid = p_.strategy == GLB_NS ? (unsigned)cap_relax_  // as HP windows
                                                       : grid_for(n_in, (int)per, cap_relax_);
           ev.threads = (long long)grid * kBlock;
+#ifdef GLB_EXP_SORT
+          {
+            int bits = 1;
+            while ((1ll << bits) < n_all_) ++bits;
+            exp_sort(n_in, bits);
+          }
+#endif
           if (timing) GLB_CUDA_TRY(cudaEventRecord(ev.k0, s_));
           launch_relax(grid);
           if (timing) GLB_CUDA_TRY(cudaEventRecord(ev.k1, s_));
@@ -597,7 +664,7 @@ class Runner {
       << (const void*)ctrl_ << '|' << (const void*)items_[0] << '|' << (const void*)items_[1] << '|'
       << (const void*)tile_first_[0] << '|' << (const void*)tile_first_[1] << '|'
       << (const void*)lb_.flags << '|' << (const void*)lb_.aggs << '|' << g_->n << '|' << n_all_
-      << '|' << mdt_ << '|' << resume_graph_;
+      << '|' << mdt_ << '|' << resume_graph_ << '|' << (const void*)bm_[0] << '|' << bm_vec_;
     return k.str();
   }
 

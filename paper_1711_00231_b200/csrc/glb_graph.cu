@@ -955,16 +955,9 @@ int glb_graph_destroy(glb_graph* g) {
   glb::dfree(g->col);
   glb::dfree(g->wt);
   glb::Workspace& ws = g->ws;
-  glb::DevBuf* bufs[] = {&ws.dist,   &ws.stamp,  &ws.q[0],     &ws.q[1],    &ws.q[2],
-                         &ws.q[3],   &ws.wd_items[0], &ws.wd_items[1], &ws.wd_tiles[0],
-                         &ws.wd_tiles[1], &ws.scan_flags, &ws.scan_vals, &ws.stats, &ws.ctrl,
-                         &ws.ns_row, &ws.ns_col, &ws.ns_w,   &ws.ns_parent, &ws.ns_cs,  &ws.ns_tmp,
-                         &ws.ep_src, &ws.eq[0],  &ws.eq[1],    &ws.out64,   &ws.misc,
-                         &ws.recs,   &ws.hist,   &ws.tile_node, &ws.misc_small,
-                         &ws.shard_tmp, &ws.hp_big};
   delete g->shard;
   g->shard = nullptr;
-  for (auto* b : bufs) glb::free_buf(*b);
+  ws.each([](glb::DevBuf& b) { glb::free_buf(b); });
   for (auto e : g->ev_pool) cudaEventDestroy(e);
   if (g->ev[0]) cudaEventDestroy(g->ev[0]);
   if (g->ev[1]) cudaEventDestroy(g->ev[1]);

@@ -10,6 +10,8 @@
 //   queue: uint32[n]    node worklists (capacity n is overflow-free with dedup)
 #pragma once
 
+#include <initializer_list>
+
 #include <cuda_runtime.h>
 #include <nvtx3/nvToolsExt.h>
 #include <stdint.h>
@@ -275,6 +277,16 @@ struct DevCtrl {
   // thread t of the launch recorded next adds its work to ptw[ptw_off + t]
   uint32_t* ptw;                // null: summed counters only
   unsigned long long ptw_off, ptw_cap;
+  // ---- BS id-ordered frontiers: bm[i] holds one bit per node of list i's
+  // members; a relax step over >= bm_thr nodes first rebuilds its list in id
+  // order from the bitmap (k_bm_compact), so the row / column / weight /
+  // cell accesses of neighbouring lanes fall on shared sectors
+  uint32_t* bm[2];
+  unsigned int bm_thr;          // 0: off
+  unsigned int bm_ctr;          // compaction cursor (zeroed by the relax step after it)
+  unsigned int bm_err;          // a compaction produced a list of another length
+  unsigned int bm_pad;
+  int bm_valid[2];              // bm[i] holds exactly list i's members (else it is all zero)
 };
 
 // --------------------------------------------------------- device graph ---
@@ -299,7 +311,18 @@ struct Workspace {
   DevBuf misc_small, shard_tmp;              // sharded-run counters / local split
   DevBuf hp_big;                             // HP CTA-bin entries
   DevBuf ptw;                                // per-thread work lists (instrumented runs)
+  DevBuf bm;                                 // BS frontier bitmaps (two lists)
+  // every buffer above (glb_graph_destroy frees them all)
+  template <class F>
+  void each(F f) {
+    for (DevBuf* b : {&dist, &stamp, &q[0], &q[1], &q[2], &q[3], &wd_items[0], &wd_items[1],
+                      &wd_tiles[0], &wd_tiles[1], &scan_flags, &scan_vals, &stats, &ctrl, &ns_row,
+                      &ns_col, &ns_w, &ns_parent, &ns_cs, &ns_tmp, &ep_src, &eq[0], &eq[1], &out64,
+                      &recs, &misc, &hist, &tile_node, &misc_small, &shard_tmp, &hp_big, &ptw, &bm})
+      f(*b);
+  }
 };
+static_assert(sizeof(Workspace) == 33 * sizeof(DevBuf), "Workspace::each must list every buffer");
 
 }  // namespace glb
 

@@ -61,13 +61,19 @@ namespace glb {
 constexpr int kQCap = 2048;
 struct BlockQ {          // control words; the items live in a separate smem array
   uint32_t* items;       // kQCap entries
+  uint32_t* bm;          // BS: the out list's member bitmap (null: none)
   unsigned int count;
   unsigned int base;
 };
 
-__device__ __forceinline__ void bq_init(BlockQ& q, uint32_t* items) {
+__device__ __forceinline__ void bm_set(uint32_t* bm, uint32_t v) {
+  atomicOr(bm + (v >> 5), 1u << (v & 31u));
+}
+
+__device__ __forceinline__ void bq_init(BlockQ& q, uint32_t* items, uint32_t* bm = nullptr) {
   if (threadIdx.x == 0) {
     q.items = items;
+    q.bm = bm;
     q.count = 0;
   }
   __syncthreads();
@@ -83,10 +89,12 @@ __device__ __forceinline__ void bq_push(BlockQ& q, uint32_t* qout, unsigned int*
   unsigned base = 0;
   if (lane_id() == leader) base = atomicAdd(&q.count, (unsigned)__popc(mask));
   base = __shfl_sync(mask, base, leader) + rank;
-  if (base < (unsigned)kQCap)
+  if (base < (unsigned)kQCap) {
     q.items[base] = v;
-  else
+  } else {
     qout[atomicAdd(nout, 1u)] = v;
+    if (q.bm) bm_set(q.bm, v);
+  }
 }
 
 // All threads of the CTA: one global reservation, coalesced copy-out.
@@ -97,7 +105,12 @@ __device__ __forceinline__ void bq_flush(BlockQ& q, uint32_t* qout, unsigned int
   __syncthreads();
   const unsigned b = q.base;
   const uint32_t* items = q.items;
-  for (unsigned i = threadIdx.x; i < n; i += blockDim.x) qout[b + i] = items[i];
+  uint32_t* bm = q.bm;
+  for (unsigned i = threadIdx.x; i < n; i += blockDim.x) {
+    const uint32_t v = items[i];
+    qout[b + i] = v;
+    if (bm) bm_set(bm, v);
+  }
   __syncthreads();
   if (threadIdx.x == 0) q.count = 0;
   __syncthreads();
@@ -378,12 +391,22 @@ __global__ void __launch_bounds__(kBlock) k_bs_relax(const long long* __restrict
   __shared__ uint32_t s_q[kQCap];
   __shared__ BlockQ bq;
   const unsigned n = ctrl->qcount[ctrl->in];
+  // id-ordered frontiers: a list k_bm_compact did not rebuild clears its
+  // members' bitmap words here (this step sets bits in the other bitmap)
+  const unsigned bm_thr = ctrl->bm_thr;
+  const bool bm_in = bm_thr && ctrl->bm_valid[ctrl->in];
+  uint32_t* bm_clear = bm_in && n < bm_thr ? ctrl->bm[ctrl->in] : nullptr;
+  if (bm_thr && blockIdx.x == 0 && threadIdx.x == 0) {
+    if (bm_in && n >= bm_thr && ctrl->bm_ctr != n) ctrl->bm_err = 1;
+    ctrl->bm_ctr = 0;  // k_bm_compact of the next step starts from 0
+    ctrl->bm_valid[ctrl->out] = 1;  // this step sets the out list's bits
+  }
   if (blockIdx.x * kBlock >= n) {  // idle CTA: no barriers, no atomics
     ctl_tail(tail, ctrl);
     return;
   }
   timer_begin(ctrl->t_relax);
-  bq_init(bq, s_q);
+  bq_init(bq, s_q, bm_thr ? ctrl->bm[ctrl->out] : nullptr);
   const Relaxer<D, W> rx = bind(rx0, ctrl);
   const uint32_t* __restrict__ qin = ctrl->qptr[ctrl->in];
   ThreadCounters c;
@@ -391,6 +414,7 @@ __global__ void __launch_bounds__(kBlock) k_bs_relax(const long long* __restrict
     const unsigned i = base + threadIdx.x;
     if (i < n) {
       const uint32_t u = qin[i];
+      if (bm_clear) bm_clear[u >> 5] = 0u;
       const D du = rx.dist(u);
       if (du != DistTraits<D>::kInf) relax_range_thread<4>(rx, bq, row[u], row[u + 1], du, c);
     }
@@ -399,6 +423,45 @@ __global__ void __launch_bounds__(kBlock) k_bs_relax(const long long* __restrict
   flush_counters(ctrl, c);
   timer_end(ctrl->t_relax);
   ctl_tail(tail, ctrl);
+}
+
+// BS id-ordered frontier: rebuild the in-list from its member bitmap when it
+// holds >= bm_thr nodes (the same set and length; node_based.py:43-67 takes
+// the worklist in any order).  Each CTA turns 256 consecutive bitmap words
+// into ids with one CTA scan, stages them in shared memory and copies them
+// out coalesced behind one global reservation, so the list is in id order
+// inside every 8K-node chunk; the words are zeroed as
+// they are read.  Pushes arrive in warp/CTA-queue order, which on a
+// low-degree graph (C3) scatters a lane's row / column / weight / cell
+// accesses over separate sectors; in id order they share them.
+constexpr int kBmBlock = 256;
+__global__ void __launch_bounds__(kBmBlock) k_bm_compact(DevCtrl* ctrl, long long nwords) {
+  const unsigned n = ctrl->qcount[ctrl->in];
+  // below the threshold the relax kernel clears the words instead; a list
+  // the cluster loop produced has no bits (it is taken in push order)
+  if (n < ctrl->bm_thr || !ctrl->bm_valid[ctrl->in]) return;
+  using Scan = cub::BlockScan<unsigned, kBmBlock>;
+  __shared__ typename Scan::TempStorage ts;
+  __shared__ uint32_t s_ids[kBmBlock * 32];  // the chunk's ids, copied out coalesced
+  __shared__ unsigned s_base;
+  uint32_t* __restrict__ bm = ctrl->bm[ctrl->in];
+  uint32_t* __restrict__ q = ctrl->qptr[ctrl->in];
+  for (long long b = (long long)blockIdx.x * kBmBlock; b < nwords; b += (long long)gridDim.x * kBmBlock) {
+    const long long i = b + threadIdx.x;
+    const uint32_t w = i < nwords ? bm[i] : 0u;
+    unsigned ex, total;
+    Scan(ts).ExclusiveSum((unsigned)__popc(w), ex, total);
+    if (total) {  // CTA-uniform
+      if (threadIdx.x == 0) s_base = atomicAdd(&ctrl->bm_ctr, total);
+      const uint32_t id0 = (uint32_t)(i * 32);
+      for (uint32_t x = w; x; x &= x - 1u) s_ids[ex++] = id0 + (uint32_t)(__ffs(x) - 1);
+      if (w) bm[i] = 0u;
+      __syncthreads();
+      const unsigned base = s_base;
+      for (unsigned j = threadIdx.x; j < total; j += kBmBlock) q[base + j] = s_ids[j];
+    }
+    __syncthreads();  // scan storage / s_ids / s_base reuse
+  }
 }
 
 // ============================================================ EP (K2) ===

@@ -38,6 +38,9 @@ namespace cg = cooperative_groups;
 #ifndef GLB_SMALL_CTAS
 #define GLB_SMALL_CTAS 8
 #endif
+#ifndef GLB_SMALL_PRECHECK
+#define GLB_SMALL_PRECHECK 1  // plain-load filter before the atomic inside the cluster loop
+#endif
 #ifndef GLB_SMALL_BRANCHLESS
 #define GLB_SMALL_BRANCHLESS 1  // small_relax without divergent regions (C3 BFS BS 79.5 -> 75.1 ms)
 #endif
@@ -93,7 +96,7 @@ __device__ __forceinline__ unsigned small_relax(const Relaxer<D, W>& rx, unsigne
   }
   D cur[K];
 #pragma unroll
-  for (int k = 0; k < K; ++k) cur[k] = dist_cg<D>(rx.cells, v[k]);
+  for (int k = 0; k < K; ++k) cur[k] = GLB_SMALL_PRECHECK ? dist_cg<D>(rx.cells, v[k]) : DistTraits<D>::kInf;
   c.work += __popc(valid);
   c.relax += __popc(valid);
   bool ovf = false;
@@ -251,6 +254,9 @@ __global__ void __cluster_dims__(kSmallCtas, 1, 1) __launch_bounds__(kSmallThrea
     for (int k = 0; k < 4; ++k) s_acc[tid][k] = 0;
   }
   cluster.sync();
+#ifdef GLB_SMALL_TRACE
+  unsigned long long tr[4] = {0, 0, 0, 0}, tr_n = 0, tr_t = gtime();
+#endif
   for (unsigned it = 0; s_go; ++it) {
     const unsigned slot = it % 3u;
     const unsigned n = sc.qcount[sc.in];
@@ -410,8 +416,13 @@ __global__ void __cluster_dims__(kSmallCtas, 1, 1) __launch_bounds__(kSmallThrea
       }
     } else {
       // ---- BS / NS: thread per worklist node (node i -> cluster thread i mod 8192)
+      // BS id-ordered frontiers: the list a grid step handed over has its
+      // bits set -- clear them; the cluster's own lists carry no bits
+      // (bm_valid is dropped on exit), so its pushes stay off the bitmap
+      uint32_t* bm_in = it == 0 && sc.bm_thr && !cs && sc.bm_valid[sc.in] ? sc.bm[sc.in] : nullptr;
       for (unsigned i = gt; i < n; i += kSmallAll) {
         const uint32_t u = __ldcg(qin + i);
+        if (bm_in) bm_in[u >> 5] = 0u;
         const uint32_t lo = (uint32_t)row[u], hi = (uint32_t)row[u + 1];  // in flight with du
         const D du = dist_cg<D>(rx.cells, u);
         if (du == DistTraits<D>::kInf) continue;
@@ -449,6 +460,9 @@ __global__ void __cluster_dims__(kSmallCtas, 1, 1) __launch_bounds__(kSmallThrea
         }
       }
     }
+#ifdef GLB_SMALL_TRACE
+    if (tid == 0) { const unsigned long long t = gtime(); tr[0] += t - tr_t; tr_t = t; }
+#endif
     // ---- counters of the iteration meet in CTA 0 (distributed shared memory)
     if (ran && sc.ptw && c.work && sc.ptw_off + gt < sc.ptw_cap)
       sc.ptw[sc.ptw_off + gt] = c.work > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)c.work;
@@ -472,7 +486,13 @@ __global__ void __cluster_dims__(kSmallCtas, 1, 1) __launch_bounds__(kSmallThrea
         if (mx) atomicMax(max0 + slot, mx > 0xFFFFFFFFull ? 0xFFFFFFFFu : (unsigned)mx);
       }
     }
+#ifdef GLB_SMALL_TRACE
+    if (tid == 0) { const unsigned long long t = gtime(); tr[1] += t - tr_t; tr_t = t; }
+#endif
     cluster.sync();  // every push and counter of the iteration has landed
+#ifdef GLB_SMALL_TRACE
+    if (tid == 0) { const unsigned long long t = gtime(); tr[2] += t - tr_t; tr_t = t; }
+#endif
     if (tid == 0) {
       DevCtrl* cc = &sc;
       if (!ran) {
@@ -530,12 +550,21 @@ __global__ void __cluster_dims__(kSmallCtas, 1, 1) __launch_bounds__(kSmallThrea
       }
     }
     __syncthreads();  // this CTA's threads see the transition (identical in every CTA)
+#ifdef GLB_SMALL_TRACE
+    if (tid == 0) { const unsigned long long t = gtime(); tr[3] += t - tr_t; tr_t = t; ++tr_n; }
+#endif
   }
   cluster.sync();  // no CTA leaves while others may still read its shared memory
+#ifdef GLB_SMALL_TRACE
+  if (rank == 0 && tid == 0 && tr_n)
+    printf("small_loop trace: %llu iters  relax %.2f  counters %.2f  barrier %.2f  control %.2f us/iter\n",
+           tr_n, tr[0] / 1e3 / tr_n, tr[1] / 1e3 / tr_n, tr[2] / 1e3 / tr_n, tr[3] / 1e3 / tr_n);
+#endif
   if (rank == 0 && tid == 0) {
     sc.overflow |= __ldcg(&gctrl->overflow);  // make_cand's flag lives in the global block
     sc.small_exit = 1;
     sc.use_small = 0;
+    sc.bm_valid[0] = sc.bm_valid[1] = 0;  // both bitmaps are zero now
     ctl_reset_timers(&sc);
     *gctrl = sc;
   }

@@ -39,7 +39,12 @@ VARIANTS = {"default": {}, "grid_kernels": {"GLB_NO_SMALL": "1"},
             "grid_ctl_kernel": {"GLB_NO_SMALL": "1", "GLB_NO_FUSED_CTL": "1"},
             "grid_unroll1_nopdl": {"GLB_NO_SMALL": "1", "GLB_GRAPH_UNROLL": "1", "GLB_NO_PDL": "1"},
             # BS with warp push buffers (k_bs_warp)
-            "grid_bs_warp": {"GLB_NO_SMALL": "1", "GLB_BS_WARP": "1"}}
+            "grid_bs_warp": {"GLB_NO_SMALL": "1", "GLB_BS_WARP": "1"},
+            # BS id-ordered frontiers on every step (k_bm_compact rebuilds each
+            # list from its bitmap), alone and alternating with the cluster loop
+            "grid_bm_every_step": {"GLB_NO_SMALL": "1", "GLB_BM_THR": "1"},
+            "bm_every_step": {"GLB_BM_THR": "1"},
+            "grid_bm_off": {"GLB_NO_SMALL": "1", "GLB_BM_THR": "0"}}
 
 
 @pytest.mark.parametrize("variant", list(VARIANTS))
@@ -286,7 +291,8 @@ def test_records_and_counters():
     assert sd["EP"] < sd["BS"] and sd["WD"] < sd["BS"] and sd["NS"] < sd["BS"], sd
 
 
-@pytest.mark.parametrize("variant", ["grid_kernels", "wd_fused", "grid_dense", "grid_bs_warp"])
+@pytest.mark.parametrize("variant", ["grid_kernels", "wd_fused", "grid_dense", "grid_bs_warp",
+                                     "grid_bm_every_step"])
 def test_random_graphs_execution_variants(oracle, variant, monkeypatch):
     for k, v in VARIANTS[variant].items():
         monkeypatch.setenv(k, v)
@@ -408,3 +414,19 @@ def test_high_diameter_grid_all_strategies(oracle):
                 assert np.array_equal(r.dist.array, exp), (algo, tag, loop)
             r = pkg.run_strategy(tag, g, 1000, pkg.RelaxOp(algo), pkg.KernelConfig(loop="graph"))
             assert np.array_equal(r.dist.array, oracle.oracle_distances(g, 1000, algo)), (algo, tag)
+
+
+@pytest.mark.parametrize("thr", ["1", "300", "4096"])
+def test_grid_bs_id_ordered_frontiers(oracle, thr, monkeypatch):
+    """BS on the grid with id-ordered frontiers at low thresholds: lists the
+    cluster loop hands back (no bits, taken in push order) alternate with
+    compacted grid steps; the device checks every compacted list has the
+    worklist's length (a mismatch raises)."""
+    monkeypatch.setenv("GLB_BM_THR", thr)
+    g = pkg.grid_graph(256, seed=1, max_weight=255)
+    for algo in ("bfs", "sssp"):
+        exp = oracle.oracle_distances(g, 0, algo)
+        for loop in ("host", "graph"):
+            r = pkg.run_strategy("BS", g, 0, pkg.RelaxOp(algo), pkg.KernelConfig(loop=loop))
+            assert np.array_equal(r.dist.array, exp), (thr, algo, loop)
+            assert r.records[-1].active_items >= 1
