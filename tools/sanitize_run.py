@@ -1,6 +1,7 @@
 """Small workload for compute-sanitizer (memcheck / racecheck / synccheck):
 every strategy x {bfs, sssp} x {host, graph loop} on small graphs with the
-corpus quirks, plus the grid-kernel and fused/dense WD variants, each checked
+corpus quirks, plus the grid-kernel, fused/dense WD and id-ordered BS
+frontier (compaction on every step) variants, each checked
 against the oracle.
 
     compute-sanitizer --tool memcheck python tools/sanitize_run.py
@@ -20,15 +21,16 @@ oracle.build()
 QUICK = "--quick" in sys.argv  # racecheck-sized: fewer graphs and variants
 if QUICK:
     graphs = [gs.build(pkg, gs.CORPUS[k]) for k in ("rmat10_skew", "quirks")]
-    variants = [{}, {"GLB_NO_SMALL": "1"}]
+    variants = [{}, {"GLB_NO_SMALL": "1"}, {"GLB_BM_THR": "1"}]
 else:
     graphs = [gs.build(pkg, gs.CORPUS[k]) for k in ("rmat10_skew", "quirks", "grid24", "degrees", "er_empty")]
     graphs.append(pkg.generate_rmat(13, 8, seed=2, max_weight=255))
     variants = [{}, {"GLB_NO_SMALL": "1"}, {"GLB_NO_SMALL": "1", "GLB_WD_FUSED": "1"},
-                {"GLB_NO_SMALL": "1", "GLB_WD_DENSE": "1"}]
+                {"GLB_NO_SMALL": "1", "GLB_WD_DENSE": "1"},
+                {"GLB_BM_THR": "1"}, {"GLB_NO_SMALL": "1", "GLB_BM_THR": "1"}]
 bad = 0
 for var in variants:
-    for k in ("GLB_NO_SMALL", "GLB_WD_FUSED", "GLB_WD_DENSE"):
+    for k in ("GLB_NO_SMALL", "GLB_WD_FUSED", "GLB_WD_DENSE", "GLB_BM_THR"):
         os.environ.pop(k, None)
     os.environ.update(var)
     for g in graphs:
@@ -42,7 +44,7 @@ for var in variants:
                         print("MISMATCH", var, g.num_nodes, algo, tag, loop)
 # 24-bit tier across renormalisations (> 256 generations), both loops, and
 # the device distance certificate
-for k in ("GLB_NO_SMALL", "GLB_WD_FUSED", "GLB_WD_DENSE"):
+for k in ("GLB_NO_SMALL", "GLB_WD_FUSED", "GLB_WD_DENSE", "GLB_BM_THR"):
     os.environ.pop(k, None)
 long_path = pkg.path_graph(300 if QUICK else 700, weighted=True, seed=3)
 for var in ({}, {"GLB_NO_SMALL": "1"}):
