@@ -29,9 +29,6 @@
 #include "glb_scan.cuh"
 #include "glb_small.cuh"
 #include "glb_peer.cuh"
-#ifdef GLB_EXP_SORT
-#include <cub/device/device_radix_sort.cuh>
-#endif
 
 namespace glb {
 
@@ -205,30 +202,6 @@ class Runner {
   uint32_t* bm_[2] = {nullptr, nullptr};
   long long bm_vec_ = 0;
   bool bm_on() const { return p_.strategy == GLB_BS && !bs_warp_ && !shard_mode_ && bm_thr_ > 0; }
-#ifdef GLB_EXP_SORT
-  long long sort_thr_ = getenv("GLB_SORT_THR") ? atoll(getenv("GLB_SORT_THR")) : 0;
-  uint32_t* sort_buf_ = nullptr;
-  void* sort_tmp_ = nullptr;
-  size_t sort_tmp_n_ = 0;
-  long long sort_cap_ = 0;
-  // experiment: sort the in-list (host loop only) before a relax step
-  void exp_sort(long long n_in, int bits) {
-    if (!sort_thr_ || n_in < sort_thr_) return;
-    uint32_t* q = h_->ctrl.qptr[h_->ctrl.in];
-    if (n_in > sort_cap_) {
-      if (sort_buf_) cudaFree(sort_buf_);
-      if (sort_tmp_) cudaFree(sort_tmp_);
-      sort_cap_ = n_in * 2;
-      GLB_CUDA_TRY(cudaMalloc(&sort_buf_, sort_cap_ * 4));
-      sort_tmp_n_ = 0;
-      cub::DeviceRadixSort::SortKeys(nullptr, sort_tmp_n_, q, sort_buf_, (int)sort_cap_, 0, bits, s_);
-      GLB_CUDA_TRY(cudaMalloc(&sort_tmp_, sort_tmp_n_));
-    }
-    size_t t = sort_tmp_n_;
-    GLB_CUDA_TRY(cub::DeviceRadixSort::SortKeys(sort_tmp_, t, q, sort_buf_, (int)n_in, 0, bits, s_));
-    GLB_CUDA_TRY(cudaMemcpyAsync(q, sort_buf_, n_in * 4, cudaMemcpyDeviceToDevice, s_));
-  }
-#endif
   int unroll_ = getenv("GLB_GRAPH_UNROLL") ? std::max(1, std::min(kGraphUnroll, atoi(getenv("GLB_GRAPH_UNROLL"))))
                                            : kGraphUnroll;
   double setup_ms_ = 0;
@@ -480,10 +453,13 @@ class Runner {
           k_bs_warp<D, W><<<grid, kBlock, 0, s_>>>(row_, rx, ctrl_, tail_);
           break;
         }
-        if (bm_[0]) {  // id-ordered in-list (no-op below the threshold)
+        if (bm_[0]) {  // id-ordered in-list (no-op below the threshold); the relax
+                       // kernel is its programmatic dependent launch
           k_bm_compact<<<grid_for(bm_vec_ * 4, kBmBlock, g_->num_sms * 8), kBmBlock, 0, s_>>>(ctrl_,
                                                                                           bm_vec_ * 4);
           GLB_CHECK_LAUNCH();
+          launch_dependent(k_bs_relax<D, W>, grid, row_, rx, ctrl_, tail_);
+          break;
         }
         k_bs_relax<D, W><<<grid, kBlock, 0, s_>>>(row_, rx, ctrl_, tail_);
         break;
@@ -596,13 +572,6 @@ class Runner {
           const unsigned grid = p_.strategy == GLB_NS ? (unsigned)cap_relax_  // as HP windows
                                                       : grid_for(n_in, (int)per, cap_relax_);
           ev.threads = (long long)grid * kBlock;
-#ifdef GLB_EXP_SORT
-          {
-            int bits = 1;
-            while ((1ll << bits) < n_all_) ++bits;
-            exp_sort(n_in, bits);
-          }
-#endif
           if (timing) GLB_CUDA_TRY(cudaEventRecord(ev.k0, s_));
           launch_relax(grid);
           if (timing) GLB_CUDA_TRY(cudaEventRecord(ev.k1, s_));

@@ -1,13 +1,12 @@
-"""Experiment: does a sorted worklist speed up the relax kernel on C3?
+"""C3 per-bucket relax-step time with and without id-ordered BS frontiers.
 
-    GRAPHLB_B200_LIB=_exp/sort.so python tools/c3_sort_probe.py [--k 4096] [--tags BS,HP]
-    python tools/c3_sort_probe.py --env GLB_BM_THR --thr 32768   # the id-ordered frontiers
+    python tools/c3_sort_probe.py --env GLB_BM_THR --thr 32768 [--k 4096] [--tags BS]
 
-The `_exp/sort.so` build (-DGLB_EXP_SORT) radix-sorts the in-list before every
-host-loop relax step holding >= GLB_SORT_THR items; the sort itself is outside
-the per-launch events, so the records show the relax kernel alone.  With
---env GLB_BM_THR the product's bitmap compaction is toggled instead (off =
-GLB_BM_THR=0); its kernel is inside the relax step's events.
+The bitmap compaction (k_bm_compact) is toggled by GLB_BM_THR (off = 0); its
+kernel is inside the relax step's host-loop events.  The first experiment
+(session 3, profiles/r02_c3_sorted_lists.txt) used a throw-away build that
+radix-sorted the in-list outside the events (GLB_SORT_THR): relax kernel alone,
+53 -> 29.6 us per >131K-node step.
 """
 import argparse
 import os
@@ -24,7 +23,7 @@ ap.add_argument("--k", type=int, default=4096)
 ap.add_argument("--tags", default="BS")
 ap.add_argument("--algo", default="sssp")
 ap.add_argument("--thr", default="8192")
-ap.add_argument("--env", default="GLB_SORT_THR")
+ap.add_argument("--env", default="GLB_BM_THR")
 a = ap.parse_args()
 g = pkg.grid_graph(a.k, seed=1, max_weight=255)
 ref = None
