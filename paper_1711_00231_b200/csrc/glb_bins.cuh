@@ -65,12 +65,17 @@ struct WarpSink {
   unsigned n;
   uint32_t* qout;
   unsigned int* nout;
+  uint32_t* bm = nullptr;  // NS: the out list's member bitmap (id-ordered frontiers)
   __device__ __forceinline__ void flush() {
     __syncwarp();
     unsigned base = 0;
     if (lane_id() == 0 && n) base = atomicAdd(nout, n);
     base = __shfl_sync(0xffffffffu, base, 0);
-    for (unsigned i = lane_id(); i < n; i += 32) qout[base + i] = buf[i];
+    for (unsigned i = lane_id(); i < n; i += 32) {
+      const uint32_t v = buf[i];
+      qout[base + i] = v;
+      if (bm) bm_set(bm, v);
+    }
     __syncwarp();
     n = 0;
   }
@@ -98,6 +103,7 @@ struct WarpSink {
 
 // -------------------------------------------------------------- mirrors ---
 struct NoMirror {
+  __device__ __forceinline__ void bind_bm(uint32_t*) {}
   template <int K, typename D, bool W>
   __device__ __forceinline__ void operator()(const Relaxer<D, W>&, unsigned,
                                              const uint32_t (&)[K], const D (&)[K],
@@ -110,6 +116,8 @@ struct NoMirror {
 struct NsMirror {
   const long long* __restrict__ cs;
   long long n_orig;
+  uint32_t* bm = nullptr;  // the out list's member bitmap (bound per step on the device)
+  __device__ __forceinline__ void bind_bm(uint32_t* b) { bm = b; }
   template <int K, typename D, bool W>
   __device__ __forceinline__ void operator()(const Relaxer<D, W>& rx, unsigned won,
                                              const uint32_t (&v)[K], const D (&cand)[K],
@@ -124,6 +132,7 @@ struct NsMirror {
         bool first = false;
         if (relax_cell<D>(rx.cells, child, cand[k], rx.gen, &first) && rx.claim_push(child, first)) {
           q_append(rx.qout, rx.nout, child);
+          if (bm) bm_set(bm, child);
           ++c.push;
         }
       }
@@ -330,6 +339,17 @@ __global__ void __launch_bounds__(kBlock, GLB_BIN_MINB) k_ns_relax(const long lo
   pdl_trigger();
   __shared__ uint32_t s_wq[kBinWarps][kBinWarpQ];
   const long long n = ctrl->qcount[ctrl->in];
+  // id-ordered frontiers (as k_bs_relax): clear the in list's words unless
+  // k_bm_compact rebuilt it; this step's pushes set the out list's bits
+  const unsigned bm_thr = ctrl->bm_thr;
+  const bool bm_valid_in = bm_thr && ctrl->bm_valid[ctrl->in];
+  uint32_t* bm_clear = bm_valid_in && n < bm_thr ? ctrl->bm[ctrl->in] : nullptr;
+  uint32_t* bm_out = bm_thr ? ctrl->bm[ctrl->out] : nullptr;
+  if (bm_thr && blockIdx.x == 0 && threadIdx.x == 0) {
+    if (bm_valid_in && n >= bm_thr && ctrl->bm_ctr != (unsigned)n) ctrl->bm_err = 1;
+    ctrl->bm_ctr = 0;
+    ctrl->bm_valid[ctrl->out] = 1;
+  }
   const int chunk = bin_chunk(n);
   if (blockIdx.x * (long long)kBinWarps * chunk >= n) {  // idle CTA
     ctl_tail(tail, ctrl);
@@ -337,7 +357,8 @@ __global__ void __launch_bounds__(kBlock, GLB_BIN_MINB) k_ns_relax(const long lo
   }
   timer_begin(ctrl->t_relax);
   const Relaxer<D, W> rx = bind(rx0, ctrl);
-  WarpSink sink{s_wq[threadIdx.x >> 5], 0u, rx.qout, rx.nout};
+  WarpSink sink{s_wq[threadIdx.x >> 5], 0u, rx.qout, rx.nout, bm_out};
+  mirror.bind_bm(bm_out);
   const uint32_t* __restrict__ qin = ctrl->qptr[ctrl->in];
   ThreadCounters c;
   for (long long base; (base = warp_next_chunk(ctrl, n, chunk)) >= 0;) {
@@ -346,6 +367,7 @@ __global__ void __launch_bounds__(kBlock, GLB_BIN_MINB) k_ns_relax(const long lo
     D dn = DistTraits<D>::kInf;
     if (i < n) {
       const uint32_t u = qin[i];
+      if (bm_clear) bm_clear[u >> 5] = 0u;
       const long long r0 = row[u], r1 = row[u + 1];  // in flight with dn
       dn = rx.dist(u);
       if (dn != DistTraits<D>::kInf) {
@@ -396,7 +418,10 @@ __global__ void __launch_bounds__(kBlock) k_bigbin(Relaxer<D, W> rx0, M mirror, 
     mbar_init(&s_bar[1], 1);
     mbar_fence_init();
   }
-  bq_init(bq, s_q);  // barrier: the mbarriers are ready
+  // NS id-ordered frontiers: the step's pushes set the out list's bits (HP runs have bm_thr 0)
+  uint32_t* bm_out = ctrl->bm_thr ? ctrl->bm[ctrl->out] : nullptr;
+  mirror.bind_bm(bm_out);
+  bq_init(bq, s_q, bm_out);  // barrier: the mbarriers are ready
   const unsigned long long pol = l2_evict_first();
   // thread 0: claim a piece into buffer b and start its copies
   auto claim = [&](int b) {

@@ -295,12 +295,12 @@ __device__ __forceinline__ void control_warp(DevCtrl* c, cudaGraphConditionalHan
   if (lane != 0) return;
   // this control kernel + the step's kernels (WD: scan + relax)
   // (two-kernel steps: WD scan + relax, HP window + CTA bin, NS relax + CTA bin)
-  // (BS with id-ordered frontiers: the compaction kernel + relax)
+  // (+1: the id-ordered frontier compaction before a BS / NS relax step)
   const bool two = c->mode == kModeWD ||
                    (c->bins_two && (c->mode == kModeHP ||
-                                    (c->mode == kModeRelax && c->strategy == GLB_NS))) ||
-                   (c->bm_thr && c->mode == kModeRelax && c->strategy == GLB_BS);
-  c->kernels += (c->small_exit || c->done ? 2 : (two ? 3 : 2)) - (fused ? 1 : 0);
+                                    (c->mode == kModeRelax && c->strategy == GLB_NS)));
+  const int bm = c->bm_thr && c->mode == kModeRelax ? 1 : 0;
+  c->kernels += (c->small_exit || c->done ? 2 : (two ? 3 : 2) + bm) - (fused ? 1 : 0);
   const unsigned long long wd_next = c->wd_next;
   const unsigned wd_zero = c->wd_zero_next;
   if (c->small_exit) {  // k_small_loop recorded and advanced its own iterations

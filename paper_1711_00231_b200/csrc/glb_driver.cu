@@ -145,7 +145,7 @@ class Runner {
     GLB_CUDA_TRY(cudaStreamSynchronize(s_));
     if (p_.loop_mode == GLB_LOOP_GRAPH) count_launches(h_->ctrl.kernels);
     if (h_->ctrl.overflow) throw OverflowRestart{};
-    if (h_->ctrl.bm_err) throw Error{GLB_ECUDA, "BS frontier bitmap out of step with its worklist"};
+    if (h_->ctrl.bm_err) throw Error{GLB_ECUDA, "frontier bitmap out of step with its worklist"};
     if (cnt > 0 && dist_out) {
       if (kNarrow)
         download_dist_u32(s_, (const uint32_t*)out, cnt, dist_out);
@@ -195,13 +195,15 @@ class Runner {
   // BS pushes through warp buffers (k_bs_warp): C2 SSSP BS -10 %, BFS -17 %, but
   // C3 SSSP +12 % (the CTA queue wins on degree-4 grids), so opt-in
   bool bs_warp_ = getenv("GLB_BS_WARP") != nullptr;
-  // BS id-ordered frontiers (k_bm_compact) for relax steps of >= bm_thr_
+  // BS / NS id-ordered frontiers (k_bm_compact) for relax steps of >= bm_thr_
   // nodes (and >= 1/256 of the graph); GLB_BM_THR=t sets the threshold to t
   // exactly, GLB_BM_THR=0 turns them off
   unsigned bm_thr_ = getenv("GLB_BM_THR") ? (unsigned)atoll(getenv("GLB_BM_THR")) : kBmThrDefault;
   uint32_t* bm_[2] = {nullptr, nullptr};
   long long bm_vec_ = 0;
-  bool bm_on() const { return p_.strategy == GLB_BS && !bs_warp_ && !shard_mode_ && bm_thr_ > 0; }
+  bool bm_on() const {
+    return ((p_.strategy == GLB_BS && !bs_warp_) || p_.strategy == GLB_NS) && !shard_mode_ && bm_thr_ > 0;
+  }
   int unroll_ = getenv("GLB_GRAPH_UNROLL") ? std::max(1, std::min(kGraphUnroll, atoi(getenv("GLB_GRAPH_UNROLL"))))
                                            : kGraphUnroll;
   double setup_ms_ = 0;
@@ -362,7 +364,9 @@ class Runner {
     c.bm_thr = !bm_on() ? 0u
                : getenv("GLB_BM_THR") ? bm_thr_
                                       : (unsigned)std::max<long long>(bm_thr_, n_all_ / 256);
-    c.bm_valid[0] = 1;  // the seed list's bit is set after the seed kernel
+    // the BS seed list's bit is set after the seed kernel; NS seeds the source's
+    // children too, so its first list is taken in seed order
+    c.bm_valid[0] = p_.strategy == GLB_BS ? 1 : 0;
     c.recs = drecs_;
     c.ls = ls_;
     c.ptw = ptw_;
@@ -397,7 +401,7 @@ class Runner {
     k_seed<D><<<grid_for(std::max<long long>(seeds, 1), kBlock, g_->num_sms * 4), kBlock, 0, s_>>>(
         cells_, q_[0], &ctrl_->qcount[0], src, klo, khi, elo, ehi, edges);
     GLB_CHECK_LAUNCH();
-    if (bm_[0])  // the seed list's member bit
+    if (bm_[0] && p_.strategy == GLB_BS)  // the seed list's member bit
       GLB_CUDA_TRY(cudaMemsetAsync((char*)bm_[0] + (src >> 3), 1 << (src & 7), 1, s_));
   }
 
@@ -464,6 +468,11 @@ class Runner {
         k_bs_relax<D, W><<<grid, kBlock, 0, s_>>>(row_, rx, ctrl_, tail_);
         break;
       case GLB_NS:  // binned windows + the CTA bin of the long ones (TMA-staged)
+        if (bm_[0]) {  // id-ordered in-list (no-op below the threshold)
+          k_bm_compact<<<grid_for(bm_vec_ * 4, kBmBlock, g_->num_sms * 8), kBmBlock, 0, s_>>>(ctrl_,
+                                                                                          bm_vec_ * 4);
+          GLB_CHECK_LAUNCH();
+        }
         if (!bins_two()) {  // split nodes all shorter than a CTA-bin window: one kernel
           k_ns_relax<D, W><<<grid, kBlock, 0, s_>>>(row_, ns_mirror(), rx, ctrl_, tail_);
           break;

@@ -416,10 +416,10 @@ __global__ void __cluster_dims__(kSmallCtas, 1, 1) __launch_bounds__(kSmallThrea
       }
     } else {
       // ---- BS / NS: thread per worklist node (node i -> cluster thread i mod 8192)
-      // BS id-ordered frontiers: the list a grid step handed over has its
+      // BS / NS id-ordered frontiers: the list a grid step handed over has its
       // bits set -- clear them; the cluster's own lists carry no bits
       // (bm_valid is dropped on exit), so its pushes stay off the bitmap
-      uint32_t* bm_in = it == 0 && sc.bm_thr && !cs && sc.bm_valid[sc.in] ? sc.bm[sc.in] : nullptr;
+      uint32_t* bm_in = it == 0 && sc.bm_thr && sc.bm_valid[sc.in] ? sc.bm[sc.in] : nullptr;
       for (unsigned i = gt; i < n; i += kSmallAll) {
         const uint32_t u = __ldcg(qin + i);
         if (bm_in) bm_in[u >> 5] = 0u;

@@ -418,15 +418,17 @@ def test_high_diameter_grid_all_strategies(oracle):
 
 @pytest.mark.parametrize("thr", ["1", "300", "4096"])
 def test_grid_bs_id_ordered_frontiers(oracle, thr, monkeypatch):
-    """BS on the grid with id-ordered frontiers at low thresholds: lists the
-    cluster loop hands back (no bits, taken in push order) alternate with
+    """BS / NS on the grid with id-ordered frontiers at low thresholds: lists
+    the cluster loop hands back (no bits, taken in push order) alternate with
     compacted grid steps; the device checks every compacted list has the
-    worklist's length (a mismatch raises)."""
+    worklist's length (a mismatch raises).  NS also mirrors onto split
+    children (mdt 3 splits the degree-4 nodes)."""
     monkeypatch.setenv("GLB_BM_THR", thr)
     g = pkg.grid_graph(256, seed=1, max_weight=255)
     for algo in ("bfs", "sssp"):
         exp = oracle.oracle_distances(g, 0, algo)
-        for loop in ("host", "graph"):
-            r = pkg.run_strategy("BS", g, 0, pkg.RelaxOp(algo), pkg.KernelConfig(loop=loop))
-            assert np.array_equal(r.dist.array, exp), (thr, algo, loop)
-            assert r.records[-1].active_items >= 1
+        for tag, mdt in (("BS", None), ("NS", None), ("NS", 3)):
+            for loop in ("host", "graph"):
+                r = pkg.run_strategy(tag, g, 0, pkg.RelaxOp(algo), pkg.KernelConfig(loop=loop), mdt=mdt)
+                assert np.array_equal(r.dist.array, exp), (thr, algo, tag, mdt, loop)
+                assert r.records[-1].active_items >= 1
