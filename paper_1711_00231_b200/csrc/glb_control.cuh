@@ -143,13 +143,13 @@ __device__ __forceinline__ void hp_decide_sub(DevCtrl* c) {
   }
 }
 
-// WD over a frontier holding at least 1/kDenseDiv of the nodes scans the
+// WD over a frontier holding at least 1/dense_ok of the nodes scans the
 // cells in id order (packed cells only: the generation marks the worklist).
-constexpr long long kDenseDiv = 8;
+// 24-bit tier: not right after a renormalisation (it reset the in list's tags).
 __device__ __forceinline__ void ctl_choose_dense(DevCtrl* c) {
-  c->wd_dense = c->dense_ok && c->tag_bits == 32 && c->strategy == GLB_WD && c->mode == kModeWD &&
-                !c->use_small &&
-                (long long)c->qcount[c->in] * kDenseDiv >= c->n_nodes;
+  c->wd_dense = c->dense_ok && (c->tag_bits == 32 || (c->tag_bits == 8 && c->renorm_gen != c->gen)) &&
+                c->strategy == GLB_WD && c->mode == kModeWD && !c->use_small &&
+                (long long)c->qcount[c->in] * c->dense_ok >= c->n_nodes;
 }
 
 __device__ __forceinline__ int ctl_step_kind(const DevCtrl* c) {

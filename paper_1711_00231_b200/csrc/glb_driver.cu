@@ -346,11 +346,19 @@ class Runner {
     c.hp_owner = hp_owner_;
     c.bins_two = bins_two() ? 1 : 0;
     c.n_nodes = n_all_;
-    // Dense-frontier scans (cells in id order) speed the relax kernel up per
-    // edge but the id-ordered processing does ~10 % more re-relaxation on C2,
-    // a wash overall, so they are opt-in.
-    c.dense_ok = p_.strategy == GLB_WD && !shard_mode_ && Cell<D>::kGenBits == 32 &&
-                 getenv("GLB_WD_DENSE") ? 1 : 0;
+    // Dense-frontier scans (cells in id order, frontiers of >= N/8 nodes) speed
+    // the relax kernel up per edge.  Where the cells fit L2 (32-bit tier) the
+    // id-ordered processing does ~10 % more re-relaxation (C2), a wash, so
+    // they are opt-in there; in the 24-bit tier (cells > 2x L2) they are the
+    // default (C5 at 32 bits: SSSP 266 -> 200 ms, BFS 59.6 -> 48.7).
+    // GLB_WD_DENSE=0 off, =1 on, =2 on for every frontier size (tests).
+    {
+      const char* e = getenv("GLB_WD_DENSE");
+      const int mode = e ? atoi(e) : (Cell<D>::kGenBits == 8 ? 1 : 0);
+      c.dense_ok = p_.strategy == GLB_WD && !shard_mode_ && Cell<D>::kPacked && mode > 0
+                       ? (mode >= 2 ? (1 << 30) : 8)
+                       : 0;
+    }
     c.wd_fused = p_.strategy == GLB_WD && !shard_mode_ && getenv("GLB_WD_FUSED") ? 1 : 0;
     // Inside the cluster loop the fused pushes replace the scan that every CTA
     // of the cluster would otherwise replicate over the whole list (C3 BFS WD
@@ -457,13 +465,12 @@ class Runner {
           k_bs_warp<D, W><<<grid, kBlock, 0, s_>>>(row_, rx, ctrl_, tail_);
           break;
         }
-        if (bm_[0]) {  // id-ordered in-list (no-op below the threshold); the relax
-                       // kernel is its programmatic dependent launch
+        if (bm_[0]) {  // id-ordered in-list (no-op below the threshold).  Not a
+                       // programmatic dependent launch: relax CTAs parked early
+                       // starve the compaction (C5 SSSP BS 238 -> 455 ms)
           k_bm_compact<<<grid_for(bm_vec_ * 4, kBmBlock, g_->num_sms * 8), kBmBlock, 0, s_>>>(ctrl_,
                                                                                           bm_vec_ * 4);
           GLB_CHECK_LAUNCH();
-          launch_dependent(k_bs_relax<D, W>, grid, row_, rx, ctrl_, tail_);
-          break;
         }
         k_bs_relax<D, W><<<grid, kBlock, 0, s_>>>(row_, rx, ctrl_, tail_);
         break;

@@ -250,7 +250,7 @@ struct DevCtrl {
   unsigned long long wd_next;   // (items << 32) | edges appended to list [wd_cur ^ 1]
   unsigned int wd_zero_next;    // zero-degree nodes pushed (counted for the record only)
   int wd_dense;                 // the WD scan reads the frontier from the cells, not the queue
-  int dense_ok;                 // packed cells, WD strategy, not sharded
+  int dense_ok;                 // WD id-order scans from frontiers of >= n_nodes / dense_ok (0: off)
   int tag_bits;                 // generation bits stored in a cell (8: 24-bit tier)
   int saved_mode;               // the step a renormalisation step interrupted
   unsigned int renorm_gen;      // generation of the last renormalisation

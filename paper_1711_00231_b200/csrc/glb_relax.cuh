@@ -390,7 +390,6 @@ __global__ void __launch_bounds__(kBlock) k_bs_relax(const long long* __restrict
                                                      CtlTail tail) {
   __shared__ uint32_t s_q[kQCap];
   __shared__ BlockQ bq;
-  pdl_wait();  // after k_bm_compact (a no-op when launched without PDL)
   const unsigned n = ctrl->qcount[ctrl->in];
   // id-ordered frontiers: a list k_bm_compact did not rebuild clears its
   // members' bitmap words here (this step sets bits in the other bitmap)
@@ -437,7 +436,6 @@ __global__ void __launch_bounds__(kBlock) k_bs_relax(const long long* __restrict
 // accesses over separate sectors; in id order they share them.
 constexpr int kBmBlock = 256;
 __global__ void __launch_bounds__(kBmBlock) k_bm_compact(DevCtrl* ctrl, long long nwords) {
-  pdl_trigger();  // the relax kernel may launch; it waits for this grid in pdl_wait
   const unsigned n = ctrl->qcount[ctrl->in];
   // below the threshold the relax kernel clears the words instead; a list
   // the cluster loop produced has no bits (it is taken in push order)

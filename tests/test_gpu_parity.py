@@ -34,6 +34,8 @@ VARIANTS = {"default": {}, "grid_kernels": {"GLB_NO_SMALL": "1"},
             "wd_fused": {"GLB_WD_FUSED": "1"},
             "grid_fused": {"GLB_NO_SMALL": "1", "GLB_WD_FUSED": "1"},
             "grid_dense": {"GLB_NO_SMALL": "1", "GLB_WD_DENSE": "1"},
+            # id-order WD scans for every frontier size (24-bit tier included)
+            "grid_dense_all": {"GLB_NO_SMALL": "1", "GLB_WD_DENSE": "2"},
             # graph-loop structure knobs: separate control kernel, one step per
             # WHILE iteration without programmatic dependent launch
             "grid_ctl_kernel": {"GLB_NO_SMALL": "1", "GLB_NO_FUSED_CTL": "1"},
@@ -120,12 +122,14 @@ def test_24bit_cells_boundary_and_promotion(oracle):
                         pkg.run_strategy(tag, g, 0, pkg.RelaxOp("sssp"), cfg)
 
 
-@pytest.mark.parametrize("variant", ["default", "grid_kernels", "grid_fused"])
+@pytest.mark.parametrize("variant", ["default", "grid_kernels", "grid_fused", "grid_dense_all"])
 @pytest.mark.parametrize("loop", ["host", "graph"])
 def test_24bit_generation_tags_renormalise(oracle, loop, variant, monkeypatch):
     """More than 256 generations: the 8-bit push tags of the 24-bit tier wrap
     and are renormalised every 128 generations (k_renorm); results must equal
-    the 32- and 64-bit tiers' and the oracle's."""
+    the 32- and 64-bit tiers' and the oracle's.  grid_dense_all scans every WD
+    frontier from the cells' tags, across the renormalisations too (the step
+    right after one takes its list instead)."""
     for k, v in VARIANTS[variant].items():
         monkeypatch.setenv(k, v)
     rng = np.random.default_rng(7)
@@ -291,8 +295,8 @@ def test_records_and_counters():
     assert sd["EP"] < sd["BS"] and sd["WD"] < sd["BS"] and sd["NS"] < sd["BS"], sd
 
 
-@pytest.mark.parametrize("variant", ["grid_kernels", "wd_fused", "grid_dense", "grid_bs_warp",
-                                     "grid_bm_every_step"])
+@pytest.mark.parametrize("variant", ["grid_kernels", "wd_fused", "grid_dense", "grid_dense_all",
+                                     "grid_bs_warp", "grid_bm_every_step"])
 def test_random_graphs_execution_variants(oracle, variant, monkeypatch):
     for k, v in VARIANTS[variant].items():
         monkeypatch.setenv(k, v)
