@@ -286,6 +286,10 @@ __global__ void __launch_bounds__(kBlock, GLB_BIN_MINB) k_hp_window(const long l
   pdl_trigger();
   __shared__ uint32_t s_wq[kBinWarps][kBinWarpQ];
   const long long n = ctrl->qcount[ctrl->in];
+  if (blockIdx.x == 0 && threadIdx.x == 0 && ctrl->hp_dense) {  // k_tag_compact rebuilt the list
+    if (ctrl->tag_ctr != (unsigned)n) ctrl->bm_err = 1;
+    ctrl->tag_ctr = 0;
+  }
   const int chunk = bin_chunk(n);
   if (blockIdx.x * (long long)kBinWarps * chunk >= n) {  // idle CTA
     ctl_tail(tail, ctrl);

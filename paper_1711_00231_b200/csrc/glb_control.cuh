@@ -146,10 +146,12 @@ __device__ __forceinline__ void hp_decide_sub(DevCtrl* c) {
 // WD over a frontier holding at least 1/dense_ok of the nodes scans the
 // cells in id order (packed cells only: the generation marks the worklist).
 // 24-bit tier: not right after a renormalisation (it reset the in list's tags).
+// HP: the same for the super-list a window sub-iteration 0 reads (k_tag_compact).
 __device__ __forceinline__ void ctl_choose_dense(DevCtrl* c) {
-  c->wd_dense = c->dense_ok && (c->tag_bits == 32 || (c->tag_bits == 8 && c->renorm_gen != c->gen)) &&
-                c->strategy == GLB_WD && c->mode == kModeWD && !c->use_small &&
-                (long long)c->qcount[c->in] * c->dense_ok >= c->n_nodes;
+  const bool tags = c->dense_ok && (c->tag_bits == 32 || (c->tag_bits == 8 && c->renorm_gen != c->gen)) &&
+                    !c->use_small && (long long)c->qcount[c->in] * c->dense_ok >= c->n_nodes;
+  c->wd_dense = tags && c->strategy == GLB_WD && c->mode == kModeWD;
+  c->hp_dense = tags && c->strategy == GLB_HP && c->mode == kModeHP && c->s == 0;
 }
 
 __device__ __forceinline__ int ctl_step_kind(const DevCtrl* c) {
@@ -299,7 +301,9 @@ __device__ __forceinline__ void control_warp(DevCtrl* c, cudaGraphConditionalHan
   const bool two = c->mode == kModeWD ||
                    (c->bins_two && (c->mode == kModeHP ||
                                     (c->mode == kModeRelax && c->strategy == GLB_NS)));
-  const int bm = c->bm_thr && c->mode == kModeRelax ? 1 : 0;
+  // (+1: HP window steps of a run with id-ordered super-lists start with k_tag_compact)
+  const int bm = (c->bm_thr && c->mode == kModeRelax) ||
+                 (c->dense_ok && c->strategy == GLB_HP && c->mode == kModeHP) ? 1 : 0;
   c->kernels += (c->small_exit || c->done ? 2 : (two ? 3 : 2) + bm) - (fused ? 1 : 0);
   const unsigned long long wd_next = c->wd_next;
   const unsigned wd_zero = c->wd_zero_next;

@@ -200,6 +200,7 @@ class Runner {
   // exactly, GLB_BM_THR=0 turns them off
   unsigned bm_thr_ = getenv("GLB_BM_THR") ? (unsigned)atoll(getenv("GLB_BM_THR")) : kBmThrDefault;
   uint32_t* bm_[2] = {nullptr, nullptr};
+  bool hp_dense_ = false;  // HP window steps start with k_tag_compact
   long long bm_vec_ = 0;
   bool bm_on() const {
     return ((p_.strategy == GLB_BS && !bs_warp_) || p_.strategy == GLB_NS) && !shard_mode_ && bm_thr_ > 0;
@@ -355,9 +356,11 @@ class Runner {
     {
       const char* e = getenv("GLB_WD_DENSE");
       const int mode = e ? atoi(e) : (Cell<D>::kGenBits == 8 ? 1 : 0);
-      c.dense_ok = p_.strategy == GLB_WD && !shard_mode_ && Cell<D>::kPacked && mode > 0
+      c.dense_ok = (p_.strategy == GLB_WD || p_.strategy == GLB_HP) && !shard_mode_ && Cell<D>::kPacked &&
+                           mode > 0
                        ? (mode >= 2 ? (1 << 30) : 8)
                        : 0;
+      hp_dense_ = p_.strategy == GLB_HP && c.dense_ok;
     }
     c.wd_fused = p_.strategy == GLB_WD && !shard_mode_ && getenv("GLB_WD_FUSED") ? 1 : 0;
     // Inside the cluster loop the fused pushes replace the scan that every CTA
@@ -526,6 +529,11 @@ class Runner {
   // window kernel is then the step's only kernel (and runs the control tail)
   bool bins_two() const { return mdt_ >= kBinCtaMin; }
   void launch_hp(unsigned grid) {
+    if (hp_dense_) {  // id-ordered super-list for window sub-iteration 0 (no-op otherwise)
+      k_tag_compact<D><<<grid_for((n_all_ + 31) / 32, kBmBlock, g_->num_sms * 8), kBmBlock, 0, s_>>>(cells_,
+                                                                                                   ctrl_);
+      GLB_CHECK_LAUNCH();
+    }
     if (!bins_two()) {
       k_hp_window<D, W><<<grid, kBlock, 0, s_>>>(row_, relaxer(), ctrl_, tail_);
       GLB_CHECK_LAUNCH();
@@ -649,7 +657,7 @@ class Runner {
       << (const void*)ctrl_ << '|' << (const void*)items_[0] << '|' << (const void*)items_[1] << '|'
       << (const void*)tile_first_[0] << '|' << (const void*)tile_first_[1] << '|'
       << (const void*)lb_.flags << '|' << (const void*)lb_.aggs << '|' << g_->n << '|' << n_all_
-      << '|' << mdt_ << '|' << resume_graph_ << '|' << (const void*)bm_[0] << '|' << bm_vec_;
+      << '|' << mdt_ << '|' << resume_graph_ << '|' << (const void*)bm_[0] << '|' << bm_vec_ << '|' << hp_dense_;
     return k.str();
   }
 

@@ -287,6 +287,8 @@ struct DevCtrl {
   unsigned int bm_err;          // a compaction produced a list of another length
   unsigned int bm_pad;
   int bm_valid[2];              // bm[i] holds exactly list i's members (else it is all zero)
+  int hp_dense;                 // HP: this window step's list is rebuilt in id order from the cell tags
+  unsigned int tag_ctr;         // k_tag_compact cursor
 };
 
 // --------------------------------------------------------- device graph ---

@@ -464,6 +464,51 @@ __global__ void __launch_bounds__(kBmBlock) k_bm_compact(DevCtrl* ctrl, long lon
   }
 }
 
+// HP id-ordered super-lists: the list a window sub-iteration 0 reads is
+// exactly {v : cell tag == the super-iteration's generation} (every push of a
+// super-iteration carries its generation), so a frontier holding >= N/8 nodes
+// is rebuilt in id order from the cells -- same set and length, checked --
+// like WD's dense scans (packed cells; not right after a 24-bit
+// renormalisation).  A warp turns 1024 consecutive cells into 32 bitmap words
+// with coalesced loads and ballots; then as k_bm_compact.
+template <typename D>
+__global__ void __launch_bounds__(kBmBlock) k_tag_compact(const CellS<D>* __restrict__ cells,
+                                                          DevCtrl* ctrl) {
+  if (!ctrl->hp_dense) return;
+  using Scan = cub::BlockScan<unsigned, kBmBlock>;
+  __shared__ typename Scan::TempStorage ts;
+  __shared__ uint32_t s_ids[kBmBlock * 32];
+  __shared__ unsigned s_base;
+  const long long nn = ctrl->n_nodes;
+  const long long nwords = (nn + 31) / 32;
+  const uint32_t in_gen = Cell<D>::tag(ctrl->gen - 1u);
+  uint32_t* __restrict__ q = ctrl->qptr[ctrl->in];
+  const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
+  for (long long b = (long long)blockIdx.x * kBmBlock; b < nwords; b += (long long)gridDim.x * kBmBlock) {
+    const long long wbase = b + (long long)warp * 32;  // this warp's 32 words
+    uint32_t w = 0;
+#pragma unroll 4
+    for (int k = 0; k < 32; ++k) {
+      const long long id = (wbase + k) * 32 + lane;
+      const bool m = id < nn && Cell<D>::gen(cells[id]) == in_gen;
+      const unsigned bits = __ballot_sync(0xffffffffu, m);
+      if (lane == (unsigned)k) w = bits;
+    }
+    const long long i = wbase + lane;  // word index of this thread
+    unsigned ex, total;
+    Scan(ts).ExclusiveSum((unsigned)__popc(w), ex, total);
+    if (total) {  // CTA-uniform
+      if (threadIdx.x == 0) s_base = atomicAdd(&ctrl->tag_ctr, total);
+      const uint32_t id0 = (uint32_t)(i * 32);
+      for (uint32_t x = w; x; x &= x - 1u) s_ids[ex++] = id0 + (uint32_t)(__ffs(x) - 1);
+      __syncthreads();
+      const unsigned base = s_base;
+      for (unsigned j = threadIdx.x; j < total; j += kBmBlock) q[base + j] = s_ids[j];
+    }
+    __syncthreads();
+  }
+}
+
 // ============================================================ EP (K2) ===
 // Edge worklist; improved destinations reserve their whole out-edge range.
 // Ranges are collected per CTA (one global reservation per CTA round) and
