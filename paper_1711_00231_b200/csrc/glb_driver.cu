@@ -201,6 +201,7 @@ class Runner {
   unsigned bm_thr_ = getenv("GLB_BM_THR") ? (unsigned)atoll(getenv("GLB_BM_THR")) : kBmThrDefault;
   uint32_t* bm_[2] = {nullptr, nullptr};
   bool hp_dense_ = false;  // HP window steps start with k_tag_compact
+  int small_ctas_ = kSmallCtas;  // cluster loop CTAs (8 or 16)
   long long bm_vec_ = 0;
   bool bm_on() const {
     return ((p_.strategy == GLB_BS && !bs_warp_) || p_.strategy == GLB_NS) && !shard_mode_ && bm_thr_ > 0;
@@ -293,12 +294,42 @@ class Runner {
                                                 : cap((const void*)k_bigbin<D, W, NsMirror>),
                           g_->num_sms);
     }
-    if (kSmallCtas > 8)
-      GLB_CUDA_TRY(cudaFuncSetAttribute((const void*)k_small_loop<D, W>,
-                                        cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    GLB_CUDA_TRY(cudaFuncSetAttribute((const void*)k_small_loop<D, W>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)small_smem_bytes<D>()));
+    // Cluster loop size: 16 CTAs (non-portable) for EP / HP -- C3 BFS EP
+    // 58.8 -> 52.6 ms, C2 SSSP / BFS HP -2 / -3 % -- and 8 for BS / NS / WD
+    // (16: C3 SSSP BS +2.4 %; WD C3 BFS -10 % but C2 BFS +2.7 %, SSSP +0.8 %);
+    // GLB_SMALL_CTAS=8|16 overrides.  16 needs the GPU to co-schedule a
+    // 16-CTA cluster; otherwise 8.
+    {
+      const char* e = getenv("GLB_SMALL_CTAS");
+      int want = e ? atoi(e) : (p_.strategy == GLB_EP || p_.strategy == GLB_HP ? 16 : kSmallCtas);
+      if (want != 16) want = 8;
+      GLB_CUDA_TRY(cudaFuncSetAttribute((const void*)k_small_loop<D, W, 8>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)small_smem_bytes<D>()));
+      if (want == 16) {
+        const void* k16 = (const void*)k_small_loop<D, W, 16>;
+        int nclusters = 0;
+        if (cudaFuncSetAttribute(k16, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess &&
+            cudaFuncSetAttribute(k16, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)small_smem_bytes<D>()) == cudaSuccess) {
+          cudaLaunchConfig_t lc = {};
+          lc.gridDim = dim3(16);
+          lc.blockDim = dim3(kSmallThreads);
+          lc.dynamicSmemBytes = small_smem_bytes<D>();
+          cudaLaunchAttribute at[1];
+          at[0].id = cudaLaunchAttributeClusterDimension;
+          at[0].val.clusterDim.x = 16;
+          at[0].val.clusterDim.y = 1;
+          at[0].val.clusterDim.z = 1;
+          lc.attrs = at;
+          lc.numAttrs = 1;
+          if (cudaOccupancyMaxActiveClusters(&nclusters, k16, &lc) != cudaSuccess) nclusters = 0;
+        }
+        cudaGetLastError();
+        if (nclusters < 1) want = 8;
+      }
+      small_ctas_ = want;
+    }
     if (relax_kernel()) cap_relax_ = std::max(cap(relax_kernel()), g_->num_sms);
     pin_cells_in_l2(nb * sizeof(CellS<D>));
     ptw_ = nullptr;
@@ -546,9 +577,14 @@ class Runner {
   }
   NsMirror ns_mirror() const { return NsMirror{cs_, g_->n}; }
   void launch_small() {
-    k_small_loop<D, W><<<kSmallCtas, kSmallThreads, small_smem_bytes<D>(), s_>>>(
-        row_, p_.strategy == GLB_NS ? cs_ : nullptr, g_->n,
-        p_.strategy == GLB_EP ? src_ : nullptr, p_.chunked != 0, relaxer(), ctrl_, tail_);
+    const long long* cs = p_.strategy == GLB_NS ? cs_ : nullptr;
+    const uint32_t* src = p_.strategy == GLB_EP ? src_ : nullptr;
+    if (small_ctas_ == 16)
+      k_small_loop<D, W, 16><<<16, kSmallThreads, small_smem_bytes<D>(), s_>>>(
+          row_, cs, g_->n, src, p_.chunked != 0, relaxer(), ctrl_, tail_);
+    else
+      k_small_loop<D, W, 8><<<8, kSmallThreads, small_smem_bytes<D>(), s_>>>(
+          row_, cs, g_->n, src, p_.chunked != 0, relaxer(), ctrl_, tail_);
     GLB_CHECK_LAUNCH();
   }
   void launch_control(cudaGraphConditionalHandle hl, const ModeHandles& hm, int gm) {
@@ -585,7 +621,7 @@ class Runner {
       }
       switch (c.use_small ? (int)kModeSmall : c.mode) {
         case kModeSmall: {
-          ev.threads = kSmallAll;
+          ev.threads = (long long)small_ctas_ * kSmallThreads;
           if (timing) GLB_CUDA_TRY(cudaEventRecord(ev.k0, s_));
           launch_small();
           if (timing) GLB_CUDA_TRY(cudaEventRecord(ev.k1, s_));
@@ -640,7 +676,7 @@ class Runner {
       read_ctrl();
       if (small) {  // several iterations in one launch: per-record device timers
         for (unsigned r = nrec0; r < h_->ctrl.nrec; ++r)
-          ev_of_rec_.push_back(EvPair{nullptr, nullptr, nullptr, nullptr, kSmallAll});
+          ev_of_rec_.push_back(EvPair{nullptr, nullptr, nullptr, nullptr, (long long)small_ctas_ * kSmallThreads});
       } else if (h_->ctrl.nrec > nrec0) {
         ev_of_rec_.push_back(ev);
       }
@@ -657,7 +693,7 @@ class Runner {
       << (const void*)ctrl_ << '|' << (const void*)items_[0] << '|' << (const void*)items_[1] << '|'
       << (const void*)tile_first_[0] << '|' << (const void*)tile_first_[1] << '|'
       << (const void*)lb_.flags << '|' << (const void*)lb_.aggs << '|' << g_->n << '|' << n_all_
-      << '|' << mdt_ << '|' << resume_graph_ << '|' << (const void*)bm_[0] << '|' << bm_vec_ << '|' << hp_dense_;
+      << '|' << mdt_ << '|' << resume_graph_ << '|' << (const void*)bm_[0] << '|' << bm_vec_ << '|' << hp_dense_ << '|' << small_ctas_;
     return k.str();
   }
 

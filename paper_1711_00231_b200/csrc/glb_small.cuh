@@ -44,9 +44,10 @@ namespace cg = cooperative_groups;
 #ifndef GLB_SMALL_BRANCHLESS
 #define GLB_SMALL_BRANCHLESS 1  // small_relax without divergent regions (C3 BFS BS 79.5 -> 75.1 ms)
 #endif
-constexpr int kSmallCtas = GLB_SMALL_CTAS;        // cluster size (8 = portable maximum, 16 opt-in)
+// Cluster size: 8 CTAs (the portable maximum) or 16 (non-portable opt-in),
+// a template parameter of the kernel; the driver picks per strategy.
+constexpr int kSmallCtas = GLB_SMALL_CTAS;        // the default / BS / NS cluster size
 constexpr int kSmallThreads = 1024;               // threads per CTA
-constexpr int kSmallAll = kSmallCtas * kSmallThreads;
 constexpr int kSmallItems = kSmallItemsCtl;       // worklist nodes one iteration may hold
 constexpr long long kSmallEdges = kSmallEdgesCtl;  // WD: active edges one iteration may hold
 
@@ -161,20 +162,20 @@ __device__ __forceinline__ unsigned small_relax(const Relaxer<D, W>& rx, unsigne
 // Equal edges per thread across the cluster (f = gt + r * 8192) over the item
 // table (s_pre: first edge of every item, s_pre[n_items] = total).  The loop
 // bound is warp-uniform so fused pushes can use warp collectives.
-template <typename D, bool W>
+template <int ALL, typename D, bool W>
 __device__ __forceinline__ void wd_tiles(const Relaxer<D, W>& rx, unsigned* cursor, uint32_t* qout,
                                          const uint32_t* s_pre, const uint32_t* s_base,
                                          const D* s_dn, int n_items, uint32_t total, unsigned gt,
                                          ThreadCounters& c, const SmallPush* fused) {
   constexpr int K = 4;
   const unsigned lane = lane_id();
-  for (uint32_t fb = gt - lane; fb < total; fb += (uint32_t)K * kSmallAll) {
+  for (uint32_t fb = gt - lane; fb < total; fb += (uint32_t)K * ALL) {
     uint32_t e[K];
     D d[K];
     unsigned valid = 0;
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-      const uint32_t f = fb + lane + (uint32_t)k * kSmallAll;
+      const uint32_t f = fb + lane + (uint32_t)k * ALL;
       if (f < total) {
         int lo = 0, hi = n_items;  // last item with s_pre <= f
         while (hi - lo > 1) {
@@ -198,11 +199,12 @@ __device__ __forceinline__ void wd_tiles(const Relaxer<D, W>& rx, unsigned* curs
   }
 }
 
-template <typename D, bool W>
-__global__ void __cluster_dims__(kSmallCtas, 1, 1) __launch_bounds__(kSmallThreads, 1)
+template <typename D, bool W, int CTAS>
+__global__ void __cluster_dims__(CTAS, 1, 1) __launch_bounds__(kSmallThreads, 1)
     k_small_loop(const long long* __restrict__ row, const long long* __restrict__ cs,
                  long long n_orig, const uint32_t* __restrict__ ep_src, bool ep_chunked,
                  Relaxer<D, W> rx0, DevCtrl* gctrl, CtlTail tail) {
+  constexpr int kSmallAll = CTAS * kSmallThreads;  // threads of the cluster
   extern __shared__ __align__(16) unsigned char s_dyn[];
   D* s_dn = reinterpret_cast<D*>(s_dyn);                                   // [kSmallItems]
   uint32_t* s_pre = reinterpret_cast<uint32_t*>(s_dyn + kSmallItems * sizeof(D));  // [+1]
@@ -294,7 +296,7 @@ __global__ void __cluster_dims__(kSmallCtas, 1, 1) __launch_bounds__(kSmallThrea
         s_total = sc.wd_total;
       }
       __syncthreads();
-      wd_tiles<D, W>(rx, cursor, qout, s_pre, s_base, s_dn, ni, (uint32_t)sc.wd_total, gt, c,
+      wd_tiles<kSmallAll, D, W>(rx, cursor, qout, s_pre, s_base, s_dn, ni, (uint32_t)sc.wd_total, gt, c,
                      fused);
     } else if (sc.mode == kModeWD) {
       // ---- scan of remaining degrees, replicated in every CTA (items
@@ -341,7 +343,7 @@ __global__ void __cluster_dims__(kSmallCtas, 1, 1) __launch_bounds__(kSmallThrea
         }
         if (tid == 0) s_pre[tot_i] = (uint32_t)tot_e;
         __syncthreads();
-        wd_tiles<D, W>(rx, cursor, qout, s_pre, s_base, s_dn, tot_i, (uint32_t)tot_e, gt, c,
+        wd_tiles<kSmallAll, D, W>(rx, cursor, qout, s_pre, s_base, s_dn, tot_i, (uint32_t)tot_e, gt, c,
                        fused);
       }
     } else if (sc.mode == kModeHP) {

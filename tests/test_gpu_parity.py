@@ -46,7 +46,10 @@ VARIANTS = {"default": {}, "grid_kernels": {"GLB_NO_SMALL": "1"},
             # list from its bitmap), alone and alternating with the cluster loop
             "grid_bm_every_step": {"GLB_NO_SMALL": "1", "GLB_BM_THR": "1"},
             "bm_every_step": {"GLB_BM_THR": "1"},
-            "grid_bm_off": {"GLB_NO_SMALL": "1", "GLB_BM_THR": "0"}}
+            "grid_bm_off": {"GLB_NO_SMALL": "1", "GLB_BM_THR": "0"},
+            # cluster loop at the other size than the strategy's default (8 / 16 CTAs)
+            "cluster8": {"GLB_SMALL_CTAS": "8"},
+            "cluster16": {"GLB_SMALL_CTAS": "16"}}
 
 
 @pytest.mark.parametrize("variant", list(VARIANTS))
@@ -406,9 +409,13 @@ def test_sharded_virtual_ranks_match_reference(golden):
             assert np.array_equal(d, exp), (algo, tag)
 
 
-def test_high_diameter_grid_all_strategies(oracle):
+@pytest.mark.parametrize("ctas", ["", "8", "16"])
+def test_high_diameter_grid_all_strategies(oracle, ctas, monkeypatch):
     """C3's shape at k=256 (511 BFS levels, ~530 SSSP iterations): long runs of
-    small frontiers through the cluster loop, alternating with grid steps."""
+    small frontiers through the cluster loop (default, 8- and 16-CTA
+    clusters), alternating with grid steps."""
+    if ctas:
+        monkeypatch.setenv("GLB_SMALL_CTAS", ctas)
     g = pkg.grid_graph(256, seed=1, max_weight=255)
     for algo in ("bfs", "sssp"):
         exp = oracle.oracle_distances(g, 0, algo)

@@ -18,9 +18,11 @@ ap.add_argument("--algo", default="sssp")
 ap.add_argument("--scale", type=int, default=22)
 ap.add_argument("--reps", type=int, default=9)
 ap.add_argument("--grid", type=int, default=0, help="k x k grid (C3: 4096) instead of an R-MAT")
+ap.add_argument("--skewed", action="store_true", help="C4's skewed R-MAT parameters")
 a = ap.parse_args()
 g = (pkg.grid_graph(a.grid, seed=1, max_weight=255) if a.grid else
-     pkg.generate_rmat(a.scale, 16, seed=1, max_weight=255, device=0))
+     pkg.generate_rmat(a.scale, 16, params=(0.7, 0.15, 0.10, 0.05) if a.skewed else pkg.DEFAULT_RMAT_PARAMS,
+                       seed=1, max_weight=255, device=0))
 res = {v: [] for v in a.variants}
 for rep in range(a.reps + 1):
     for v in a.variants:

@@ -1,6 +1,7 @@
 #!/bin/bash
 # round-2 (session 3) evidence on the committed build: GPU tier, smoke, bench (ours + reference),
-# ncu launch list + --set full of k_wd_relax, suite C1-C5, compute-sanitizer
+# ncu launch list + --set full of k_wd_relax and of the C5 HP tag compaction / window kernels, suite C1-C5
+# (compute-sanitizer is closed on this pool)
 O=gpurun_out/final
 rm -rf $O; mkdir -p $O
 python -c "import __graft_entry__ as g; g.build()" > $O/build.log 2>&1 || exit 1
@@ -14,8 +15,6 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_wd
   -o $O/wd_relax_full -f python tools/profile_run.py --strategy WD --algo sssp --loop host --runs 1 > $O/ncu_full.log 2>&1
 timeout 2400 python tools/suite.py --configs C1,C2,C4,C3 --reps 3 --out $O/suite.json > $O/suite.log 2>&1
 timeout 1500 python tools/suite.py --configs C5 --reps 2 --out $O/suite_c5.json > $O/suite_c5.log 2>&1
-timeout 900 compute-sanitizer --tool memcheck --print-limit 20 python tools/sanitize_run.py > $O/sanitize_memcheck.log 2>&1; echo "rc=$?" >> $O/sanitize_memcheck.log
-timeout 1200 compute-sanitizer --tool racecheck --print-limit 20 python tools/sanitize_run.py --quick > $O/sanitize_racecheck.log 2>&1; echo "rc=$?" >> $O/sanitize_racecheck.log
-timeout 900 compute-sanitizer --tool synccheck --print-limit 20 python tools/sanitize_run.py --quick > $O/sanitize_synccheck.log 2>&1; echo "rc=$?" >> $O/sanitize_synccheck.log
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_tag_compact|k_hp_window" -s 20 -c 4 \
+  -o $O/hp_c5_tag -f python tools/suite.py --configs C5 --tags HP --algos sssp --reps 1 --out $O/tmp_c5.json > $O/ncu_hp_c5.log 2>&1
 tail -n 2 $O/pytest_gpu.log; tail -n 1 $O/smoke.log; head -c 400 $O/bench.json; echo; grep "^|" $O/suite.log | tail -n 40; grep "^|" $O/suite_c5.log | tail -n 10
-tail -n 3 $O/sanitize_*.log
