@@ -16,5 +16,5 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_wd
 timeout 2400 python tools/suite.py --configs C1,C2,C4,C3 --reps 3 --out $O/suite.json > $O/suite.log 2>&1
 timeout 1500 python tools/suite.py --configs C5 --reps 2 --out $O/suite_c5.json > $O/suite_c5.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_tag_compact|k_hp_window" -s 20 -c 4 \
-  -o $O/hp_c5_tag -f python tools/suite.py --configs C5 --tags HP --algos sssp --reps 1 --out $O/tmp_c5.json > $O/ncu_hp_c5.log 2>&1
+  -o $O/hp_c5_tag -f python tools/suite.py --configs C5 --tags HP --algos sssp --reps 1 --loop host --out $O/tmp_c5.json > $O/ncu_hp_c5.log 2>&1
 tail -n 2 $O/pytest_gpu.log; tail -n 1 $O/smoke.log; head -c 400 $O/bench.json; echo; grep "^|" $O/suite.log | tail -n 40; grep "^|" $O/suite_c5.log | tail -n 10
