@@ -202,6 +202,7 @@ class Runner {
   uint32_t* bm_[2] = {nullptr, nullptr};
   bool hp_dense_ = false;  // HP window steps start with k_tag_compact
   int small_ctas_ = kSmallCtas;  // cluster loop CTAs (8 or 16)
+  uint32_t* ep_dn_[2] = {nullptr, nullptr};  // EP carried source levels (unweighted)
   long long bm_vec_ = 0;
   bool bm_on() const {
     return ((p_.strategy == GLB_BS && !bs_warp_) || p_.strategy == GLB_NS) && !shard_mode_ && bm_thr_ > 0;
@@ -255,6 +256,17 @@ class Runner {
       const size_t eb = (size_t)std::max<long long>(g_->m, 1) * 4;
       q_[0] = (uint32_t*)ensure(ws.eq[0], eb);
       q_[1] = (uint32_t*)ensure(ws.eq[1], eb);
+      ep_dn_[0] = ep_dn_[1] = nullptr;
+      // carried levels skip the pre-check, which on R-MAT tails filters most
+      // atomics (C1 BFS EP +18 %, C2 +5 %); on low-degree, high-diameter
+      // graphs the shorter chain wins (C3 BFS EP 51.8 -> 49.1 ms): average
+      // out-degree <= 8 only (GLB_EP_CARRY=0/1 forces)
+      const char* ec = getenv("GLB_EP_CARRY");
+      const bool carry = ec ? atoi(ec) != 0 : g_->m <= 8 * g_->n;
+      if (!W && sizeof(D) == 4 && !shard_mode_ && carry) {  // levels fit u32
+        ep_dn_[0] = (uint32_t*)ensure(ws.ep_dn[0], eb);
+        ep_dn_[1] = (uint32_t*)ensure(ws.ep_dn[1], eb);
+      }
       q_[2] = q_[3] = q_[1];
     } else {
       for (int i = 0; i < 4; ++i)
@@ -401,6 +413,8 @@ class Runner {
                        !getenv("GLB_NO_WD_FUSED_SMALL") ? 1 : 0;
     c.bm[0] = bm_[0];
     c.bm[1] = bm_[1];
+    c.ep_dn[0] = p_.strategy == GLB_EP ? ep_dn_[0] : nullptr;
+    c.ep_dn[1] = p_.strategy == GLB_EP ? ep_dn_[1] : nullptr;
     // a compaction reads the whole bitmap (n/8 bytes): worth it once the list
     // holds >= 1/256 of the nodes (C3 SSSP: 65,536 of 16.8M) and >= 32K of them
     c.bm_thr = !bm_on() ? 0u

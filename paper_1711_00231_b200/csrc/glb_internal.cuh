@@ -289,6 +289,9 @@ struct DevCtrl {
   int bm_valid[2];              // bm[i] holds exactly list i's members (else it is all zero)
   int hp_dense;                 // HP: this window step's list is rebuilt in id order from the cell tags
   unsigned int tag_ctr;         // k_tag_compact cursor
+  // EP on unweighted graphs inside the cluster loop: the level of each listed
+  // edge's source, written at push time next to the edge (lists 0 / 1)
+  uint32_t* ep_dn[2];
 };
 
 // --------------------------------------------------------- device graph ---
@@ -314,17 +317,19 @@ struct Workspace {
   DevBuf hp_big;                             // HP CTA-bin entries
   DevBuf ptw;                                // per-thread work lists (instrumented runs)
   DevBuf bm;                                 // BS frontier bitmaps (two lists)
+  DevBuf ep_dn[2];                           // EP carried source levels (unweighted cluster loop)
   // every buffer above (glb_graph_destroy frees them all)
   template <class F>
   void each(F f) {
     for (DevBuf* b : {&dist, &stamp, &q[0], &q[1], &q[2], &q[3], &wd_items[0], &wd_items[1],
                       &wd_tiles[0], &wd_tiles[1], &scan_flags, &scan_vals, &stats, &ctrl, &ns_row,
                       &ns_col, &ns_w, &ns_parent, &ns_cs, &ns_tmp, &ep_src, &eq[0], &eq[1], &out64,
-                      &recs, &misc, &hist, &tile_node, &misc_small, &shard_tmp, &hp_big, &ptw, &bm})
+                      &recs, &misc, &hist, &tile_node, &misc_small, &shard_tmp, &hp_big, &ptw, &bm,
+                      &ep_dn[0], &ep_dn[1]})
       f(*b);
   }
 };
-static_assert(sizeof(Workspace) == 33 * sizeof(DevBuf), "Workspace::each must list every buffer");
+static_assert(sizeof(Workspace) == 35 * sizeof(DevBuf), "Workspace::each must list every buffer");
 
 }  // namespace glb
 

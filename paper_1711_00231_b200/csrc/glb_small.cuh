@@ -385,14 +385,32 @@ __global__ void __cluster_dims__(CTAS, 1, 1) __launch_bounds__(kSmallThreads, 1)
       // ---- EP (edge_based.py:70-87): thread per worklist edge; an improved
       //      destination appends its whole out-edge range with one
       //      reservation (work chunking) or one per edge
+      // Unweighted graphs: every source of a listed edge was pushed with its
+      // final level (all candidates of a level-synchronous step are equal),
+      // so the level travels with the edge (ep_dn, written at push time) and
+      // the walk goes edge -> column -> atomic, without the src / dist loads
+      // and the pre-check (two dependent round trips less per level).  Lists
+      // this launch did not write (iteration 0) load the level.
+      const bool carry = !W && sc.ep_dn[0] != nullptr;
+      const uint32_t* dn_in = carry && it > 0 ? sc.ep_dn[sc.in] : nullptr;
+      uint32_t* dn_out = carry ? sc.ep_dn[sc.out] + sc.qcount[sc.out] : nullptr;
       for (unsigned i = gt; i < n; i += kSmallAll) {
         const uint32_t e = __ldcg(qin + i);
-        const uint32_t u = __ldg(ep_src + e);
-        const uint32_t v = __ldg(rx.col + e);
-        const uint32_t w = W ? __ldg(rx.wt + e) : 1u;
+        uint32_t v, w = 1u;
+        D du, dv;
+        if (dn_in) {
+          const uint32_t dc = __ldcg(dn_in + i);
+          v = __ldg(rx.col + e);
+          du = (D)dc;
+          dv = DistTraits<D>::kInf;
+        } else {
+          const uint32_t u = __ldg(ep_src + e);
+          v = __ldg(rx.col + e);
+          if (W) w = __ldg(rx.wt + e);
+          du = dist_cg<D>(rx.cells, u);
+          dv = dist_cg<D>(rx.cells, v);  // in flight with du
+        }
         ++c.work;
-        const D du = dist_cg<D>(rx.cells, u);
-        const D dv = dist_cg<D>(rx.cells, v);  // in flight with du
         if (du == DistTraits<D>::kInf) continue;
         ++c.relax;
         D cand;
@@ -409,10 +427,14 @@ __global__ void __cluster_dims__(CTAS, 1, 1) __launch_bounds__(kSmallThreads, 1)
           ++c.push;
           const unsigned b = atomicAdd(cursor, len);
           for (unsigned j = 0; j < len; ++j) qout[b + j] = (uint32_t)(lo + j);
+          if (dn_out)
+            for (unsigned j = 0; j < len; ++j) dn_out[b + j] = (uint32_t)cand;
         } else {
           for (unsigned j = 0; j < len; ++j) {
             ++c.push;
-            qout[atomicAdd(cursor, 1u)] = (uint32_t)(lo + j);
+            const unsigned b = atomicAdd(cursor, 1u);
+            qout[b] = (uint32_t)(lo + j);
+            if (dn_out) dn_out[b] = (uint32_t)cand;
           }
         }
       }

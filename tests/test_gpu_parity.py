@@ -49,7 +49,10 @@ VARIANTS = {"default": {}, "grid_kernels": {"GLB_NO_SMALL": "1"},
             "grid_bm_off": {"GLB_NO_SMALL": "1", "GLB_BM_THR": "0"},
             # cluster loop at the other size than the strategy's default (8 / 16 CTAs)
             "cluster8": {"GLB_SMALL_CTAS": "8"},
-            "cluster16": {"GLB_SMALL_CTAS": "16"}}
+            "cluster16": {"GLB_SMALL_CTAS": "16"},
+            # EP in the cluster loop with / without carried source levels (default: low-degree graphs only)
+            "ep_no_carry": {"GLB_EP_CARRY": "0"},
+            "ep_carry": {"GLB_EP_CARRY": "1"}}
 
 
 @pytest.mark.parametrize("variant", list(VARIANTS))
