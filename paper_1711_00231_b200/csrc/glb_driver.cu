@@ -307,13 +307,15 @@ class Runner {
                           g_->num_sms);
     }
     // Cluster loop size: 16 CTAs (non-portable) for EP / HP -- C3 BFS EP
-    // 58.8 -> 52.6 ms, C2 SSSP / BFS HP -2 / -3 % -- and 8 for BS / NS / WD
-    // (16: C3 SSSP BS +2.4 %; WD C3 BFS -10 % but C2 BFS +2.7 %, SSSP +0.8 %);
-    // GLB_SMALL_CTAS=8|16 overrides.  16 needs the GPU to co-schedule a
-    // 16-CTA cluster; otherwise 8.
+    // 58.8 -> 52.6 ms, C2 SSSP / BFS HP -2 / -3 % -- and for WD on graphs of
+    // average out-degree <= 8 (C3 BFS WD 94.3 -> 85.0, SSSP 482 -> 461; on
+    // R-MAT C2 BFS WD +2.7 %, so 8 there); 8 for BS / NS (C3 SSSP BS +2.4 %
+    // at 16).  GLB_SMALL_CTAS=8|16 overrides.  16 needs the GPU to
+    // co-schedule a 16-CTA cluster; otherwise 8.
     {
       const char* e = getenv("GLB_SMALL_CTAS");
-      int want = e ? atoi(e) : (p_.strategy == GLB_EP || p_.strategy == GLB_HP ? 16 : kSmallCtas);
+      const bool wd16 = p_.strategy == GLB_WD && g_->m <= 8 * g_->n;
+      int want = e ? atoi(e) : (p_.strategy == GLB_EP || p_.strategy == GLB_HP || wd16 ? 16 : kSmallCtas);
       if (want != 16) want = 8;
       GLB_CUDA_TRY(cudaFuncSetAttribute((const void*)k_small_loop<D, W, 8>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
